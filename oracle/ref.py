@@ -1,0 +1,188 @@
+"""ctypes binding of oracle/_ref/libskref.so -- the UNMODIFIED reference core.
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, ``__graft_entry__.smoke()`` and
+``bench.py``'s CPU legs may import this module; it is the checker and the CPU
+baseline, never the measured or shipped path.
+
+The library is built by ``oracle/Makefile`` from /root/reference/proj/src
+(compiled in place) + ``oracle/fft_shim.c`` (FFTW-API restatement) +
+``oracle/sk_oracle.cpp`` (C driver).  On the GPU box the prebuilt .so is used.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_ref" / "libskref.so"
+_lib = None
+
+SOLVER_VARS = {"ns2d": 1, "ns3d": 3}
+
+
+class RefError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def available() -> bool:
+    return LIB_PATH.exists()
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FileNotFoundError(f"{LIB_PATH} missing: run `make -C oracle`")
+        L = C.CDLL(str(LIB_PATH))
+        dp = C.POINTER(C.c_double)
+        ip = C.POINTER(C.c_int)
+        L.skref_last_error.restype = C.c_char_p
+        L.skref_set_workers.argtypes = [C.c_int]
+        L.skref_create.argtypes = [C.POINTER(C.c_void_p), C.c_char_p, C.c_int, ip,
+                                   C.c_double, C.c_double, C.c_int, C.c_double]
+        L.skref_destroy.argtypes = [C.c_void_p]
+        for f in ("skref_spect_size", "skref_phys_size", "skref_iteration"):
+            getattr(L, f).argtypes = [C.c_void_p]
+            getattr(L, f).restype = C.c_long
+        L.skref_nvars.argtypes = [C.c_void_p]
+        for f in ("skref_energy", "skref_enstrophy", "skref_time"):
+            getattr(L, f).argtypes = [C.c_void_p]
+            getattr(L, f).restype = C.c_double
+        L.skref_set_state.argtypes = [C.c_void_p, dp]
+        L.skref_get_state.argtypes = [C.c_void_p, dp]
+        L.skref_step.argtypes = [C.c_void_p, C.c_long, dp]
+        L.skref_run.argtypes = [C.c_void_p, C.c_long, dp]
+        L.skref_tendency.argtypes = [C.c_void_p, dp, dp]
+        L.skref_grid.argtypes = [C.c_void_p, C.c_int, dp, C.POINTER(C.c_ubyte)]
+        L.skref_last_divergence.argtypes = [C.c_void_p, C.POINTER(C.c_long), ip]
+        L.skref_fft_forward.argtypes = [C.c_int, ip, dp, dp]
+        L.skref_fft_inverse.argtypes = [C.c_int, ip, dp, dp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise RefError(rc, lib().skref_last_error().decode())
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def set_workers(n: int) -> None:
+    """set_fft_workers (proj/src/fft.cpp:51-54); capped by SPECTRALKIT_NUM_THREADS."""
+    lib().skref_set_workers(int(n))
+
+
+def fft_forward(u: np.ndarray) -> np.ndarray:
+    """FftPlan::forward (proj/src/fft.cpp:92-98): r2c then *= 1/N."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    shape = (C.c_int * u.ndim)(*u.shape)
+    out = np.empty(u.shape[:-1] + (u.shape[-1] // 2 + 1,), np.complex128)
+    _check(lib().skref_fft_forward(u.ndim, shape, _dp(u), _dp(out.view(np.float64))))
+    return out
+
+
+def fft_inverse(uhat: np.ndarray, shape) -> np.ndarray:
+    """FftPlan::inverse (proj/src/fft.cpp:100-106): unnormalised c2r, input kept."""
+    uhat = np.ascontiguousarray(uhat, dtype=np.complex128)
+    cs = (C.c_int * len(shape))(*shape)
+    out = np.empty(tuple(shape), np.float64)
+    _check(lib().skref_fft_inverse(len(shape), cs, _dp(uhat.view(np.float64)), _dp(out)))
+    return out
+
+
+class RefSimulation:
+    """A reference ``Simulation`` (proj/src/simulation.cpp:297-346) with files
+    and forcing off, fixed dt and an injected spectral state."""
+
+    def __init__(self, solver: str, n, nu: float, dt: float, scheme: str = "RK4",
+                 dealias_coef: float = 2.0 / 3.0):
+        self.solver = solver
+        self.n = tuple(int(x) for x in n)
+        h = C.c_void_p()
+        cn = (C.c_int * len(self.n))(*self.n)
+        _check(lib().skref_create(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
+                                  float(dt), 1 if scheme.upper() == "RK2" else 0,
+                                  float(dealias_coef)))
+        self._h = h
+        self.nvars = lib().skref_nvars(h)
+        self.spect_shape = self.n[:-1] + (self.n[-1] // 2 + 1,)
+
+    def close(self):
+        if self._h:
+            lib().skref_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_state(self, s: np.ndarray) -> None:
+        s = np.ascontiguousarray(s, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)
+        _check(lib().skref_set_state(self._h, _dp(s.view(np.float64))))
+
+    def get_state(self) -> np.ndarray:
+        out = np.empty((self.nvars,) + self.spect_shape, np.complex128)
+        _check(lib().skref_get_state(self._h, _dp(out.view(np.float64))))
+        return out
+
+    def step(self, nsteps: int = 1) -> float:
+        """step_once x nsteps (simulation.cpp:535-555); returns wall seconds."""
+        sec = C.c_double(0.0)
+        _check(lib().skref_step(self._h, int(nsteps), C.byref(sec)))
+        return sec.value
+
+    def run(self, nsteps: int) -> float:
+        """Simulation::run with n_iters = nsteps (simulation.cpp:565-590)."""
+        sec = C.c_double(0.0)
+        _check(lib().skref_run(self._h, int(nsteps), C.byref(sec)))
+        return sec.value
+
+    def tendency(self, s: np.ndarray) -> np.ndarray:
+        """Solver::tendency via Simulation::compute_tendency (simulation.cpp:478-480)."""
+        s = np.ascontiguousarray(s, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)
+        out = np.empty_like(s)
+        _check(lib().skref_tendency(self._h, _dp(s.view(np.float64)), _dp(out.view(np.float64))))
+        return out
+
+    def grid(self):
+        """(k_axis list, dealias mask) from make_grid (proj/src/grid.cpp:20-110)."""
+        ks = []
+        mask = np.empty(self.spect_shape, np.uint8)
+        for ax in range(len(self.n)):
+            k = np.empty(self.spect_shape[ax], np.float64)
+            _check(lib().skref_grid(self._h, ax, _dp(k),
+                                    mask.ctypes.data_as(C.POINTER(C.c_ubyte))))
+            ks.append(k)
+        return ks, mask
+
+    def last_divergence(self):
+        it = C.c_long(-1)
+        var = C.c_int(-1)
+        lib().skref_last_divergence(self._h, C.byref(it), C.byref(var))
+        return it.value, var.value
+
+    @property
+    def energy(self) -> float:
+        return lib().skref_energy(self._h)
+
+    @property
+    def enstrophy(self) -> float:
+        return lib().skref_enstrophy(self._h)
+
+    @property
+    def t(self) -> float:
+        return lib().skref_time(self._h)
+
+    @property
+    def iteration(self) -> int:
+        return lib().skref_iteration(self._h)
