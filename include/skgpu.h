@@ -1,0 +1,138 @@
+/*
+ * skgpu.h -- C ABI of the B200-native pseudo-spectral Navier-Stokes step.
+ *
+ * Drop-in boundary for the reference's hot path (spectralkit, mounted at
+ * /root/reference; paths below are relative to /root/reference/proj).
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams are passed as void*).  Host pointers are borrowed for the
+ * duration of a call (copy-in / copy-out); *_device variants take device
+ * pointers for zero-copy use.  Spectral arrays use the reference layout:
+ * per variable, row-major over (n0, ..., n_{d-1}/2+1), complex128
+ * interleaved (re, im) -- include/spectralkit/grid.hpp:18-25,
+ * include/spectralkit/state.hpp (StateSet spectral storage).
+ *
+ * Status codes mirror include/spectralkit/errors.hpp:
+ *   SKG_ECONFIG     <- ConfigError / ParamError   (bad extents, nu < 0, dt <= 0)
+ *   SKG_ESHAPE      <- ShapeError                 (size mismatch, bad axis)
+ *   SKG_EDIVERGENCE <- DivergenceError(iteration, field)  (simulation.cpp:557-563)
+ *   SKG_ECUDA       CUDA runtime failure (no reference equivalent)
+ *   SKG_EUNSUPPORTED extent outside what the sm_100a kernels implement
+ * One context per host thread, as the reference allows one thread per
+ * Simulation.  skg_last_error() is thread-local.
+ */
+#ifndef SKGPU_H
+#define SKGPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKG_OK 0
+#define SKG_ECONFIG 1
+#define SKG_ESHAPE 2
+#define SKG_EDIVERGENCE 3
+#define SKG_ECUDA 4
+#define SKG_ENCCL 5
+#define SKG_EUNSUPPORTED 6
+
+#define SKG_RK4 0 /* Scheme::RK4, include/spectralkit/time_stepping.hpp:14 */
+#define SKG_RK2 1 /* Scheme::RK2 */
+
+typedef struct skg_ctx skg_ctx;
+
+/* Version string of the library ("skgpu <semver> sm_100a"). */
+const char* skg_version(void);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* skg_last_error(void);
+
+/*
+ * Create a solver context on one device.
+ *   solver: "ns2d" (vorticity form, 1 variable "rot") or "ns3d" (rotational
+ *           form, 3 variables vx, vy, vz) -- replaces resolve_solver +
+ *           Solver factory (simulation.cpp:33-70, solvers.cpp:398-427).
+ *   dims/n/L: grid extents and box lengths -- replaces make_grid
+ *           (grid.cpp:20-110); L == NULL means 2*pi on every axis.
+ *   dealias_coef: 2/3 in every BASELINE config (simulation.cpp:91).
+ *   nu:     nu_2; sigma = -nu |k|^2 (Solver::linear_coef, simulation.cpp:147-157);
+ *           nu == 0 selects the "no linear part" RK branch (time_stepping.cpp:177-185).
+ *   scheme: SKG_RK4 or SKG_RK2 (ExactLinStepper, time_stepping.cpp:72-194).
+ *   device: CUDA ordinal.
+ * The state starts at zero, like init_fields.type = "constant" with value 0.
+ */
+int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+               double dealias_coef, double nu, int scheme, int device);
+int skg_destroy(skg_ctx* ctx);
+
+/* Launch all work on this CUDA stream (cudaStream_t passed as void*);
+ * NULL restores the context's own stream. */
+int skg_set_stream(skg_ctx* ctx, void* stream);
+
+/* Sizes: spectral modes per variable (S), physical points (P), variables. */
+long skg_spect_size(const skg_ctx* ctx);
+long skg_phys_size(const skg_ctx* ctx);
+int skg_nvars(const skg_ctx* ctx);
+
+/* State I/O, reference layout, nvars * S complex128 -- replaces
+ * StateSet::spect()/spect_mut() (state.hpp).  set_state also decides whether
+ * the dealiased fast path applies (every masked-out mode exactly zero). */
+int skg_set_state(skg_ctx* ctx, const double* spect);
+int skg_get_state(skg_ctx* ctx, double* spect_out);
+int skg_set_state_device(skg_ctx* ctx, const double* d_spect);
+int skg_get_state_device(skg_ctx* ctx, double* d_spect_out);
+
+/* nsteps x Simulation::step_once with fixed dt, forcing off
+ * (simulation.cpp:535-555): integrating-factor RK4/RK2 with the nonlinear
+ * tendency of the solver, check_finite after every step.  Blocking; returns
+ * SKG_EDIVERGENCE with the state frozen after the first non-finite step
+ * (see skg_last_divergence). */
+int skg_step(skg_ctx* ctx, double dt, long nsteps);
+/* Same, enqueued on the context stream without waiting; skg_sync() waits
+ * and reports divergence. */
+int skg_step_async(skg_ctx* ctx, double dt, long nsteps);
+int skg_sync(skg_ctx* ctx);
+
+/* Iteration count and time, as Simulation::iteration()/t(). */
+long skg_iteration(const skg_ctx* ctx);
+double skg_time(const skg_ctx* ctx);
+
+/* == Solver::tendency (solvers.cpp:133-174 ns2d, 299-339 ns3d) on an
+ * arbitrary stage state (dealiased output, mean mode 0).  Host buffers,
+ * nvars * S complex128 each. */
+int skg_tendency(skg_ctx* ctx, const double* in, double* out);
+
+/* == FftPlan::forward (fft.cpp:92-98: r2c then *= 1/N) and FftPlan::inverse
+ * (fft.cpp:100-106: unnormalised c2r, input untouched) on the context grid.
+ * u: P doubles; uhat: S complex128. */
+int skg_fft_forward(skg_ctx* ctx, const double* u, double* uhat);
+int skg_fft_inverse(skg_ctx* ctx, const double* uhat, double* u);
+
+/* Stateless transform operators for any shape (rank 1..3, even extents >= 4,
+ * as plan_fft checks in fft.cpp:34-44): FftPlan::forward / inverse. */
+int skg_plan_forward(int rank, const int* shape, const double* u, double* uhat, int device);
+int skg_plan_inverse(int rank, const int* shape, const double* uhat, double* u, int device);
+
+/* Wavenumbers and dealias mask computed ON THE DEVICE from indices, copied
+ * back for a bit-exact comparison with make_grid (grid.cpp:49-100).
+ * k_axis: spect_shape[axis] doubles; mask: S bytes or NULL. */
+int skg_get_grid(skg_ctx* ctx, int axis, double* k_axis, unsigned char* mask);
+
+/* Divergence report of the last failing step: iteration (as
+ * DivergenceError::iteration) and variable index (keys_state_spect order). */
+int skg_last_divergence(const skg_ctx* ctx, long* iteration, int* var);
+
+/* Energy / enstrophy of the current state (Simulation::energy/enstrophy,
+ * simulation.cpp:592-615), reduced on the device. */
+int skg_energy(skg_ctx* ctx, double* energy, double* enstrophy);
+
+/* 1 if the dealiased (pruned) fast path is active for the current state. */
+int skg_pruned(const skg_ctx* ctx);
+
+/* Number of kernel launches issued since the context was created. */
+long skg_launch_count(const skg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -78,7 +78,7 @@ def forward(u):
 
 def inverse(uhat, shape):
     """FftPlan::inverse, src/fft.cpp:100-106: unnormalised c2r."""
-    return np.fft.irfftn(uhat, s=tuple(shape), norm="forward")
+    return np.fft.irfftn(uhat, s=tuple(shape), axes=tuple(range(len(shape))), norm="forward")
 
 
 # ------------------------------------------------------------- tendencies

@@ -1,0 +1,325 @@
+"""Host mirror of the reference interface over the C ABI (include/skgpu.h).
+
+Names and semantics follow spectralkit (paths relative to
+/root/reference/proj):
+  Simulation.step_once / run / compute_tendency / energy / enstrophy
+      -> simulation.hpp:127-151 (fixed dt, forcing and files off)
+  Simulation.state (spectral, reference layout)  -> state.hpp (StateSet)
+  fft_forward / fft_inverse                       -> FftPlan::forward / inverse (fft.cpp:92-106)
+  exceptions                                      -> errors.hpp (ConfigError, ShapeError,
+                                                     DivergenceError(iteration, field))
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+_LIB_PATH = _PKG / "_lib" / "libskgpu.so"
+_lib = None
+
+SKG_OK, SKG_ECONFIG, SKG_ESHAPE, SKG_EDIVERGENCE, SKG_ECUDA, SKG_ENCCL, SKG_EUNSUPPORTED = range(7)
+SKG_RK4, SKG_RK2 = 0, 1
+
+KEYS_STATE_SPECT = {"ns2d": ["rot_fft"], "ns3d": ["vx_fft", "vy_fft", "vz_fft"]}
+
+EXPORTS = [
+    "skg_version", "skg_last_error", "skg_create", "skg_destroy", "skg_set_stream",
+    "skg_spect_size", "skg_phys_size", "skg_nvars", "skg_set_state", "skg_get_state",
+    "skg_set_state_device", "skg_get_state_device", "skg_step", "skg_step_async", "skg_sync",
+    "skg_iteration", "skg_time", "skg_tendency", "skg_fft_forward", "skg_fft_inverse",
+    "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
+    "skg_energy", "skg_pruned", "skg_launch_count",
+]
+
+
+class SkgError(RuntimeError):
+    """Base class (spectralkit::Error)."""
+
+
+class ConfigError(SkgError):
+    pass
+
+
+class ShapeError(SkgError):
+    pass
+
+
+class CudaError(SkgError):
+    pass
+
+
+class UnsupportedError(SkgError):
+    pass
+
+
+class DivergenceError(SkgError):
+    """Non-finite state after a step (errors.hpp:44-51)."""
+
+    def __init__(self, msg: str, iteration: int, field: str):
+        super().__init__(msg)
+        self.iteration = iteration
+        self.field = field
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load the sm_100a library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        raise SkgError(f"{_LIB_PATH} is missing: run `python -m paper_1807_01769_b200.build`")
+    L = C.CDLL(str(_LIB_PATH))
+    vp, dp, ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)
+    L.skg_version.restype = C.c_char_p
+    L.skg_last_error.restype = C.c_char_p
+    L.skg_create.argtypes = [C.POINTER(vp), C.c_char_p, C.c_int, ip, dp, C.c_double, C.c_double,
+                             C.c_int, C.c_int]
+    L.skg_destroy.argtypes = [vp]
+    L.skg_set_stream.argtypes = [vp, vp]
+    for f in ("skg_spect_size", "skg_phys_size", "skg_iteration", "skg_launch_count"):
+        getattr(L, f).argtypes = [vp]
+        getattr(L, f).restype = C.c_long
+    for f in ("skg_nvars", "skg_pruned"):
+        getattr(L, f).argtypes = [vp]
+    L.skg_time.argtypes = [vp]
+    L.skg_time.restype = C.c_double
+    for f in ("skg_set_state", "skg_get_state", "skg_set_state_device", "skg_get_state_device"):
+        getattr(L, f).argtypes = [vp, C.c_void_p]
+    L.skg_step.argtypes = [vp, C.c_double, C.c_long]
+    L.skg_step_async.argtypes = [vp, C.c_double, C.c_long]
+    L.skg_sync.argtypes = [vp]
+    L.skg_tendency.argtypes = [vp, C.c_void_p, C.c_void_p]
+    L.skg_fft_forward.argtypes = [vp, C.c_void_p, C.c_void_p]
+    L.skg_fft_inverse.argtypes = [vp, C.c_void_p, C.c_void_p]
+    L.skg_plan_forward.argtypes = [C.c_int, ip, C.c_void_p, C.c_void_p, C.c_int]
+    L.skg_plan_inverse.argtypes = [C.c_int, ip, C.c_void_p, C.c_void_p, C.c_int]
+    L.skg_get_grid.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p]
+    L.skg_last_divergence.argtypes = [vp, C.POINTER(C.c_long), ip]
+    L.skg_energy.argtypes = [vp, dp, dp]
+    _lib = L
+    return L
+
+
+def _raise(rc: int, ctx=None, solver=None):
+    L = load_library()
+    msg = L.skg_last_error().decode()
+    if rc == SKG_ECONFIG:
+        raise ConfigError(msg)
+    if rc == SKG_ESHAPE:
+        raise ShapeError(msg)
+    if rc == SKG_EDIVERGENCE:
+        it = C.c_long(-1)
+        var = C.c_int(-1)
+        L.skg_last_divergence(ctx, C.byref(it), C.byref(var))
+        keys = KEYS_STATE_SPECT.get(solver, ["?"])
+        field = keys[var.value] if 0 <= var.value < len(keys) else "?"
+        raise DivergenceError(msg, it.value, field)
+    if rc == SKG_EUNSUPPORTED:
+        raise UnsupportedError(msg)
+    if rc == SKG_ECUDA:
+        raise CudaError(msg)
+    raise SkgError(f"[{rc}] {msg}")
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _check_shape(shape):
+    shape = tuple(int(x) for x in shape)
+    if not 1 <= len(shape) <= 3:
+        raise ShapeError(f"transform rank must be 1..3, got {len(shape)}")
+    for n in shape:
+        if n < 4:
+            raise ShapeError(f"extent {n} too small (min 4)")
+        if n % 2:
+            raise ShapeError(f"extent {n} is odd")
+    return shape
+
+
+def fft_forward(u: np.ndarray, device: int = 0) -> np.ndarray:
+    """FftPlan::forward (fft.cpp:92-98) of a real field on the GPU."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    shape = _check_shape(u.shape)
+    out = np.empty(shape[:-1] + (shape[-1] // 2 + 1,), np.complex128)
+    cs = (C.c_int * len(shape))(*shape)
+    rc = load_library().skg_plan_forward(len(shape), cs, _ptr(u), _ptr(out), device)
+    if rc:
+        _raise(rc)
+    return out
+
+
+def fft_inverse(uhat: np.ndarray, shape, device: int = 0) -> np.ndarray:
+    """FftPlan::inverse (fft.cpp:100-106): unnormalised c2r, input intact."""
+    shape = _check_shape(shape)
+    uhat = np.ascontiguousarray(uhat, dtype=np.complex128)
+    if uhat.shape != shape[:-1] + (shape[-1] // 2 + 1,):
+        raise ShapeError(f"inverse: field has shape {uhat.shape}, plan expects "
+                         f"{shape[:-1] + (shape[-1] // 2 + 1,)}")
+    out = np.empty(shape, np.float64)
+    cs = (C.c_int * len(shape))(*shape)
+    rc = load_library().skg_plan_inverse(len(shape), cs, _ptr(uhat), _ptr(out), device)
+    if rc:
+        _raise(rc)
+    return out
+
+
+class Simulation:
+    """Device-resident counterpart of spectralkit::Simulation for ns2d/ns3d
+    with fixed dt and forcing/output off (the bench protocol, bench.cpp:51-85)."""
+
+    def __init__(self, solver: str, n, nu: float = 0.0, dt: float = 0.0, scheme: str = "RK4",
+                 L=None, dealias_coef: float = 2.0 / 3.0, device: int = 0):
+        L_ = load_library()
+        self.solver = solver
+        self.n = tuple(int(x) for x in n)
+        self.dims = len(self.n)
+        self.nu = float(nu)
+        self.dt = float(dt)
+        self.scheme = scheme.upper()
+        if self.scheme not in ("RK4", "RK2"):
+            raise ConfigError(f"unknown time scheme '{scheme}' (use RK2 or RK4)")
+        self.spect_shape = self.n[:-1] + (self.n[-1] // 2 + 1,)
+        h = C.c_void_p()
+        cn = (C.c_int * self.dims)(*self.n)
+        cL = None if L is None else (C.c_double * self.dims)(*L)
+        rc = L_.skg_create(C.byref(h), solver.encode(), self.dims, cn, cL, float(dealias_coef),
+                           self.nu, SKG_RK2 if self.scheme == "RK2" else SKG_RK4, int(device))
+        if rc:
+            _raise(rc)
+        self._h = h
+        self.nvars = L_.skg_nvars(h)
+        self.keys_state_spect = KEYS_STATE_SPECT[solver]
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().skg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _call(self, fn, *args):
+        rc = getattr(load_library(), fn)(self._h, *args)
+        if rc:
+            _raise(rc, self._h, self.solver)
+
+    # ----------------------------------------------------------------- state
+    def set_state(self, spect: np.ndarray) -> None:
+        s = np.ascontiguousarray(spect, dtype=np.complex128)
+        if s.size != self.nvars * int(np.prod(self.spect_shape)):
+            raise ShapeError(f"state has {s.size} modes, expected "
+                             f"{self.nvars} x {self.spect_shape}")
+        self._call("skg_set_state", _ptr(s))
+
+    def get_state(self) -> np.ndarray:
+        out = np.empty((self.nvars,) + self.spect_shape, np.complex128)
+        self._call("skg_get_state", _ptr(out))
+        return out
+
+    def set_state_device(self, ptr: int) -> None:
+        self._call("skg_set_state_device", C.c_void_p(ptr))
+
+    def get_state_device(self, ptr: int) -> None:
+        self._call("skg_get_state_device", C.c_void_p(ptr))
+
+    def set_stream(self, stream_ptr) -> None:
+        self._call("skg_set_stream", C.c_void_p(stream_ptr))
+
+    # ---------------------------------------------------------------- stepping
+    def step_once(self, dt: float | None = None) -> None:
+        self.step(1, dt)
+
+    def step(self, nsteps: int, dt: float | None = None) -> None:
+        dt = self.dt if dt is None else float(dt)
+        self._call("skg_step", C.c_double(dt), C.c_long(int(nsteps)))
+
+    def step_async(self, nsteps: int, dt: float | None = None) -> None:
+        dt = self.dt if dt is None else float(dt)
+        self._call("skg_step_async", C.c_double(dt), C.c_long(int(nsteps)))
+
+    def sync(self) -> None:
+        self._call("skg_sync")
+
+    def run(self, n_iters: int) -> None:
+        """Simulation::run with n_iters (simulation.cpp:565-590)."""
+        self.step(n_iters)
+
+    def compute_tendency(self, spect: np.ndarray) -> np.ndarray:
+        s = np.ascontiguousarray(spect, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)
+        out = np.empty_like(s)
+        self._call("skg_tendency", _ptr(s), _ptr(out))
+        return out
+
+    # ----------------------------------------------------------- operators
+    def fft_forward(self, u: np.ndarray) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.shape != self.n:
+            raise ShapeError(f"forward: field has shape {u.shape}, grid is {self.n}")
+        out = np.empty(self.spect_shape, np.complex128)
+        self._call("skg_fft_forward", _ptr(u), _ptr(out))
+        return out
+
+    def fft_inverse(self, uhat: np.ndarray) -> np.ndarray:
+        uhat = np.ascontiguousarray(uhat, dtype=np.complex128)
+        if uhat.shape != self.spect_shape:
+            raise ShapeError(f"inverse: field has shape {uhat.shape}, grid is {self.spect_shape}")
+        out = np.empty(self.n, np.float64)
+        self._call("skg_fft_inverse", _ptr(uhat), _ptr(out))
+        return out
+
+    def grid(self):
+        """(k_axis per axis, uint8 dealias mask) computed on the device."""
+        ks = []
+        mask = np.empty(self.spect_shape, np.uint8)
+        for ax in range(self.dims):
+            k = np.empty(self.spect_shape[ax], np.float64)
+            self._call("skg_get_grid", C.c_int(ax), _ptr(k), _ptr(mask) if ax == 0 else None)
+            ks.append(k)
+        return ks, mask
+
+    # -------------------------------------------------------------- queries
+    @property
+    def iteration(self) -> int:
+        return load_library().skg_iteration(self._h)
+
+    @property
+    def t(self) -> float:
+        return load_library().skg_time(self._h)
+
+    @property
+    def pruned(self) -> bool:
+        return bool(load_library().skg_pruned(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return load_library().skg_launch_count(self._h)
+
+    def energy_enstrophy(self):
+        e = C.c_double()
+        z = C.c_double()
+        self._call("skg_energy", C.byref(e), C.byref(z))
+        return e.value, z.value
+
+    def energy(self) -> float:
+        return self.energy_enstrophy()[0]
+
+    def enstrophy(self) -> float:
+        return self.energy_enstrophy()[1]

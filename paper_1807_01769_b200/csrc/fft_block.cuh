@@ -1,0 +1,229 @@
+// fft_block.cuh -- register-resident FP64 Stockham FFT for one line per
+// thread group, exchanging through shared memory between radix passes.
+//
+// Replaces the FFTW execution behind FftPlan (reference proj/src/fft.cpp:92-106)
+// on the hot path.  Layout contract ("natural"): a line of N complex values is
+// held by T = N/E threads, thread t owning elements t + T*e, e in [0, E).
+// Every pass reads natural order from registers, and the last pass leaves the
+// result in natural order in registers, so the caller loads inputs and stores
+// outputs fully coalesced and fuses its prologue/epilogue arithmetic there.
+//
+// Pass p (radix R, Ns = product of earlier radices), butterfly j in [0, N/R):
+//   u[r] = x[j + r N/R] * W_{Ns R}^{(j mod Ns) r}      (skip when Ns == 1)
+//   u    = DFT_R(u)
+//   y[(j / Ns) Ns R + (j mod Ns) + r Ns] = u[r]          (to smem, autosort)
+// Radix 16 (4x4 in registers) until the remainder is < 16, then 2/4/8, so a
+// 4096-point line costs 3 register passes and 2 shared-memory exchanges.
+// Twiddles W_N^m come from a per-length table built on the host in extended
+// precision (forward sign; the inverse uses the conjugate).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace skg {
+
+typedef double2 cd;
+
+__device__ __forceinline__ cd mk(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ cd add(cd a, cd b) { return mk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cd sub(cd a, cd b) { return mk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cd mul(cd a, cd b) {
+    return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ cd mulconj(cd a, cd b) {  // a * conj(b)
+    return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ cd conj(cd a) { return mk(a.x, -a.y); }
+__device__ __forceinline__ cd scale(cd a, double s) { return mk(a.x * s, a.y * s); }
+__device__ __forceinline__ cd muli(cd a) { return mk(-a.y, a.x); }   // i * a
+__device__ __forceinline__ cd mulmi(cd a) { return mk(a.y, -a.x); }  // -i * a
+__device__ __forceinline__ cd zero() { return mk(0.0, 0.0); }
+
+// S = -1 forward (e^{-i}), S = +1 inverse (e^{+i}).
+template <int S>
+__device__ __forceinline__ cd rot90(cd a) {  // a * W_4^1 = a * (S i)
+    return S < 0 ? mulmi(a) : muli(a);
+}
+
+constexpr double kC8 = 0.70710678118654752440084436210484904;   // cos(pi/4)
+constexpr double kC16 = 0.92387953251128675612818318939678829;  // cos(pi/8)
+constexpr double kS16 = 0.38268343236508977172845837907404220;  // sin(pi/8)
+
+// a * W_R^M with W_R = e^{S 2 pi i / R}; constant-folded special cases.
+template <int S, int M, int R>
+__device__ __forceinline__ cd twc(cd a) {
+    constexpr int m = ((M % R) + R) % R;
+    if constexpr (m == 0) return a;
+    else if constexpr (4 * m == R) return rot90<S>(a);
+    else if constexpr (2 * m == R) return mk(-a.x, -a.y);
+    else if constexpr (4 * m == 3 * R) return rot90<-S>(a);
+    else if constexpr (8 * m == R) {  // (1 + S i)/sqrt2
+        return S < 0 ? mk((a.x + a.y) * kC8, (a.y - a.x) * kC8)
+                     : mk((a.x - a.y) * kC8, (a.y + a.x) * kC8);
+    } else if constexpr (8 * m == 3 * R) {  // (-1 + S i)/sqrt2
+        return S < 0 ? mk((a.y - a.x) * kC8, -(a.x + a.y) * kC8)
+                     : mk(-(a.x + a.y) * kC8, (a.x - a.y) * kC8);
+    } else if constexpr (8 * m == 5 * R) {  // (-1 - S i)/sqrt2
+        return S < 0 ? mk(-(a.x + a.y) * kC8, (a.x - a.y) * kC8)
+                     : mk((a.y - a.x) * kC8, -(a.x + a.y) * kC8);
+    } else if constexpr (8 * m == 7 * R) {  // (1 - S i)/sqrt2
+        return S < 0 ? mk((a.x - a.y) * kC8, (a.y + a.x) * kC8)
+                     : mk((a.x + a.y) * kC8, (a.y - a.x) * kC8);
+    } else {
+        static_assert(R == 16, "general twiddle only for radix 16");
+        // m in {1,3,5,7,9,11,13,15}: cos/sin of 2 pi m / 16
+        constexpr double c = (m == 1 || m == 15) ? kC16
+                             : (m == 3 || m == 13) ? kS16
+                             : (m == 5 || m == 11) ? -kS16
+                                                   : -kC16;
+        constexpr double s0 = (m == 1 || m == 7) ? kS16
+                              : (m == 3 || m == 5) ? kC16
+                              : (m == 9 || m == 15) ? -kS16
+                                                    : -kC16;
+        constexpr double s = S * s0;
+        return mk(a.x * c - a.y * s, a.x * s + a.y * c);
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void dft2(cd& a, cd& b) {
+    cd t = a;
+    a = add(t, b);
+    b = sub(t, b);
+}
+
+template <int S>
+__device__ __forceinline__ void dft4(cd& x0, cd& x1, cd& x2, cd& x3) {
+    cd a = add(x0, x2), b = sub(x0, x2), c = add(x1, x3), d = rot90<S>(sub(x1, x3));
+    x0 = add(a, c);
+    x2 = sub(a, c);
+    x1 = add(b, d);
+    x3 = sub(b, d);
+}
+
+// Natural order in, natural order out.
+template <int S>
+__device__ __forceinline__ void dft8(cd* x) {
+    // n = 2 n1 + n2 (n1 < 4, n2 < 2); k = k1 + 4 k2
+    dft4<S>(x[0], x[2], x[4], x[6]);
+    dft4<S>(x[1], x[3], x[5], x[7]);
+    // y[n2][k1] at x[2 k1 + n2]; twiddle W_8^{n2 k1}
+    x[3] = twc<S, 1, 8>(x[3]);
+    x[5] = twc<S, 2, 8>(x[5]);
+    x[7] = twc<S, 3, 8>(x[7]);
+    cd o[8];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        cd a = x[2 * k1], b = x[2 * k1 + 1];
+        o[k1] = add(a, b);
+        o[k1 + 4] = sub(a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = o[i];
+}
+
+template <int S>
+__device__ __forceinline__ void dft16(cd* x) {
+    // n = 4 n1 + n2, k = k1 + 4 k2
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<S>(x[n2], x[4 + n2], x[8 + n2], x[12 + n2]);
+    // y[n2][k1] stored at x[4 k1 + n2]; twiddle W_16^{n2 k1}
+    x[5] = twc<S, 1, 16>(x[5]);
+    x[6] = twc<S, 2, 16>(x[6]);
+    x[7] = twc<S, 3, 16>(x[7]);
+    x[9] = twc<S, 2, 16>(x[9]);
+    x[10] = twc<S, 4, 16>(x[10]);
+    x[11] = twc<S, 6, 16>(x[11]);
+    x[13] = twc<S, 3, 16>(x[13]);
+    x[14] = twc<S, 6, 16>(x[14]);
+    x[15] = twc<S, 9, 16>(x[15]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4<S>(x[4 * k1], x[4 * k1 + 1], x[4 * k1 + 2], x[4 * k1 + 3]);
+    // X[k1 + 4 k2] now at x[4 k1 + k2]
+    cd o[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) o[k1 + 4 * k2] = x[4 * k1 + k2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = o[i];
+}
+
+template <int R, int S>
+__device__ __forceinline__ void dft(cd* x) {
+    if constexpr (R == 1) {
+    } else if constexpr (R == 2) dft2<S>(x[0], x[1]);
+    else if constexpr (R == 4) dft4<S>(x[0], x[1], x[2], x[3]);
+    else if constexpr (R == 8) dft8<S>(x);
+    else if constexpr (R == 16) dft16<S>(x);
+    else static_assert(R == 16, "unsupported radix");
+}
+
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+
+// Block FFT of a power-of-two length N in natural layout.
+template <int N>
+struct BFFT {
+    static_assert((N & (N - 1)) == 0 && N >= 2, "power-of-two length");
+    static constexpr int E = N < 16 ? N : 16;  // elements per thread
+    static constexpr int T = N / E;            // threads per line
+    static constexpr int PADSH = ilog2c(E);    // one pad slot per E elements
+    static constexpr int SMEM = N + (N >> PADSH) + 1;  // cd slots per line
+    __device__ __forceinline__ static int pad(int i) { return i + (i >> PADSH); }
+
+    // One pass, then recurse.  tw: W_N^m table (forward sign).
+    template <int S, int Ns>
+    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const cd* __restrict__ tw) {
+        constexpr int rem = N / Ns;
+        constexpr int R = rem >= 16 ? 16 : rem;
+        constexpr int B = E / R;  // butterflies per thread in this pass
+        constexpr bool last = (Ns * R == N);
+        static_assert(E % R == 0, "radix must divide elements per thread");
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int j = t + T * b;
+            cd u[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) u[r] = v[b + r * B];
+            const int jm = j & (Ns - 1);
+            if constexpr (Ns > 1) {
+                constexpr int step = N / (Ns * R);
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    cd w = __ldg(&tw[jm * r * step]);
+                    u[r] = S < 0 ? mul(u[r], w) : mulconj(u[r], w);
+                }
+            }
+            dft<R, S>(u);
+            if constexpr (last) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[b + r * B] = u[r];
+            } else {
+                const int base = (j / Ns) * Ns * R + jm;
+#pragma unroll
+                for (int r = 0; r < R; ++r) sm[pad(base + r * Ns)] = u[r];
+            }
+        }
+        if constexpr (!last) {
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e)];
+            __syncthreads();
+            pass<S, Ns * R>(v, sm, t, tw);
+        }
+    }
+
+    template <int S>
+    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const cd* __restrict__ tw) {
+        pass<S, 1>(v, sm, t, tw);
+    }
+
+    // Number of __syncthreads() a run issues (callers with inactive lines
+    // must still participate).
+    static constexpr int passes() {
+        int p = 0;
+        for (int ns = 1; ns < N; ns *= (N / ns >= 16 ? 16 : N / ns)) ++p;
+        return p;
+    }
+};
+
+}  // namespace skg

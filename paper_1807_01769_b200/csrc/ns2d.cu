@@ -1,0 +1,374 @@
+// ns2d.cu -- fused RK stage of the 2D vorticity-form solver on sm_100a.
+//
+// One RK stage = three kernels (SURVEY.md 8(a) GPU mapping, ns2d):
+//   k1_xinv : x-inverse c2c on each ky column of the internal CM state
+//             ([ky][kx], columns contiguous).  Prologue recomputes the RK
+//             stage state from u and the previous k (time_stepping.cpp:
+//             128-170) and applies the x-multipliers of the four fields the
+//             product needs: psi = w/|k|^2, kx psi, kx w, w
+//             (velocity_from_vorticity2d grid.cpp:251-274, gradient_component
+//             grid.cpp:124-143).  Writes 4 intermediates [x][ky].
+//   k3_phys : y pass per pair of rows: two packed c2r (ux + i dx w,
+//             uy + i dy w; the ky factors i*ky are applied here), the product
+//             -(ux dx w + uy dy w) (solvers.cpp:160-164), one packed r2c of the
+//             two rows, *1/N, ky-dealias (only kept ky stored).
+//   k4_xfwd : x-forward c2c per kept ky column, kx-dealias, mean = 0
+//             (solvers.cpp:171-172), RK accumulate / final update
+//             (time_stepping.cpp:174-193) and the check_finite guard
+//             (simulation.cpp:557-563) in the epilogue.
+// "pruned": when the state is dealiased every masked-out mode is exactly zero
+// and stays zero, so masked columns/rows are never read or
+// written.  Otherwise every mode is processed, with identical results.
+#include <cstdio>
+
+#include "skg_internal.h"
+
+namespace skg {
+
+namespace {
+
+__device__ __forceinline__ bool finite2(cd v) { return isfinite(v.x) && isfinite(v.y); }
+
+// RK stage state at (kx index i, ky index j) from u and the previous k.
+__device__ __forceinline__ cd stage_input(const Ns2dArgs& a, int stage, int ky, int i,
+                                          size_t idx) {
+    cd u = a.u[idx];
+    if (stage <= 1) return u;
+    if (a.has_sigma) {
+        if (stage == 2) {
+            const double e1 = a.e1x[i] * a.e1y[ky];
+            cd k = a.k1[idx];
+            return scale(add(u, scale(k, a.hdt)), e1);
+        } else if (stage == 3) {
+            const double e1 = a.e1x[i] * a.e1y[ky];
+            cd k = a.k2[idx];
+            return add(scale(u, e1), scale(k, a.hdt));
+        } else {
+            const double e1 = a.e1x[i] * a.e1y[ky];
+            const double e2 = a.e2x[i] * a.e2y[ky];
+            cd k = a.k3[idx];
+            return add(scale(u, e2), scale(k, a.dt * e1));
+        }
+    } else {
+        if (stage == 2) return add(u, scale(a.k1[idx], a.hdt));
+        if (stage == 3) return add(u, scale(a.k2[idx], a.hdt));
+        return add(u, scale(a.k3[idx], a.dt));
+    }
+}
+
+template <int NX>
+__global__ void __launch_bounds__(256, 2) k1_xinv(Ns2dArgs a, int stage) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T, E = F::E;
+    constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x / T, t = threadIdx.x % T;
+    const int ky = blockIdx.x * LPC + l;
+    const bool active = ky < a.ky_in;
+    if (a.flags->diverged) return;
+    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.flags != nullptr)
+        atomicAdd(&a.flags->steps, 1);
+    cd* sm = smem + l * F::SMEM;
+    const double kyv = a.ky_scale * (double)ky;
+#pragma unroll 1
+    for (int m = 0; m < 4; ++m) {
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = t + T * e;
+            const int si = signed_index(i, NX);
+            const bool keep = active && (!a.pruned || abs(si) <= a.kcx);
+            cd s = zero();
+            if (keep) s = stage_input(a, stage, ky, i, (size_t)ky * NX + i);
+            const double kxv = a.kx_scale * (double)si;
+            cd r;
+            if (m == 0 || m == 1) {
+                const double ksq = kxv * kxv + kyv * kyv;
+                cd psi = ksq == 0.0 ? zero() : mk(s.x / ksq, s.y / ksq);
+                r = m == 0 ? psi : scale(psi, kxv);
+            } else {
+                r = m == 2 ? scale(s, kxv) : s;
+            }
+            v[e] = r;
+        }
+        F::template run<+1>(v, sm, t, a.twx);
+        if (active) {
+            cd* out = a.I[m];
+#pragma unroll
+            for (int e = 0; e < E; ++e) out[(size_t)(t + T * e) * a.ld_i + ky] = v[e];
+        }
+        if constexpr (F::T > 1) __syncthreads();  // sm reused by the next field
+    }
+}
+
+// -(ux dx w + uy dy w) of row x in natural layout (y = t + T e).
+template <int NY>
+__device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool active, cd* sm, int t,
+                                            double* acc) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T, E = F::E;
+    const size_t row = (size_t)x * a.ld_i;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+        const cd* P = a.I[q == 0 ? 0 : 1];  // X[psi] | X[kx psi]
+        const cd* Q = a.I[q == 0 ? 2 : 3];  // X[kx w] | X[w]
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int idx = t + T * e;
+            const bool mirror = idx > NY / 2;
+            const int ki = mirror ? NY - idx : idx;
+            cd ah = zero(), bh = zero();
+            if (active && ki < a.ky_in) {
+                const double kyv = a.ky_scale * (double)ki;
+                cd p = P[row + ki];
+                cd qq = Q[row + ki];
+                if (q == 0) {
+                    ah = mk(-kyv * p.y, kyv * p.x);   // ux: i ky X[psi]
+                    bh = muli(qq);                    // dx w: i X[kx w]
+                } else {
+                    ah = mulmi(p);                    // uy: -i X[kx psi]
+                    bh = mk(-kyv * qq.y, kyv * qq.x); // dy w: i ky X[w]
+                }
+                if (ki == 0 || 2 * ki == NY) {  // c2r ignores these imaginary parts
+                    ah.y = 0.0;
+                    bh.y = 0.0;
+                }
+            }
+            // packed spectrum of (a + i b) over the full ky range
+            v[e] = mirror ? mk(ah.x + bh.y, bh.x - ah.y) : mk(ah.x - bh.y, ah.y + bh.x);
+        }
+        F::template run<+1>(v, sm, t, a.twy);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double p = v[e].x * v[e].y;
+            acc[e] = q == 0 ? p : -(acc[e] + p);
+        }
+    }
+}
+
+template <int NY>
+__global__ void __launch_bounds__(256, 2) k3_phys(Ns2dArgs a) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T, E = F::E;
+    constexpr int G = T >= 256 ? 1 : 256 / T;
+    constexpr int SLOT = F::SMEM + NY / 2;  // exchange + one row of doubles
+    extern __shared__ cd smem[];
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const int xa = 2 * (blockIdx.x * G + g);
+    const bool active = xa < a.nx;
+    if (a.flags->diverged) return;
+    cd* sm = smem + g * SLOT;
+    double* prow = reinterpret_cast<double*>(sm + F::SMEM);
+    {
+        double acc[E];
+        row_product<NY>(a, xa, active, sm, t, acc);
+#pragma unroll
+        for (int e = 0; e < E; ++e) prow[t + T * e] = acc[e];
+    }
+    cd v[E];
+    {
+        double acc[E];
+        row_product<NY>(a, xa + 1, active, sm, t, acc);
+        // forward r2c of both rows packed: z = prod_a + i prod_b
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = mk(prow[t + T * e], acc[e]);
+    }
+    F::template run<-1>(v, sm, t, a.twy);
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+    __syncthreads();
+    if (active) {
+        const double h = 0.5 * a.inv_n;
+        cd* ra = a.nl + (size_t)xa * a.ld_o;
+        cd* rb = ra + a.ld_o;
+        for (int k = t; k < a.ld_o; k += T) {
+            cd zk = sm[F::pad(k)];
+            cd zm = sm[F::pad((NY - k) & (NY - 1))];
+            ra[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+            rb[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+        }
+    }
+}
+
+template <int NX>
+__global__ void __launch_bounds__(256, 2) k4_xfwd(Ns2dArgs a, int stage) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T, E = F::E;
+    constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x / T, t = threadIdx.x % T;
+    const int ky = blockIdx.x * LPC + l;
+    const bool active = ky < a.ld_o;
+    if (a.flags->diverged) return;
+    cd* sm = smem + l * F::SMEM;
+    cd v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        v[e] = active ? a.nl[(size_t)(t + T * e) * a.ld_o + ky] : zero();
+    F::template run<-1>(v, sm, t, a.twx);
+    if (!active) return;
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = t + T * e;
+        const int si = signed_index(i, NX);
+        bool keep = abs(si) <= a.kcx;
+        if (i == 0 && ky == 0) keep = false;  // mean mode of the tendency is 0
+        if (!keep && a.pruned) continue;
+        const cd kv = keep ? v[e] : zero();
+        const size_t idx = (size_t)ky * NX + i;
+        if (!final) {
+            kout[idx] = kv;
+        } else {
+            cd u = a.u[idx];
+            cd un;
+            if (a.has_sigma) {
+                const double e1 = a.e1x[i] * a.e1y[ky];
+                const double e2 = a.e2x[i] * a.e2y[ky];
+                if (a.rk2) {
+                    un = add(scale(u, e2), scale(kv, a.dt * e1));
+                } else {
+                    cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                    cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
+                    un = add(scale(u, e2), scale(sum, a.sdt));
+                }
+            } else {
+                cd delta;
+                if (a.rk2) {
+                    delta = scale(kv, a.dt);
+                } else {
+                    cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                }
+                un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
+            }
+            a.u[idx] = un;
+            bad |= !finite2(un);
+        }
+    }
+    if (bad) {
+        atomicMin(&a.flags->div_var, 0);
+        atomicExch(&a.flags->div_step, a.flags->steps);
+        atomicExch(&a.flags->diverged, 1);
+    }
+}
+
+// Unpruned final update of the ky columns above the cut: tendency is zero
+// there, so u <- E2 u (time_stepping.cpp:186-192 with k = 0).
+__global__ void k4_decay(Ns2dArgs a) {
+    if (a.flags->diverged) return;
+    const size_t cols = (size_t)(a.nh - (a.kcy + 1));
+    const size_t total = cols * a.nx;
+    bool bad = false;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int ky = a.kcy + 1 + (int)(q / a.nx);
+        const int i = (int)(q % a.nx);
+        const size_t idx = (size_t)ky * a.nx + i;
+        cd u = a.u[idx];
+        if (a.has_sigma) {
+            const double e2 = a.e2x[i] * a.e2y[ky];
+            u = scale(u, e2);
+            a.u[idx] = u;
+        }
+        bad |= !finite2(u);
+    }
+    if (bad) {
+        atomicMin(&a.flags->div_var, 0);
+        atomicExch(&a.flags->div_step, a.flags->steps);
+        atomicExch(&a.flags->diverged, 1);
+    }
+}
+
+template <int NX>
+cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T;
+    constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    const size_t smem = sizeof(cd) * F::SMEM * LPC;
+    const int cols = inverse ? a.ky_in : a.ld_o;
+    const int grid = (cols + LPC - 1) / LPC;
+    if (grid == 0) return cudaSuccess;
+    if (inverse) {
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(k1_xinv<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            init = true;
+        }
+        k1_xinv<NX><<<grid, T * LPC, smem, s>>>(a, stage);
+    } else {
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(k4_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            init = true;
+        }
+        k4_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
+    }
+    return cudaGetLastError();
+}
+
+template <int NY>
+cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T;
+    constexpr int G = T >= 256 ? 1 : 256 / T;
+    const size_t smem = sizeof(cd) * (F::SMEM + NY / 2) * G;
+    const int pairs = a.nx / 2;
+    const int grid = (pairs + G - 1) / G;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k3_phys<NY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = true;
+    }
+    k3_phys<NY><<<grid, T * G, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define SKG_POW2_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+
+cudaError_t dispatch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    switch (a.nx) {
+#define CASE(N) \
+    case N: return launch_x<N>(a, stage, inverse, s);
+        SKG_POW2_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t dispatch_y(const Ns2dArgs& a, cudaStream_t s) {
+    switch (a.ny) {
+#define CASE(N) \
+    case N: return launch_y<N>(a, s);
+        SKG_POW2_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+bool ns2d_supported(int nx, int ny) {
+    auto ok = [](int n) { return n >= 4 && n <= 8192 && (n & (n - 1)) == 0; };
+    return ok(nx) && ok(ny);
+}
+
+cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches) {
+    cudaError_t err;
+    if ((err = dispatch_x(a, stage, true, s)) != cudaSuccess) return err;
+    if ((err = dispatch_y(a, s)) != cudaSuccess) return err;
+    if ((err = dispatch_x(a, stage, false, s)) != cudaSuccess) return err;
+    *launches += 3;
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    if (final && !a.pruned && a.nh > a.kcy + 1) {
+        k4_decay<<<296, 256, 0, s>>>(a);
+        *launches += 1;
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace skg

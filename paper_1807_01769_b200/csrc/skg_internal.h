@@ -1,0 +1,114 @@
+// skg_internal.h -- shared host/device declarations of the skgpu library.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "fft_block.cuh"
+
+namespace skg {
+
+// Device flags shared by every kernel of a context (one allocation).
+struct DevFlags {
+    int diverged;   // set by the final RK update on a non-finite value
+    int div_var;    // variable index of the first non-finite value
+    int div_step;   // step counter value (1-based within the launch batch)
+    int steps;      // steps started since the counter was last reset
+};
+
+// Grid description shared by the 2D and 3D solvers.  Axis 0 is the slowest
+// (row-major), the last axis is the half-stored Hermitian one.
+struct GridDesc {
+    int dims;
+    int n[3];        // physical extents (padded with 1 on the left for 2D: NOT used)
+    int nh;          // n[dims-1]/2 + 1
+    int kc[3];       // keep iff |signed index| <= kc[d]  (bit-exact dealias rule)
+    double kscale[3];  // 2 pi / L_d: k = kscale * signed index
+};
+
+__host__ __device__ __forceinline__ int signed_index(int i, int n) { return i <= n / 2 ? i : i - n; }
+
+// ---------------------------------------------------------------- ns2d
+// Internal spectral layout "CM": [ky][kx] (each ky column contiguous over
+// kx), nh columns of nx complex.  Intermediates between the x and y passes
+// are row-major [x][ky] with row stride ld (only the ky columns that can be
+// non-zero are stored).
+struct Ns2dArgs {
+    int nx, ny, nh;
+    int kcx, kcy;       // dealias: keep |kx_i| <= kcx and ky_i <= kcy
+    int ky_in;          // columns read by the x-inverse pass (kcy+1 pruned, nh full)
+    int ld_i;           // row stride of the four intermediates (= ky_in)
+    int ld_o;           // row stride of the tendency rows (= kcy+1)
+    int pruned;         // 1: state is dealiased, skip masked modes
+    int has_sigma;      // nu != 0
+    int rk2;            // scheme
+    double kx_scale, ky_scale;
+    double inv_n;       // 1 / (nx ny)
+    double dt, hdt, sdt;
+    const double* e1x;  // exp(0.5 dt (-nu kx^2)) per kx index (nx)
+    const double* e1y;  // exp(0.5 dt (-nu ky^2)) per ky index (nh)
+    const double* e2x;  // exp(dt (-nu kx^2))
+    const double* e2y;
+    cd* u;              // state (CM)
+    cd* k1;
+    cd* k2;
+    cd* k3;
+    cd* I[4];           // X[psi], X[kx psi], X[kx w], X[w]  ([x][ld_i])
+    cd* nl;             // tendency rows [x][ld_o] (x-space, ky spectral)
+    const cd* twx;      // W_nx table
+    const cd* twy;      // W_ny table
+    DevFlags* flags;
+};
+
+// Launchers (ns2d.cu).  stage in 1..4 (RK4) or 1..2 (RK2); stage 0 = plain
+// tendency evaluation of u into k1 (no RK arithmetic).
+cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches);
+bool ns2d_supported(int nx, int ny);
+
+// ---------------------------------------------------------------- ns3d
+struct Ns3dArgs {
+    int nx, ny, nz, nh;     // nh = nz/2+1
+    int kcx, kcy, kcz;
+    int pruned, has_sigma, rk2;
+    // extents of the stored/processed index ranges
+    int ky_in, kz_in;       // (ky, kz) lines processed by the x-inverse pass
+    double kx_scale, ky_scale, kz_scale;
+    double inv_n;
+    double dt, hdt, sdt;
+    const double *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
+    cd* u[3];               // state, reference layout [kx][ky][kz]
+    cd* k1[3];
+    cd* k2[3];
+    cd* k3[3];
+    cd* A[5];               // x-pass outputs  [x][ky][kz]   (kz < kz_in)
+    cd* B[6];               // y-pass outputs  [x][y][kz]
+    cd* C[3];               // z-pass outputs  [x][y][kz]   (kz <= kcz)
+    cd* D[3];               // y-forward outputs [x][ky][kz]
+    const cd *twx, *twy, *twz;
+    DevFlags* flags;
+};
+cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches);
+bool ns3d_supported(int nx, int ny, int nz);
+
+// ---------------------------------------------------------------- utilities (util.cu)
+cudaError_t launch_transpose_c(const cd* in, cd* out, int rows, int cols, int conj_flag,
+                               cudaStream_t s, long* launches);  // out[c][r] = in[r][c]
+cudaError_t launch_count_masked(const cd* f, int dims, const int* n, const int* kc, int nvars,
+                                long long spect_size, unsigned long long* d_count,
+                                cudaStream_t s, long* launches);
+cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double* kscale,
+                             int axis, double* d_k, unsigned char* d_mask, cudaStream_t s,
+                             long* launches);
+cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* kscale, int nvars,
+                          int solver2d, double* d_out, cudaStream_t s, long* launches);
+
+// Plain transforms on the context grid / arbitrary shapes (fft_ops.cu).
+// u: row-major real (n0..n_{d-1}); uhat: row-major half spectrum.
+cudaError_t fft_forward_dev(int rank, const int* n, const double* d_u, cd* d_uhat, cd* d_work,
+                            const cd* const* tw, cudaStream_t s, long* launches);
+cudaError_t fft_inverse_dev(int rank, const int* n, const cd* d_uhat, double* d_u, cd* d_work,
+                            const cd* const* tw, cudaStream_t s, long* launches);
+bool fft_pow2(int n);
+
+}  // namespace skg

@@ -1,0 +1,603 @@
+// skgpu.cu -- context, device memory and the extern "C" boundary (include/skgpu.h).
+//
+// Mirrors the reference's Simulation / ExactLinStepper / Solver contract
+// (proj/src/simulation.cpp:297-590, proj/src/time_stepping.cpp:72-194) for a
+// device-resident state.  The host side only validates arguments, builds the
+// small per-axis tables (twiddles, exp factors, dealias cut indices) and
+// enqueues kernels; every per-mode operation runs in sm_100a kernels.  There is
+// no CPU fallback: a missing device or an unsupported extent is an error.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/skgpu.h"
+#include "skg_internal.h"
+
+using skg::cd;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(SKG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;  // grid.cpp:11
+
+// W_n^m = exp(-2 pi i m / n), m in [0, n), in extended precision.
+std::vector<cd> twiddles(int n) {
+    std::vector<cd> w(n);
+    const long double tp = 6.283185307179586476925286766559005768L;
+    for (int m = 0; m < n; ++m) {
+        long double a = tp * (long double)m / (long double)n;
+        w[m] = make_double2((double)cosl(a), (double)-sinl(a));
+    }
+    return w;
+}
+
+// Largest |signed index| kept by the dealias rule |k_d| <= kcut_d of
+// make_grid (grid.cpp:78-100), evaluated with the same double arithmetic.
+int cut_index(int n, double L, double coef, bool half) {
+    const double spacing = kTwoPi / L;
+    const double kcut = coef * (kTwoPi / L) * (n / 2);
+    int best = -1;
+    const int hi = half ? n / 2 : n / 2;
+    for (int i = 0; i <= hi; ++i)
+        if (std::abs(spacing * i) <= kcut) best = i;
+    // negative indices -(n/2-1)..-1 mirror the positive ones for |k|
+    return best;
+}
+
+}  // namespace
+
+struct skg_ctx {
+    int device = 0;
+    int solver = 2;  // 2: ns2d, 3: ns3d
+    int dims = 2;
+    int n[3] = {1, 1, 1};
+    double L[3] = {kTwoPi, kTwoPi, kTwoPi};
+    double coef = 2.0 / 3.0;
+    double nu = 0.0;
+    int scheme = SKG_RK4;
+    int nvars = 1;
+    int nh = 0;
+    int kc[3] = {0, 0, 0};
+    double kscale[3] = {1, 1, 1};
+    long long S = 0, P = 0;
+
+    cudaStream_t own = nullptr, stream = nullptr;
+    long launches = 0;
+
+    // device buffers
+    cd* u = nullptr;      // nvars * S (2D: CM layout; 3D: reference layout)
+    cd* k[3] = {nullptr, nullptr, nullptr};
+    cd* inter = nullptr;  // intermediates
+    size_t inter_elems = 0;
+    cd* io = nullptr;     // nvars * S staging in reference layout
+    double* phys = nullptr;
+    cd* work = nullptr;
+    double* etab = nullptr;  // e1[axis], e2[axis] tables
+    cd* tw[3] = {nullptr, nullptr, nullptr};
+    skg::DevFlags* flags = nullptr;
+    unsigned long long* d_count = nullptr;
+    double* d_red = nullptr;
+
+    bool pruned = false;
+    double cached_dt = -1.0;
+    long it = 0;
+    double t = 0.0;
+    long div_it = -1;
+    int div_var = -1;
+    long pending_steps = 0;
+    double pending_dt = 0.0;
+};
+
+namespace {
+
+int refresh_exp(skg_ctx* c, double dt) {
+    if (dt == c->cached_dt) return SKG_OK;
+    // Separable factors: exp(h sigma) = prod_d exp(h (-nu k_d^2)) with
+    // sigma = -nu |k|^2 (simulation.cpp:147-157, time_stepping.cpp:49-52).
+    const int d = c->dims;
+    std::vector<double> h;
+    int off = 0;
+    int ext[3];
+    for (int a = 0; a < d; ++a) ext[a] = a == d - 1 ? c->nh : c->n[a];
+    std::vector<double> tab;
+    for (int which = 0; which < 2; ++which) {
+        const double hdt = which == 0 ? 0.5 * dt : dt;
+        for (int a = 0; a < d; ++a) {
+            for (int i = 0; i < ext[a]; ++i) {
+                const int si = a == d - 1 ? i : skg::signed_index(i, c->n[a]);
+                const double kv = c->kscale[a] * si;
+                tab.push_back(std::exp(hdt * (-c->nu * (kv * kv))));
+            }
+        }
+    }
+    (void)off;
+    CUDA_TRY(cudaMemcpyAsync(c->etab, tab.data(), tab.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream));
+    c->cached_dt = dt;
+    return SKG_OK;
+}
+
+const double* etab_ptr(const skg_ctx* c, int which, int axis) {
+    int off = 0;
+    int ext[3];
+    for (int a = 0; a < c->dims; ++a) ext[a] = a == c->dims - 1 ? c->nh : c->n[a];
+    int per = 0;
+    for (int a = 0; a < c->dims; ++a) per += ext[a];
+    off = which * per;
+    for (int a = 0; a < axis; ++a) off += ext[a];
+    return c->etab + off;
+}
+
+skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
+    skg::Ns2dArgs a{};
+    a.nx = c->n[0];
+    a.ny = c->n[1];
+    a.nh = c->nh;
+    a.kcx = c->kc[0];
+    a.kcy = c->kc[1];
+    a.pruned = c->pruned ? 1 : 0;
+    a.ky_in = c->pruned ? c->kc[1] + 1 : c->nh;
+    a.ld_i = a.ky_in;
+    a.ld_o = c->kc[1] + 1;
+    a.has_sigma = c->nu != 0.0;
+    a.rk2 = c->scheme == SKG_RK2;
+    a.kx_scale = c->kscale[0];
+    a.ky_scale = c->kscale[1];
+    a.inv_n = 1.0 / (double)c->P;
+    a.dt = dt;
+    a.hdt = 0.5 * dt;
+    a.sdt = dt / 6.0;
+    a.e1x = etab_ptr(c, 0, 0);
+    a.e1y = etab_ptr(c, 0, 1);
+    a.e2x = etab_ptr(c, 1, 0);
+    a.e2y = etab_ptr(c, 1, 1);
+    a.u = c->u;
+    a.k1 = c->k[0];
+    a.k2 = c->k[1];
+    a.k3 = c->k[2];
+    const size_t isz = (size_t)c->n[0] * c->nh;
+    for (int m = 0; m < 4; ++m) a.I[m] = c->inter + m * isz;
+    a.nl = c->inter + 4 * isz;
+    a.twx = c->tw[0];
+    a.twy = c->tw[1];
+    a.flags = c->flags;
+    return a;
+}
+
+int sync_and_check(skg_ctx* c, long nsteps, double dt) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    skg::DevFlags f;
+    CUDA_TRY(cudaMemcpy(&f, c->flags, sizeof(f), cudaMemcpyDeviceToHost));
+    if (f.diverged) {
+        const long done = f.div_step;
+        for (long i = 0; i < done; ++i) c->t += dt;
+        c->it += done;
+        c->div_it = c->it;
+        c->div_var = f.div_var;
+        static const char* keys2[] = {"rot_fft"};
+        static const char* keys3[] = {"vx_fft", "vy_fft", "vz_fft"};
+        const char* key = c->solver == 2 ? keys2[0] : keys3[f.div_var >= 0 && f.div_var < 3 ? f.div_var : 0];
+        return fail(SKG_EDIVERGENCE, std::string("non-finite value in field '") + key +
+                                         "' at iteration " + std::to_string(c->it));
+    }
+    for (long i = 0; i < nsteps; ++i) c->t += dt;
+    c->it += nsteps;
+    return SKG_OK;
+}
+
+int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
+    if (!(dt > 0.0)) return fail(SKG_ECONFIG, "step: nonpositive dt");
+    if (nsteps < 0) return fail(SKG_ECONFIG, "step: negative step count");
+    CUDA_TRY(cudaSetDevice(c->device));
+    int rc = refresh_exp(c, dt);
+    if (rc) return rc;
+    skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
+    CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    const int nst = c->scheme == SKG_RK2 ? 2 : 4;
+    if (c->solver == 2) {
+        skg::Ns2dArgs a = args2d(c, dt);
+        for (long s = 0; s < nsteps; ++s)
+            for (int st = 1; st <= nst; ++st)
+                CUDA_TRY(skg::ns2d_launch_stage(a, st, c->stream, &c->launches));
+    } else {
+        return fail(SKG_EUNSUPPORTED, "ns3d step not built");
+    }
+    return SKG_OK;
+}
+
+int decide_pruned(skg_ctx* c, const cd* d_ref_layout) {
+    // fast path iff every masked-out mode of every variable is exactly zero
+    CUDA_TRY(skg::launch_count_masked(d_ref_layout, c->dims, c->n, c->kc, c->nvars, c->S,
+                                      c->d_count, c->stream, &c->launches));
+    unsigned long long cnt = 0;
+    CUDA_TRY(cudaMemcpyAsync(&cnt, c->d_count, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->pruned = cnt == 0;
+    return SKG_OK;
+}
+
+// reference layout (io) -> internal state
+int load_state_from_io(skg_ctx* c) {
+    int rc = decide_pruned(c, c->io);
+    if (rc) return rc;
+    if (c->solver == 2) {
+        CUDA_TRY(skg::launch_transpose_c(c->io, c->u, c->n[0], c->nh, 0, c->stream, &c->launches));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(c->u, c->io, sizeof(cd) * c->S * c->nvars,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return SKG_OK;
+}
+
+int store_state_to_io(skg_ctx* c, const cd* src) {
+    if (c->solver == 2) {
+        CUDA_TRY(skg::launch_transpose_c(src, c->io, c->nh, c->n[0], 0, c->stream, &c->launches));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(c->io, src, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    }
+    return SKG_OK;
+}
+
+struct TwCache {
+    std::mutex mu;
+    std::map<std::pair<int, int>, cd*> tabs;  // (device, n) -> table
+} g_tw;
+
+cd* twiddle_table(int device, int n) {
+    std::lock_guard<std::mutex> lk(g_tw.mu);
+    auto key = std::make_pair(device, n);
+    auto it = g_tw.tabs.find(key);
+    if (it != g_tw.tabs.end()) return it->second;
+    std::vector<cd> w = twiddles(n);
+    cd* d = nullptr;
+    if (cudaMalloc(&d, sizeof(cd) * n) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, w.data(), sizeof(cd) * n, cudaMemcpyHostToDevice);
+    g_tw.tabs[key] = d;
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skg_version(void) { return "skgpu 0.1.0 sm_100a"; }
+
+const char* skg_last_error(void) { return g_err.c_str(); }
+
+int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+               double dealias_coef, double nu, int scheme, int device) {
+    if (!out) return fail(SKG_ECONFIG, "create: null output pointer");
+    *out = nullptr;
+    std::string s = solver ? solver : "";
+    int sid = s == "ns2d" ? 2 : s == "ns3d" ? 3 : 0;
+    if (!sid) return fail(SKG_ECONFIG, "unknown solver '" + s + "' (registered: ns2d, ns3d)");
+    if (dims != sid) return fail(SKG_ECONFIG, "solver " + s + " needs " + std::to_string(sid) + " extents");
+    for (int d = 0; d < dims; ++d) {
+        if (n[d] < 4) return fail(SKG_ECONFIG, "extent " + std::to_string(n[d]) + " too small (min 4)");
+        if (n[d] % 2) return fail(SKG_ECONFIG, "extent " + std::to_string(n[d]) + " is odd");
+        if (L && !(L[d] > 0)) return fail(SKG_ECONFIG, "domain length must be positive");
+    }
+    if (!(dealias_coef > 0.0) || dealias_coef > 1.0)
+        return fail(SKG_ECONFIG, "dealias_coef must be in (0, 1]");
+    if (!(nu >= 0.0)) return fail(SKG_ECONFIG, "viscosity must be >= 0");
+    if (scheme != SKG_RK4 && scheme != SKG_RK2) return fail(SKG_ECONFIG, "unknown time scheme");
+    if (sid == 2 && !skg::ns2d_supported(n[0], n[1]))
+        return fail(SKG_EUNSUPPORTED, "ns2d kernels need power-of-two extents in [4, 8192]");
+    if (sid == 3) return fail(SKG_EUNSUPPORTED, "ns3d kernels not built yet");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SKG_ECUDA, "no CUDA device visible (the library has no CPU path)");
+    if (device < 0 || device >= ndev) return fail(SKG_ECONFIG, "device ordinal out of range");
+
+    auto c = new skg_ctx();
+    c->device = device;
+    c->solver = sid;
+    c->dims = dims;
+    c->coef = dealias_coef;
+    c->nu = nu;
+    c->scheme = scheme;
+    c->nvars = sid == 2 ? 1 : 3;
+    for (int d = 0; d < dims; ++d) {
+        c->n[d] = n[d];
+        c->L[d] = L ? L[d] : kTwoPi;
+        c->kscale[d] = kTwoPi / c->L[d];
+        c->kc[d] = cut_index(n[d], c->L[d], dealias_coef, d == dims - 1);
+    }
+    c->nh = n[dims - 1] / 2 + 1;
+    c->S = c->nh;
+    c->P = 1;
+    for (int d = 0; d < dims - 1; ++d) c->S *= n[d];
+    for (int d = 0; d < dims; ++d) c->P *= n[d];
+
+    auto cleanup = [&](int code, const std::string& msg) {
+        skg_destroy(c);
+        return fail(code, msg);
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return cleanup(SKG_ECUDA, "cudaSetDevice failed");
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(SKG_ECUDA, "stream creation failed");
+    c->stream = c->own;
+    const size_t S = (size_t)c->S;
+    auto alloc = [&](void** p, size_t bytes) {
+        if (cudaMalloc(p, bytes) != cudaSuccess) return false;
+        return cudaMemset(*p, 0, bytes) == cudaSuccess;
+    };
+    bool ok = alloc((void**)&c->u, sizeof(cd) * S * c->nvars);
+    for (int i = 0; i < 3 && ok; ++i) ok = alloc((void**)&c->k[i], sizeof(cd) * S * c->nvars);
+    if (sid == 2) c->inter_elems = 5 * S;  // 4 intermediates + tendency rows
+    ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
+    ok = ok && alloc((void**)&c->io, sizeof(cd) * S * c->nvars);
+    ok = ok && alloc((void**)&c->phys, sizeof(double) * (size_t)c->P);
+    ok = ok && alloc((void**)&c->work, sizeof(cd) * S);
+    int ext_total = 0;
+    for (int d = 0; d < dims; ++d) ext_total += d == dims - 1 ? c->nh : n[d];
+    ok = ok && alloc((void**)&c->etab, sizeof(double) * 2 * ext_total);
+    ok = ok && alloc((void**)&c->flags, sizeof(skg::DevFlags));
+    ok = ok && alloc((void**)&c->d_count, sizeof(unsigned long long));
+    ok = ok && alloc((void**)&c->d_red, 2 * sizeof(double));
+    if (!ok) return cleanup(SKG_ECUDA, "device allocation failed (grid too large for this GPU?)");
+    for (int d = 0; d < dims; ++d) {
+        c->tw[d] = twiddle_table(device, n[d]);
+        if (!c->tw[d]) return cleanup(SKG_ECUDA, "twiddle table allocation failed");
+    }
+    c->pruned = true;  // zero state is dealiased
+    *out = c;
+    return SKG_OK;
+}
+
+int skg_destroy(skg_ctx* c) {
+    if (!c) return SKG_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->u);
+    for (auto p : c->k) cudaFree(p);
+    cudaFree(c->inter);
+    cudaFree(c->io);
+    cudaFree(c->phys);
+    cudaFree(c->work);
+    cudaFree(c->etab);
+    cudaFree(c->flags);
+    cudaFree(c->d_count);
+    cudaFree(c->d_red);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+    return SKG_OK;
+}
+
+int skg_set_stream(skg_ctx* c, void* stream) {
+    c->stream = stream ? (cudaStream_t)stream : c->own;
+    return SKG_OK;
+}
+
+long skg_spect_size(const skg_ctx* c) { return (long)c->S; }
+long skg_phys_size(const skg_ctx* c) { return (long)c->P; }
+int skg_nvars(const skg_ctx* c) { return c->nvars; }
+long skg_iteration(const skg_ctx* c) { return c->it; }
+double skg_time(const skg_ctx* c) { return c->t; }
+int skg_pruned(const skg_ctx* c) { return c->pruned ? 1 : 0; }
+long skg_launch_count(const skg_ctx* c) { return c->launches; }
+
+int skg_set_state(skg_ctx* c, const double* spect) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(c->io, spect, sizeof(cd) * c->S * c->nvars, cudaMemcpyHostToDevice,
+                             c->stream));
+    int rc = load_state_from_io(c);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
+int skg_set_state_device(skg_ctx* c, const double* d_spect) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(c->io, d_spect, sizeof(cd) * c->S * c->nvars,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    return load_state_from_io(c);
+}
+
+int skg_get_state(skg_ctx* c, double* spect_out) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    int rc = store_state_to_io(c, c->u);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(spect_out, c->io, sizeof(cd) * c->S * c->nvars,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
+int skg_get_state_device(skg_ctx* c, double* d_out) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    int rc = store_state_to_io(c, c->u);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(d_out, c->io, sizeof(cd) * c->S * c->nvars,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    return SKG_OK;
+}
+
+int skg_step_async(skg_ctx* c, double dt, long nsteps) {
+    int rc = enqueue_steps(c, dt, nsteps);
+    if (rc) return rc;
+    c->pending_steps += nsteps;
+    c->pending_dt = dt;
+    return SKG_OK;
+}
+
+int skg_sync(skg_ctx* c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    long n = c->pending_steps;
+    c->pending_steps = 0;
+    return sync_and_check(c, n, c->pending_dt);
+}
+
+int skg_step(skg_ctx* c, double dt, long nsteps) {
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    int rc = enqueue_steps(c, dt, nsteps);
+    if (rc) return rc;
+    return sync_and_check(c, nsteps, dt);
+}
+
+int skg_tendency(skg_ctx* c, const double* in, double* out) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->io, in, sizeof(cd) * c->S * c->nvars, cudaMemcpyHostToDevice,
+                             c->stream));
+    const bool keep_pruned = c->pruned;
+    int rc = decide_pruned(c, c->io);
+    if (rc) return rc;
+    if (c->solver == 2) {
+        // input (CM) in k[2], tendency into k[0]
+        CUDA_TRY(skg::launch_transpose_c(c->io, c->k[2], c->n[0], c->nh, 0, c->stream, &c->launches));
+        rc = refresh_exp(c, c->cached_dt > 0 ? c->cached_dt : 1.0);
+        if (rc) return rc;
+        skg::Ns2dArgs a = args2d(c, c->cached_dt);
+        a.u = c->k[2];
+        skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(skg::ns2d_launch_stage(a, 1, c->stream, &c->launches));
+        rc = store_state_to_io(c, c->k[0]);
+        if (rc) return rc;
+    } else {
+        return fail(SKG_EUNSUPPORTED, "ns3d tendency not built");
+    }
+    CUDA_TRY(cudaMemcpyAsync(out, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->pruned = keep_pruned;
+    return SKG_OK;
+}
+
+int skg_fft_forward(skg_ctx* c, const double* u, double* uhat) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(c->phys, u, sizeof(double) * c->P, cudaMemcpyHostToDevice, c->stream));
+    const cd* tw[3] = {c->tw[0], c->tw[1], c->tw[2]};
+    CUDA_TRY(skg::fft_forward_dev(c->dims, c->n, c->phys, c->io, c->work, tw, c->stream, &c->launches));
+    CUDA_TRY(cudaMemcpyAsync(uhat, c->io, sizeof(cd) * c->S, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
+int skg_fft_inverse(skg_ctx* c, const double* uhat, double* u) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(c->io, uhat, sizeof(cd) * c->S, cudaMemcpyHostToDevice, c->stream));
+    const cd* tw[3] = {c->tw[0], c->tw[1], c->tw[2]};
+    CUDA_TRY(skg::fft_inverse_dev(c->dims, c->n, c->io, c->phys, c->work, tw, c->stream, &c->launches));
+    CUDA_TRY(cudaMemcpyAsync(u, c->phys, sizeof(double) * c->P, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
+static int plan_common(int rank, const int* shape, long long* P, long long* S) {
+    if (rank < 1 || rank > 3)
+        return fail(SKG_ESHAPE, "transform rank must be 1..3, got " + std::to_string(rank));
+    *P = 1;
+    *S = 1;
+    for (int d = 0; d < rank; ++d) {
+        if (shape[d] < 4) return fail(SKG_ESHAPE, "extent " + std::to_string(shape[d]) + " too small (min 4)");
+        if (shape[d] % 2) return fail(SKG_ESHAPE, "extent " + std::to_string(shape[d]) + " is odd");
+        *P *= shape[d];
+        *S *= d == rank - 1 ? shape[d] / 2 + 1 : shape[d];
+    }
+    return SKG_OK;
+}
+
+int skg_plan_forward(int rank, const int* shape, const double* u, double* uhat, int device) {
+    long long P, S;
+    int rc = plan_common(rank, shape, &P, &S);
+    if (rc) return rc;
+    CUDA_TRY(cudaSetDevice(device));
+    double* du;
+    cd* dh;
+    CUDA_TRY(cudaMalloc(&du, sizeof(double) * P));
+    CUDA_TRY(cudaMalloc(&dh, sizeof(cd) * S));
+    CUDA_TRY(cudaMemcpy(du, u, sizeof(double) * P, cudaMemcpyHostToDevice));
+    const cd* tw[3] = {nullptr, nullptr, nullptr};
+    for (int d = 0; d < rank; ++d) tw[d] = twiddle_table(device, shape[d]);
+    long l = 0;
+    cudaError_t e = skg::fft_forward_dev(rank, shape, du, dh, nullptr, tw, 0, &l);
+    if (e == cudaSuccess) e = cudaMemcpy(uhat, dh, sizeof(cd) * S, cudaMemcpyDeviceToHost);
+    cudaFree(du);
+    cudaFree(dh);
+    if (e != cudaSuccess) return fail(SKG_ECUDA, cudaGetErrorString(e));
+    return SKG_OK;
+}
+
+int skg_plan_inverse(int rank, const int* shape, const double* uhat, double* u, int device) {
+    long long P, S;
+    int rc = plan_common(rank, shape, &P, &S);
+    if (rc) return rc;
+    CUDA_TRY(cudaSetDevice(device));
+    double* du;
+    cd *dh, *dw;
+    CUDA_TRY(cudaMalloc(&du, sizeof(double) * P));
+    CUDA_TRY(cudaMalloc(&dh, sizeof(cd) * S));
+    CUDA_TRY(cudaMalloc(&dw, sizeof(cd) * S));
+    CUDA_TRY(cudaMemcpy(dh, uhat, sizeof(cd) * S, cudaMemcpyHostToDevice));
+    const cd* tw[3] = {nullptr, nullptr, nullptr};
+    for (int d = 0; d < rank; ++d) tw[d] = twiddle_table(device, shape[d]);
+    long l = 0;
+    cudaError_t e = skg::fft_inverse_dev(rank, shape, dh, du, dw, tw, 0, &l);
+    if (e == cudaSuccess) e = cudaMemcpy(u, du, sizeof(double) * P, cudaMemcpyDeviceToHost);
+    cudaFree(du);
+    cudaFree(dh);
+    cudaFree(dw);
+    if (e != cudaSuccess) return fail(SKG_ECUDA, cudaGetErrorString(e));
+    return SKG_OK;
+}
+
+int skg_get_grid(skg_ctx* c, int axis, double* k_axis, unsigned char* mask) {
+    if (axis < 0 || axis >= c->dims) return fail(SKG_ESHAPE, "axis out of range");
+    CUDA_TRY(cudaSetDevice(c->device));
+    double* dk = reinterpret_cast<double*>(c->work);  // >= nh doubles
+    unsigned char* dm = mask ? reinterpret_cast<unsigned char*>(c->io) : nullptr;
+    CUDA_TRY(skg::launch_grid_dump(c->dims, c->n, c->kc, c->kscale, axis, dk, dm, c->stream, &c->launches));
+    const int ext = axis == c->dims - 1 ? c->nh : c->n[axis];
+    CUDA_TRY(cudaMemcpyAsync(k_axis, dk, sizeof(double) * ext, cudaMemcpyDeviceToHost, c->stream));
+    if (mask) CUDA_TRY(cudaMemcpyAsync(mask, dm, (size_t)c->S, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
+int skg_last_divergence(const skg_ctx* c, long* iteration, int* var) {
+    *iteration = c->div_it;
+    *var = c->div_var;
+    return SKG_OK;
+}
+
+int skg_energy(skg_ctx* c, double* energy, double* enstrophy) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
+                                c->d_red, c->stream, &c->launches));
+    double h[2];
+    CUDA_TRY(cudaMemcpyAsync(h, c->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (energy) *energy = h[0];
+    if (enstrophy) *enstrophy = c->solver == 2 ? h[1] : 0.0;
+    return SKG_OK;
+}
+
+}  // extern "C"

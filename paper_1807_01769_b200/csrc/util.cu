@@ -1,0 +1,195 @@
+// util.cu -- layout transposes, dealias-state check, device grid dump and
+// diagnostic reductions.
+#include "skg_internal.h"
+
+namespace skg {
+
+namespace {
+
+constexpr int TD = 32;
+
+// out[c][r] = in[r][c] (complex), 32x32 tiles through shared memory.
+__global__ void transpose_c(const cd* __restrict__ in, cd* __restrict__ out, int rows, int cols) {
+    __shared__ cd tile[TD][TD + 1];
+    const int c0 = blockIdx.x * TD, r0 = blockIdx.y * TD;
+    for (int j = threadIdx.y; j < TD; j += blockDim.y) {
+        const int r = r0 + j, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = in[(size_t)r * cols + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < TD; j += blockDim.y) {
+        const int c = c0 + j, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[(size_t)c * rows + r] = tile[threadIdx.x][j];
+    }
+}
+
+struct MaskGeo {
+    int dims;
+    int n[3];
+    int nh;
+    int kc[3];
+};
+
+// Multi-index (reference layout) of a flat spectral index.
+__device__ __forceinline__ void unflatten(const MaskGeo& g, long long q, int* ix) {
+    if (g.dims == 1) {
+        ix[0] = (int)q;
+    } else if (g.dims == 2) {
+        ix[1] = (int)(q % g.nh);
+        ix[0] = (int)(q / g.nh);
+    } else {
+        ix[2] = (int)(q % g.nh);
+        long long r = q / g.nh;
+        ix[1] = (int)(r % g.n[1]);
+        ix[0] = (int)(r / g.n[1]);
+    }
+}
+
+__device__ __forceinline__ bool kept(const MaskGeo& g, const int* ix) {
+    for (int d = 0; d < g.dims; ++d) {
+        const int si = d == g.dims - 1 ? ix[d] : signed_index(ix[d], g.n[d]);
+        if (abs(si) > g.kc[d]) return false;
+    }
+    return true;
+}
+
+__global__ void count_masked(const cd* __restrict__ f, MaskGeo g, int nvars, long long S,
+                             unsigned long long* count) {
+    unsigned long long c = 0;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < S;
+         q += (long long)gridDim.x * blockDim.x) {
+        int ix[3];
+        unflatten(g, q, ix);
+        if (kept(g, ix)) continue;
+        for (int v = 0; v < nvars; ++v) {
+            cd x = f[v * S + q];
+            if (x.x != 0.0 || x.y != 0.0) ++c;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void grid_dump(MaskGeo g, int axis, double kscale, double* k, unsigned char* mask,
+                          long long S) {
+    const int ext = axis == g.dims - 1 ? g.nh : g.n[axis];
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < S;
+         q += (long long)gridDim.x * blockDim.x) {
+        if (q < ext) {
+            const int si = axis == g.dims - 1 ? (int)q : signed_index((int)q, g.n[axis]);
+            k[q] = kscale * (double)si;
+        }
+        if (mask) {
+            int ix[3];
+            unflatten(g, q, ix);
+            mask[q] = kept(g, ix) ? 1 : 0;
+        }
+    }
+}
+
+struct EnGeo {
+    MaskGeo m;
+    double ks[3];
+    int solver2d;  // 1: ns2d on the CM layout ([ky][kx]); 0: reference layout
+};
+
+// E and Z (Simulation::energy / enstrophy, simulation.cpp:592-615 with the
+// ns2d mode_energy / mode_enstrophy of solvers.cpp:211-230 and the default
+// Solver::mode_energy of simulation.cpp:163-170).
+__global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long long S,
+                              double* out) {
+    double e = 0.0, z = 0.0;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < S;
+         q += (long long)gridDim.x * blockDim.x) {
+        int ix[3];
+        if (g.solver2d) {  // CM: q = ky * nx + kx
+            ix[0] = (int)(q % g.m.n[0]);
+            ix[1] = (int)(q / g.m.n[0]);
+        } else {
+            unflatten(g.m, q, ix);
+        }
+        const int il = ix[g.m.dims - 1];
+        const double w = (il == 0 || il == g.m.nh - 1) ? 1.0 : 2.0;
+        double ksq = 0.0;
+        for (int d = 0; d < g.m.dims; ++d) {
+            const int si = d == g.m.dims - 1 ? ix[d] : signed_index(ix[d], g.m.n[d]);
+            const double k = g.ks[d] * si;
+            ksq += k * k;
+        }
+        for (int v = 0; v < nvars; ++v) {
+            cd x = f[v * S + q];
+            const double nrm = x.x * x.x + x.y * x.y;
+            if (g.solver2d) {
+                if (ksq > 0.0) e += 0.5 * w * nrm / ksq;
+                z += 0.5 * w * nrm;
+            } else {
+                e += 0.5 * w * nrm;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_down_sync(0xffffffffu, e, o);
+        z += __shfl_down_sync(0xffffffffu, z, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], e);
+        atomicAdd(&out[1], z);
+    }
+}
+
+MaskGeo make_geo(int dims, const int* n, const int* kc) {
+    MaskGeo g{};
+    g.dims = dims;
+    for (int d = 0; d < dims; ++d) {
+        g.n[d] = n[d];
+        g.kc[d] = kc[d];
+    }
+    g.nh = n[dims - 1] / 2 + 1;
+    return g;
+}
+
+}  // namespace
+
+cudaError_t launch_transpose_c(const cd* in, cd* out, int rows, int cols, int, cudaStream_t s,
+                               long* launches) {
+    dim3 grid((cols + TD - 1) / TD, (rows + TD - 1) / TD);
+    transpose_c<<<grid, dim3(TD, 8), 0, s>>>(in, out, rows, cols);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_masked(const cd* f, int dims, const int* n, const int* kc, int nvars,
+                                long long S, unsigned long long* d_count, cudaStream_t s,
+                                long* launches) {
+    cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
+    count_masked<<<592, 256, 0, s>>>(f, make_geo(dims, n, kc), nvars, S, d_count);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double* kscale, int axis,
+                             double* d_k, unsigned char* d_mask, cudaStream_t s, long* launches) {
+    MaskGeo g = make_geo(dims, n, kc);
+    long long S = 1;
+    for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.nh : n[d]);
+    grid_dump<<<592, 256, 0, s>>>(g, axis, kscale[axis], d_k, d_mask, S);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* kscale, int nvars,
+                          int solver2d, double* d_out, cudaStream_t s, long* launches) {
+    int kc[3] = {0, 0, 0};
+    EnGeo g{};
+    g.m = make_geo(dims, n, kc);
+    for (int d = 0; d < dims; ++d) g.ks[d] = kscale[d];
+    g.solver2d = solver2d;
+    long long S = 1;
+    for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.m.nh : n[d]);
+    cudaMemsetAsync(d_out, 0, 2 * sizeof(double), s);
+    energy_kernel<<<592, 256, 0, s>>>(f, g, nvars, S, d_out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace skg

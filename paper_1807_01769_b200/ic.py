@@ -141,7 +141,7 @@ def cfl_dt(solver, n, state, cfl=0.5, dt_max=0.1):
     dt = dt_max
     dx = K_TWO_PI / n[0]
     for a, c in enumerate(comps):
-        u = np.fft.irfftn(c, s=n, norm="forward")
+        u = np.fft.irfftn(c, s=n, axes=tuple(range(len(n))), norm="forward")
         vel = max(float(np.abs(u).max()), 1e-30)
         dt = min(dt, cfl * (K_TWO_PI / n[a]) / vel)
     return dt

@@ -1,0 +1,192 @@
+"""GPU parity tests, ns2d + transform operators, through the C ABI.
+
+Bars (BASELINE.json north_star): wavenumbers and dealias masks bit-exact;
+states within 1e-10 relative L2 per field after the stated steps; transforms
+within the reference's own test tolerances (test_fft.cpp).
+"""
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import spectral_np as O
+from paper_1807_01769_b200 import api, ic
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+PARITY = 1e-10
+
+
+def rel(a, b):
+    return O.rel_l2(a, b)
+
+
+@pytest.mark.parametrize("n", [(8, 8), (64, 32), (32, 128), (1024, 1024), (4096, 4096)])
+def test_grid_bit_exact(ref_lib, n):
+    g = api.Simulation("ns2d", n, 0.0, 0.1)
+    ks, mask = g.grid()
+    r = ref_lib.RefSimulation("ns2d", n, 0.0, 0.1)
+    rks, rmask = r.grid()
+    for a, b in zip(ks, rks):
+        assert a.tobytes() == b.tobytes()
+    assert mask.tobytes() == rmask.tobytes()
+
+
+@pytest.mark.parametrize("shape", [(8,), (8, 6), (6, 4, 8), (64, 64), (16, 16, 16), (16, 12, 8),
+                                   (1024, 1024), (4096, 64), (32, 4096), (128, 64, 32)])
+def test_fft_operators_match_reference(ref_lib, shape):
+    rng = np.random.default_rng(11)
+    u = rng.uniform(-1, 1, size=shape)
+    uh = api.fft_forward(u)
+    ruh = ref_lib.fft_forward(u)
+    assert np.abs(uh - ruh).max() < 1e-13  # test_fft.cpp:122
+    back = api.fft_inverse(uh, shape)
+    assert np.abs(back - u).max() / np.abs(u).max() < 1e-12  # test_fft.cpp:141-155
+    assert np.abs(back - ref_lib.fft_inverse(ruh, shape)).max() < 1e-12
+
+
+def test_fft_known_answers():
+    u = np.cos(2 * math.pi * np.arange(8) / 8)
+    uh = api.fft_forward(u)
+    assert abs(uh[1] - 0.5) < 1e-15
+    uh = api.fft_forward(np.full((16, 16), 3.0))
+    assert abs(uh[0, 0] - 3.0) < 1e-14 and np.abs(uh.ravel()[1:]).max() < 1e-14
+    h = np.zeros(5, complex)
+    h[1] = 0.5
+    assert np.allclose(api.fft_inverse(h, (8,)), np.cos(2 * math.pi * np.arange(8) / 8),
+                       rtol=0, atol=1e-15)
+    # the inverse leaves its input intact (test_fft.cpp:157-168)
+    rng = np.random.default_rng(5)
+    uh = api.fft_forward(rng.uniform(-1, 1, (16, 16)))
+    keep = uh.copy()
+    api.fft_inverse(uh, (16, 16))
+    assert np.array_equal(uh, keep)
+
+
+def test_context_fft_matches_plan(ref_lib):
+    g = api.Simulation("ns2d", (256, 128), 0.0, 0.1)
+    rng = np.random.default_rng(2)
+    u = rng.standard_normal((256, 128))
+    assert np.abs(g.fft_forward(u) - ref_lib.fft_forward(u)).max() < 1e-14
+    uh = ref_lib.fft_forward(u)
+    assert np.abs(g.fft_inverse(uh) - u).max() < 1e-12
+
+
+@pytest.mark.parametrize("n", [(16, 16), (32, 32), (64, 32), (32, 64), (256, 256), (1024, 1024)])
+def test_tendency_matches_reference(ref_lib, n):
+    u0 = ic.ns2d_ic(n, seed=3)
+    r = ref_lib.RefSimulation("ns2d", n, 1e-3, 1e-3)
+    g = api.Simulation("ns2d", n, 1e-3, 1e-3)
+    t_ref = r.tendency(u0)
+    t_gpu = g.compute_tendency(u0)
+    assert rel(t_gpu, t_ref) < 1e-12
+    # dealiased output: masked modes exactly zero, mean zero
+    mask = O.dealias_mask(n).astype(bool)
+    assert np.all(t_gpu[0][~mask] == 0)
+    assert t_gpu[0, 0, 0] == 0
+
+
+@pytest.mark.parametrize("n", [(16, 16), (64, 32), (128, 128)])
+def test_tendency_of_non_dealiased_input(ref_lib, n):
+    # the reference's tendency does not dealias its input (solvers.cpp:133-174):
+    # the unpruned path must see every mode
+    rng = np.random.default_rng(9)
+    w = O.forward(rng.standard_normal(n))[None]
+    r = ref_lib.RefSimulation("ns2d", n, 0.0, 0.1)
+    g = api.Simulation("ns2d", n, 0.0, 0.1)
+    assert rel(g.compute_tendency(w), r.tendency(w)) < 1e-12
+
+
+@pytest.mark.parametrize("path", sorted(GOLD.glob("ns2d*.npz")), ids=lambda p: p.stem)
+def test_golden_fixtures(path):
+    f = np.load(path)
+    n = tuple(int(x) for x in f["n"])
+    g = api.Simulation("ns2d", n, float(f["nu"]), float(f["dt"]), scheme=str(f["scheme"]))
+    assert rel(g.compute_tendency(f["u0"]), f["tendency"]) < 1e-12
+    g.set_state(f["u0"])
+    assert g.pruned
+    g.step(int(f["steps"]))
+    assert rel(g.get_state(), f["final"]) < PARITY
+    assert g.iteration == int(f["steps"])
+
+
+@pytest.mark.parametrize("n,steps,nu,dt", [((1024, 1024), 10, 1e-4, 1e-3), ((512, 256), 10, 1e-4, 2e-3)])
+def test_baseline_config_parity(ref_lib, n, steps, nu, dt):
+    """configs[0] of BASELINE.json: ns2d 1024^2, nu 1e-4, dt 1e-3, 10 RK4 steps."""
+    u0 = ic.ns2d_ic(n, seed=1234)
+    ref_lib.set_workers(8)
+    r = ref_lib.RefSimulation("ns2d", n, nu, dt)
+    r.set_state(u0)
+    r.step(steps)
+    g = api.Simulation("ns2d", n, nu, dt)
+    g.set_state(u0)
+    g.step(steps)
+    assert rel(g.get_state(), r.get_state()) < PARITY
+    e, z = g.energy_enstrophy()
+    assert abs(e - r.energy) < 1e-12 * max(1.0, r.energy)
+    assert abs(z - r.enstrophy) < 1e-10 * max(1.0, r.enstrophy)
+
+
+def test_unpruned_step_matches_reference(ref_lib):
+    # a state with energy in masked-out modes takes the full (unpruned) path
+    n = (64, 64)
+    rng = np.random.default_rng(4)
+    w = O.forward(rng.standard_normal(n))[None] * 5.0
+    w[0, 0, 0] = 0.3
+    r = ref_lib.RefSimulation("ns2d", n, 1e-2, 1e-3)
+    r.set_state(w)
+    r.step(5)
+    g = api.Simulation("ns2d", n, 1e-2, 1e-3)
+    g.set_state(w)
+    assert not g.pruned
+    g.step(5)
+    assert rel(g.get_state(), r.get_state()) < PARITY
+
+
+def test_taylor_green_known_answers():
+    # test_solvers.cpp:62-80 (zero nonlinear term) and 164-192 (exact decay)
+    n = (64, 64)
+    x = np.arange(64) * (2 * math.pi / 64)
+    w = 2.0 * np.sin(x)[:, None] * np.sin(x)[None, :]
+    wh = O.forward(w)[None]
+    nu, dt = 0.01, 0.01
+    g = api.Simulation("ns2d", n, nu, dt)
+    assert np.abs(g.compute_tendency(wh)).max() < 1e-13
+    g.set_state(wh)
+    assert abs(g.energy() - 0.25) < 1e-12 and abs(g.enstrophy() - 0.5) < 1e-12
+    g.step(20)
+    decay = math.exp(-2 * nu * 20 * dt)
+    assert np.abs(g.get_state() - wh * decay).max() < 1e-11
+
+
+def test_zero_state_gives_zero_tendency():
+    g = api.Simulation("ns2d", (32, 32), 1e-3, 1e-3)
+    z = np.zeros((1, 32, 17), complex)
+    assert np.all(g.compute_tendency(z) == 0)
+
+
+def test_divergence_error():
+    # NaN injection -> DivergenceError(iteration, field), state frozen (simulation.cpp:557-563)
+    n = (32, 32)
+    u0 = ic.ns2d_ic(n, seed=1)
+    u0[0, 3, 2] = np.nan
+    g = api.Simulation("ns2d", n, 1e-3, 1e-3)
+    g.set_state(u0)
+    with pytest.raises(api.DivergenceError) as ei:
+        g.step(5)
+    assert ei.value.iteration == 1
+    assert ei.value.field == "rot_fft"
+    assert g.iteration == 1
+
+
+def test_bad_dt():
+    g = api.Simulation("ns2d", (32, 32), 1e-3, 0.0)
+    with pytest.raises(api.ConfigError):
+        g.step(1)
+
+
+def test_state_shape_error():
+    g = api.Simulation("ns2d", (32, 32), 1e-3, 1e-3)
+    with pytest.raises(api.ShapeError):
+        g.set_state(np.zeros((1, 32, 16), complex))
