@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- RK4 step of the pseudo-spectral NS solver on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config ns2d_4096|ns2d_1024|ns3d_128|ns3d_512]
+
+A "step" is one RK4 time step (Simulation::step_once, reference
+proj/src/simulation.cpp:535-555) of the BASELINE config on synthetic seeded
+input (paper_1807_01769_b200/ic.py), state resident in HBM.  Default workload:
+BASELINE.json configs[1], ns2d 4096^2, nu 1e-4, dt from CFL 0.5 on the IC
+(the largest single-GPU config the metric is quoted on).
+
+Our arm: W untimed steps, then K steps timed with CUDA events on the launch
+stream (bracketed by barrier + synchronize, max over ranks), per-kernel-class
+CUDA events inside the same region for the roofline, NVML clocks sampled
+during it.  Every field array is larger than L2 (126 MB), so no L2 flush is
+needed between steps.  `e2e` re-times the same metric through the public C
+ABI with host buffers: per step skg_set_state (pinned H2D) + skg_step(1) +
+skg_get_state (D2H).  `cpu_baseline` times the reference's own CPU step
+(oracle/_ref: proj/src compiled unmodified + oracle/fft_shim.c) on a bounded
+sample on this host.
+
+--impl reference: the reference CPU implementation alone (rank 0), same
+config/metric, K steps after W warm-up steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "pseudo-spectral NS RK4 ms/step & Gpts·steps/s; % of HBM/NVLink roofline"
+UNIT = "Gpts*steps/s"
+
+CONFIGS = {
+    # name: solver, n, nu, dt (None = CFL 0.5 on the IC), BASELINE steps
+    "ns2d_4096": ("ns2d", (4096, 4096), 1e-4, None, 20),
+    "ns2d_1024": ("ns2d", (1024, 1024), 1e-4, 1e-3, 10),
+    "ns3d_128": ("ns3d", (128, 128, 128), 1e-3, None, 10),
+    "ns3d_512": ("ns3d", (512, 512, 512), 2e-4, None, 10),
+}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(cfg_name):
+    """ncu dram bytes per launch of the dominant kernel, from the committed summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(cfg_name, {}).get("dominant_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons, sampled from a thread during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.reasons = 0
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def make_input(cfg_name):
+    from paper_1807_01769_b200 import ic
+    solver, n, nu, dt, _ = CONFIGS[cfg_name]
+    u0 = ic.initial_state(solver, n, seed=1234)
+    if dt is None:
+        dt = ic.cfl_dt(solver, n, u0, cfl=0.5)
+    return solver, n, nu, dt, u0
+
+
+def cpu_reference_rate(solver, n, nu, dt, u0, steps, warmup, threads):
+    """Reference CPU step (oracle/_ref) on this host; returns (s/step list, threads)."""
+    from oracle import ref
+    ref.set_workers(threads)
+    r = ref.RefSimulation(solver, n, nu, dt)
+    r.set_state(u0)
+    if warmup:
+        r.step(warmup)
+    times = [r.step(1) for _ in range(steps)]
+    r.close()
+    return times
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    solver, n, nu, dt, u0 = make_input(args.config)
+    P = int(np.prod(n))
+    threads = os.cpu_count() or 1
+    from oracle import ref
+    ref.set_workers(threads)
+    r = ref.RefSimulation(solver, n, nu, dt)
+    r.set_state(u0)
+    # warm-up as the reference's own bench protocol: one untimed step
+    # (proj/src/bench.cpp:79-82); then up to K steps within a time budget so
+    # the run stays within a few minutes (each step is a full step_once).
+    t_warm = r.step(1)
+    budget = args.ref_budget_s
+    times = []
+    while len(times) < args.steps and (sum(times) + (times[-1] if times else t_warm)) <= budget:
+        times.append(r.step(1))
+    if not times:
+        times.append(r.step(1))
+    r.close()
+    sec = sum(times) / len(times)
+    value = P / sec / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": len(times),
+        "requested_steps": args.steps, "warmup": 1, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded spectral Gaussian IC, BASELINE recipe)", "impl": "reference",
+        "config": {"workload": f"{args.config} RK4 step (step_once), nu={nu}, dt={dt:.6g}",
+                   "solver": solver, "n": list(n), "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{len(times)} step_once calls of {args.config} after "
+                                   f"1 warm-up (budget {budget:.0f} s); reference proj/src compiled "
+                                   f"unmodified, FFT = oracle/fft_shim.c (not FFTW)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_our_arm(args):
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1807_01769_b200 import api
+
+    solver, n, nu, dt, u0 = make_input(args.config)
+    P = int(np.prod(n))
+    S = u0.size  # complex modes over all variables
+    sim = api.Simulation(solver, n, nu, dt, device=local)
+    stream = torch.cuda.current_stream()
+    sim.set_stream(stream.cuda_stream)
+    sim.set_state(u0)
+    pruned = sim.pruned
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- warm-up
+    sim.step(args.warmup)
+    sim.reset_stats()
+    sim.set_timing(True)
+    l0 = sim.launch_count
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        start.record(stream)
+        sim.step_async(args.steps)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    sim.sync()
+    launches = sim.launch_count - l0
+    stats = sim.kernel_stats()
+    sim.set_timing(False)
+    ms = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * P * args.steps / (ms / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel class
+    peak, peak_src = load_peaks()
+    dom = max(stats, key=lambda k: stats[k][0])
+    dms, dn, dbytes = stats[dom]
+    achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9 if dn else 0.0
+    kernels = {k: {"ms_total": v[0], "launches": v[1],
+                   "avg_us": (v[0] / v[1] * 1e3) if v[1] else None,
+                   "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None,
+                   "share": v[0] / sum(x[0] for x in stats.values())} for k, v in stats.items()
+               if v[1]}
+    step_bytes = sum(v[2] for v in stats.values()) / args.steps
+    traffic = load_traffic(args.config)
+
+    # ---- e2e through the C ABI with host buffers
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    host_in = torch.empty(u0.shape, dtype=torch.complex128, pin_memory=True).numpy()
+    host_in[...] = u0
+    host_out = torch.empty(u0.shape, dtype=torch.complex128, pin_memory=True).numpy()
+    sim.set_stream(None)  # C-ABI default stream of the context
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sim.set_state(host_in)
+        sim.step(1)
+        sim.get_state(out=host_out)
+    t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = ws * P * e2e_steps / t_e2e / 1e9
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            times = cpu_reference_rate(solver, n, nu, dt, u0, args.cpu_steps, 1, threads)
+            sec = sum(times) / len(times)
+            cpu = {"value": P / sec / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{args.cpu_steps} step_once of {args.config} after 1 warm-up "
+                             f"({sec:.2f} s/step); reference proj/src compiled unmodified, "
+                             f"FFT = oracle/fft_shim.c (FFTW absent), {threads} threads"}
+        except Exception as exc:  # the oracle .so may be missing on a foreign box
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded spectral Gaussian IC, BASELINE recipe)",
+            "config": {
+                "workload": f"{args.config}: {solver} {'x'.join(map(str, n))} RK4 step, "
+                            f"nu={nu}, dt={dt:.6g} (CFL 0.5)",
+                "solver": solver, "n": list(n), "global_batch": ws,
+                "parallelism": "replicas" if ws > 1 else "single-gpu",
+                "l2": "every field array > 126 MB L2; no flush needed",
+                "dealiased_fast_path": pruned,
+            },
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_launch": dbytes / dn if dn else None,
+                         "step_algorithmic_GB": step_bytes / 1e9,
+                         "step_frac": (step_bytes / (ms_step / 1e3) / 1e9) / peak},
+            "kernels": kernels,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": S * 16,
+                    "d2h_bytes_per_step": S * 16, "steps": e2e_steps,
+                    "path": "skg_set_state(host) + skg_step(1) + skg_get_state(host)"},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="ns2d_4096")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

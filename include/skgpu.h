@@ -131,6 +131,17 @@ int skg_pruned(const skg_ctx* ctx);
 /* Number of kernel launches issued since the context was created. */
 long skg_launch_count(const skg_ctx* ctx);
 
+/* Per-kernel-class device timing for the roofline report: when enabled,
+ * CUDA events bracket every hot-path launch on the context stream.
+ * Classes: 0 x-inverse pass, 1 physical-space pass, 2 x-forward pass + RK,
+ * 3 other (3D y passes, decay, utilities).  skg_kernel_stats returns the
+ * accumulated device milliseconds, launch count and ALGORITHMIC bytes (the
+ * HBM bytes the kernel must move: fields crossing the pass boundary, read or
+ * written once) of one class since the last reset. */
+int skg_set_timing(skg_ctx* ctx, int enable);
+int skg_kernel_stats(skg_ctx* ctx, int cls, double* total_ms, long* launches, double* bytes);
+int skg_reset_stats(skg_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

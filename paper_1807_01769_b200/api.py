@@ -31,7 +31,8 @@ EXPORTS = [
     "skg_set_state_device", "skg_get_state_device", "skg_step", "skg_step_async", "skg_sync",
     "skg_iteration", "skg_time", "skg_tendency", "skg_fft_forward", "skg_fft_inverse",
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
-    "skg_energy", "skg_pruned", "skg_launch_count",
+    "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
+    "skg_reset_stats",
 ]
 
 
@@ -103,6 +104,9 @@ def load_library():
     L.skg_get_grid.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p]
     L.skg_last_divergence.argtypes = [vp, C.POINTER(C.c_long), ip]
     L.skg_energy.argtypes = [vp, dp, dp]
+    L.skg_set_timing.argtypes = [vp, C.c_int]
+    L.skg_kernel_stats.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_long), dp]
+    L.skg_reset_stats.argtypes = [vp]
     _lib = L
     return L
 
@@ -229,8 +233,12 @@ class Simulation:
                              f"{self.nvars} x {self.spect_shape}")
         self._call("skg_set_state", _ptr(s))
 
-    def get_state(self) -> np.ndarray:
-        out = np.empty((self.nvars,) + self.spect_shape, np.complex128)
+    def get_state(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.nvars,) + self.spect_shape, np.complex128)
+        elif (out.dtype != np.complex128 or not out.flags.c_contiguous
+              or out.size != self.nvars * int(np.prod(self.spect_shape))):
+            raise ShapeError("get_state: out must be a contiguous complex128 array of the state size")
         self._call("skg_get_state", _ptr(out))
         return out
 
@@ -311,6 +319,25 @@ class Simulation:
     @property
     def launch_count(self) -> int:
         return load_library().skg_launch_count(self._h)
+
+    KERNEL_CLASSES = ("x_inverse", "physical", "x_forward_rk", "other")
+
+    def set_timing(self, on: bool) -> None:
+        self._call("skg_set_timing", C.c_int(1 if on else 0))
+
+    def reset_stats(self) -> None:
+        self._call("skg_reset_stats")
+
+    def kernel_stats(self):
+        """{class: (total_ms, launches, algorithmic_bytes)} since the last reset."""
+        out = {}
+        for i, name in enumerate(self.KERNEL_CLASSES):
+            ms = C.c_double()
+            nl = C.c_long()
+            by = C.c_double()
+            self._call("skg_kernel_stats", C.c_int(i), C.byref(ms), C.byref(nl), C.byref(by))
+            out[name] = (ms.value, nl.value, by.value)
+        return out
 
     def energy_enstrophy(self):
         e = C.c_double()

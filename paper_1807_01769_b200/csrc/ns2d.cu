@@ -356,15 +356,30 @@ bool ns2d_supported(int nx, int ny) {
     return ok(nx) && ok(ny);
 }
 
-cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches) {
+cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches,
+                              const LaunchHook& hook) {
     cudaError_t err;
-    if ((err = dispatch_x(a, stage, true, s)) != cudaSuccess) return err;
-    if ((err = dispatch_y(a, s)) != cudaSuccess) return err;
-    if ((err = dispatch_x(a, stage, false, s)) != cudaSuccess) return err;
-    *launches += 3;
+    const double B = sizeof(cd);
     const bool final = a.rk2 ? stage == 2 : stage == 4;
+    const double kx_kept = a.pruned ? 2.0 * a.kcx + 1.0 : (double)a.nx;
+    const double s_in = kx_kept * a.ky_in;          // modes K1 reads per field
+    const double s_out = kx_kept * a.ld_o;          // modes K4 touches per field
+    const double inter = (double)a.nx * a.ky_in;    // one intermediate field
+    const double rows = (double)a.nx * a.ld_o;      // tendency rows
+    hook.begin(0);
+    if ((err = dispatch_x(a, stage, true, s)) != cudaSuccess) return err;
+    hook.end(0, B * (s_in * (stage == 1 ? 1.0 : 2.0) + 4.0 * inter));
+    hook.begin(1);
+    if ((err = dispatch_y(a, s)) != cudaSuccess) return err;
+    hook.end(1, B * (4.0 * inter + rows));
+    hook.begin(2);
+    if ((err = dispatch_x(a, stage, false, s)) != cudaSuccess) return err;
+    hook.end(2, B * (rows + (final ? (a.rk2 ? 3.0 : 5.0) * s_out : s_out)));
+    *launches += 3;
     if (final && !a.pruned && a.nh > a.kcy + 1) {
+        hook.begin(3);
         k4_decay<<<296, 256, 0, s>>>(a);
+        hook.end(3, B * 2.0 * a.nx * (a.nh - a.kcy - 1));
         *launches += 1;
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }

@@ -61,9 +61,23 @@ struct Ns2dArgs {
     DevFlags* flags;
 };
 
+// Optional per-launch instrumentation: hook(user, cls, 0, 0) before a launch
+// and hook(user, cls, 1, algorithmic_bytes) after it.
+struct LaunchHook {
+    void (*fn)(void* user, int cls, int phase, double bytes) = nullptr;
+    void* user = nullptr;
+    void begin(int cls) const {
+        if (fn) fn(user, cls, 0, 0.0);
+    }
+    void end(int cls, double bytes) const {
+        if (fn) fn(user, cls, 1, bytes);
+    }
+};
+
 // Launchers (ns2d.cu).  stage in 1..4 (RK4) or 1..2 (RK2); stage 0 = plain
 // tendency evaluation of u into k1 (no RK arithmetic).
-cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches);
+cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches,
+                              const LaunchHook& hook);
 bool ns2d_supported(int nx, int ny);
 
 // ---------------------------------------------------------------- ns3d

@@ -104,9 +104,69 @@ struct skg_ctx {
     int div_var = -1;
     long pending_steps = 0;
     double pending_dt = 0.0;
+
+    // per-kernel-class event timing (skg_set_timing)
+    struct Pending {
+        cudaEvent_t a, b;
+        int cls;
+        double bytes;
+    };
+    bool timing = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<Pending> pend;
+    cudaEvent_t cur = nullptr;
+    double st_ms[4] = {0, 0, 0, 0};
+    long st_n[4] = {0, 0, 0, 0};
+    double st_bytes[4] = {0, 0, 0, 0};
 };
 
 namespace {
+
+cudaEvent_t take_event(skg_ctx* c) {
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void timing_hook(void* user, int cls, int phase, double bytes) {
+    auto* c = static_cast<skg_ctx*>(user);
+    cudaEvent_t e = take_event(c);
+    cudaEventRecord(e, c->stream);
+    if (phase == 0) {
+        c->cur = e;
+    } else {
+        c->pend.push_back({c->cur, e, cls, bytes});
+        c->cur = nullptr;
+    }
+}
+
+skg::LaunchHook hook_of(skg_ctx* c) {
+    skg::LaunchHook h;
+    if (c->timing) {
+        h.fn = timing_hook;
+        h.user = c;
+    }
+    return h;
+}
+
+void harvest(skg_ctx* c) {
+    for (auto& p : c->pend) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            c->st_ms[p.cls] += ms;
+            c->st_n[p.cls] += 1;
+            c->st_bytes[p.cls] += p.bytes;
+        }
+        c->pool.push_back(p.a);
+        c->pool.push_back(p.b);
+    }
+    c->pend.clear();
+}
 
 int refresh_exp(skg_ctx* c, double dt) {
     if (dt == c->cached_dt) return SKG_OK;
@@ -184,6 +244,7 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
 
 int sync_and_check(skg_ctx* c, long nsteps, double dt) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    harvest(c);
     skg::DevFlags f;
     CUDA_TRY(cudaMemcpy(&f, c->flags, sizeof(f), cudaMemcpyDeviceToHost));
     if (f.diverged) {
@@ -214,9 +275,10 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     if (c->solver == 2) {
         skg::Ns2dArgs a = args2d(c, dt);
+        const skg::LaunchHook hook = hook_of(c);
         for (long s = 0; s < nsteps; ++s)
             for (int st = 1; st <= nst; ++st)
-                CUDA_TRY(skg::ns2d_launch_stage(a, st, c->stream, &c->launches));
+                CUDA_TRY(skg::ns2d_launch_stage(a, st, c->stream, &c->launches, hook));
     } else {
         return fail(SKG_EUNSUPPORTED, "ns3d step not built");
     }
@@ -379,6 +441,8 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->flags);
     cudaFree(c->d_count);
     cudaFree(c->d_red);
+    harvest(c);
+    for (auto e : c->pool) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
     return SKG_OK;
@@ -478,7 +542,7 @@ int skg_tendency(skg_ctx* c, const double* in, double* out) {
         a.u = c->k[2];
         skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-        CUDA_TRY(skg::ns2d_launch_stage(a, 1, c->stream, &c->launches));
+        CUDA_TRY(skg::ns2d_launch_stage(a, 1, c->stream, &c->launches, hook_of(c)));
         rc = store_state_to_io(c, c->k[0]);
         if (rc) return rc;
     } else {
@@ -585,6 +649,34 @@ int skg_get_grid(skg_ctx* c, int axis, double* k_axis, unsigned char* mask) {
 int skg_last_divergence(const skg_ctx* c, long* iteration, int* var) {
     *iteration = c->div_it;
     *var = c->div_var;
+    return SKG_OK;
+}
+
+int skg_set_timing(skg_ctx* c, int enable) {
+    c->timing = enable != 0;
+    return SKG_OK;
+}
+
+int skg_reset_stats(skg_ctx* c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    harvest(c);
+    for (int i = 0; i < 4; ++i) {
+        c->st_ms[i] = 0;
+        c->st_n[i] = 0;
+        c->st_bytes[i] = 0;
+    }
+    return SKG_OK;
+}
+
+int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, double* bytes) {
+    if (cls < 0 || cls > 3) return fail(SKG_ESHAPE, "kernel class out of range");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    harvest(c);
+    if (total_ms) *total_ms = c->st_ms[cls];
+    if (launches) *launches = c->st_n[cls];
+    if (bytes) *bytes = c->st_bytes[cls];
     return SKG_OK;
 }
 
