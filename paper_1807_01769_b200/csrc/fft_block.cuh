@@ -160,24 +160,122 @@ __device__ __forceinline__ void dft(cd* x) {
 
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 
+// u[r] *= w^r, r = 1..R-1, where w = W_N^m (forward sign) from the table and
+// the direction S conjugates it.  Powers are generated in registers so a pass
+// issues one table load per butterfly instead of R-1.  Radix 16 uses the
+// 4x4 split w^(4 n1 + n2) = (w^4)^n1 w^n2 to keep few powers live.
+template <int S, int R>
+__device__ __forceinline__ void apply_twiddles(cd* u, cd w) {
+    if constexpr (S > 0) w = conj(w);
+    if constexpr (R == 2) {
+        u[1] = mul(u[1], w);
+    } else if constexpr (R == 4) {
+        const cd w2 = mul(w, w);
+        u[1] = mul(u[1], w);
+        u[2] = mul(u[2], w2);
+        u[3] = mul(u[3], mul(w2, w));
+    } else if constexpr (R == 8) {
+        const cd w2 = mul(w, w);
+        const cd w3 = mul(w2, w);
+        const cd w4 = mul(w2, w2);
+        u[1] = mul(u[1], w);
+        u[2] = mul(u[2], w2);
+        u[3] = mul(u[3], w3);
+        u[4] = mul(u[4], w4);
+        u[5] = mul(u[5], mul(w4, w));
+        u[6] = mul(u[6], mul(w4, w2));
+        u[7] = mul(u[7], mul(w4, w3));
+    } else {
+        static_assert(R == 16, "radix");
+        const cd w2 = mul(w, w);
+        const cd w3 = mul(w2, w);
+#pragma unroll
+        for (int n1 = 0; n1 < 4; ++n1) {
+            u[4 * n1 + 1] = mul(u[4 * n1 + 1], w);
+            u[4 * n1 + 2] = mul(u[4 * n1 + 2], w2);
+            u[4 * n1 + 3] = mul(u[4 * n1 + 3], w3);
+        }
+        const cd w4 = mul(w2, w2);
+        const cd w8 = mul(w4, w4);
+        const cd w12 = mul(w8, w4);
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) {
+            u[4 + n2] = mul(u[4 + n2], w4);
+            u[8 + n2] = mul(u[8 + n2], w8);
+            u[12 + n2] = mul(u[12 + n2], w12);
+        }
+    }
+}
+
 // Block FFT of a power-of-two length N in natural layout.
 template <int N>
 struct BFFT {
     static_assert((N & (N - 1)) == 0 && N >= 2, "power-of-two length");
     static constexpr int E = N < 16 ? N : 16;  // elements per thread
     static constexpr int T = N / E;            // threads per line
-    static constexpr int PADSH = ilog2c(E);    // one pad slot per E elements
-    static constexpr int SMEM = N + (N >> PADSH) + 1;  // cd slots per line
-    __device__ __forceinline__ static int pad(int i) { return i + (i >> PADSH); }
+    static constexpr int SH = ilog2c(E);
+    // Exchange buffer: N slots, XOR-swizzled on the 16-byte slot within each
+    // 128-byte line so the stride-E writes of the first pass and the
+    // unit-stride reads are both conflict-free (no padding).
+    static constexpr int SMEM = N;
+    __device__ __forceinline__ static int pad(int i) {
+        if constexpr (E >= 8) return i ^ ((i >> SH) & 7);
+        else return i;
+    }
 
-    // One pass, then recurse.  tw: W_N^m table (forward sign).
-    template <int S, int Ns>
-    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const cd* __restrict__ tw) {
+    static constexpr int npasses() {
+        int p = 0;
+        for (int ns = 1; ns < N; ns *= (N / ns >= 16 ? 16 : N / ns)) ++p;
+        return p;
+    }
+    static constexpr int NP = npasses();
+
+    // Per-thread twiddle bases, one per pass after the first:
+    // w[p] = W_N^{(t mod Ns_p) * N / (Ns_p R_p)}.  Loaded once per kernel so
+    // no global load sits between a barrier and the butterflies.
+    struct Bases {
+        cd w[NP > 1 ? NP - 1 : 1];
+    };
+    __device__ __forceinline__ static Bases bases(int t, const cd* __restrict__ tw) {
+        Bases b;
+        int ns = 1;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const int R = N / ns >= 16 ? 16 : N / ns;
+            if (p > 0) b.w[p - 1] = __ldg(&tw[(t & (ns - 1)) * (N / (ns * R))]);
+            ns *= R;
+        }
+        return b;
+    }
+
+    // w * W_E^q (forward sign), q a compile-time constant after unrolling.
+    template <int Q>
+    __device__ __forceinline__ static cd twq(cd w) {
+        if constexpr (Q == 0) return w;
+        else return twc<-1, Q, E>(w);
+    }
+    __device__ __forceinline__ static cd twc_e(cd w, int b) {
+        cd r = w;
+#define SKG_TWQ(Q) \
+    if constexpr (Q < E) {  \
+        if (b == Q) r = twq<Q>(w); \
+    }
+        SKG_TWQ(1) SKG_TWQ(2) SKG_TWQ(3) SKG_TWQ(4) SKG_TWQ(5) SKG_TWQ(6) SKG_TWQ(7)
+        SKG_TWQ(8) SKG_TWQ(9) SKG_TWQ(10) SKG_TWQ(11) SKG_TWQ(12) SKG_TWQ(13) SKG_TWQ(14)
+        SKG_TWQ(15)
+#undef SKG_TWQ
+        return r;
+    }
+
+    // One pass, then recurse.
+    template <int S, int Ns, int P>
+    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const Bases& wb) {
         constexpr int rem = N / Ns;
         constexpr int R = rem >= 16 ? 16 : rem;
-        constexpr int B = E / R;  // butterflies per thread in this pass
+        constexpr int B = E / R;  // butterflies per thread in this pass (> 1 only in the last)
         constexpr bool last = (Ns * R == N);
         static_assert(E % R == 0, "radix must divide elements per thread");
+        static_assert(B == 1 || last, "multi-butterfly passes only at the end");
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             const int j = t + T * b;
@@ -186,12 +284,9 @@ struct BFFT {
             for (int r = 0; r < R; ++r) u[r] = v[b + r * B];
             const int jm = j & (Ns - 1);
             if constexpr (Ns > 1) {
-                constexpr int step = N / (Ns * R);
-#pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    cd w = __ldg(&tw[jm * r * step]);
-                    u[r] = S < 0 ? mul(u[r], w) : mulconj(u[r], w);
-                }
+                // last pass: W_N^{t + T b} = W_N^t W_E^b (step 1, jm = j)
+                const cd w = b > 0 ? twc_e(wb.w[P - 1], b) : wb.w[P - 1];
+                apply_twiddles<S, R>(u, w);
             }
             dft<R, S>(u);
             if constexpr (last) {
@@ -208,21 +303,17 @@ struct BFFT {
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e)];
             __syncthreads();
-            pass<S, Ns * R>(v, sm, t, tw);
+            pass<S, Ns * R, P + 1>(v, sm, t, wb);
         }
     }
 
     template <int S>
-    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const cd* __restrict__ tw) {
-        pass<S, 1>(v, sm, t, tw);
+    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const Bases& wb) {
+        pass<S, 1, 0>(v, sm, t, wb);
     }
-
-    // Number of __syncthreads() a run issues (callers with inactive lines
-    // must still participate).
-    static constexpr int passes() {
-        int p = 0;
-        for (int ns = 1; ns < N; ns *= (N / ns >= 16 ? 16 : N / ns)) ++p;
-        return p;
+    template <int S>
+    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const cd* __restrict__ tw) {
+        pass<S, 1, 0>(v, sm, t, bases(t, tw));
     }
 };
 

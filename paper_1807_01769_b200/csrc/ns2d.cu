@@ -56,55 +56,76 @@ __device__ __forceinline__ cd stage_input(const Ns2dArgs& a, int stage, int ky, 
     }
 }
 
-template <int NX>
-__global__ void __launch_bounds__(256, 2) k1_xinv(Ns2dArgs a, int stage) {
+// PZ: the state is dealiased and the kept |kx| <= kcx < 6T, so the elements
+// e in [6, 10) of every thread (kx in [6T, 10T)) are exactly zero: they are
+// neither loaded nor stored, and the stage-state slots shrink from 16 to 12.
+template <int NX, bool PZ>
+__global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E;
     constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    constexpr int ZLO = PZ ? 6 : E, ZHI = PZ ? 10 : E;
+    constexpr int NS = E - (ZHI - ZLO);  // stage-state slots per thread
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
     const int ky = blockIdx.x * LPC + l;
     const bool active = ky < a.ky_in;
     if (a.flags->diverged) return;
-    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.flags != nullptr)
-        atomicAdd(&a.flags->steps, 1);
-    cd* sm = smem + l * F::SMEM;
+    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.flags->steps, 1);
+    cd* sm = smem + l * (F::SMEM + NS * T);
+    cd* sv = sm + F::SMEM;  // thread-private slots sv[slot * T + t]
     const double kyv = a.ky_scale * (double)ky;
+    const typename F::Bases wb = F::bases(t, a.twx);
+    // RK stage state w, computed once per column (time_stepping.cpp:128-170),
+    // kept as psi = w/|k|^2 (grid.cpp:262-270): the four x-multipliers are then
+    // psi, kx psi, kx |k|^2 psi, |k|^2 psi -- no division inside the loop.
+    // (|k|^2 psi differs from w in the last bit and is 0 at k = 0, where w
+    // only feeds columns multiplied by kx = 0 or ky = 0.)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= ZLO && e < ZHI) continue;
+        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+        const int i = t + T * e;
+        const int si = signed_index(i, NX);
+        const bool keep = active && (!a.pruned || abs(si) <= a.kcx);
+        cd psi = zero();
+        if (keep) {
+            const cd s = stage_input(a, stage, ky, i, (size_t)ky * NX + i);
+            const double kxv = a.kx_scale * (double)si;
+            const double ksq = kxv * kxv + kyv * kyv;
+            if (ksq != 0.0) psi = mk(s.x / ksq, s.y / ksq);
+        }
+        sv[slot * T + t] = psi;
+    }
 #pragma unroll 1
     for (int m = 0; m < 4; ++m) {
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int i = t + T * e;
-            const int si = signed_index(i, NX);
-            const bool keep = active && (!a.pruned || abs(si) <= a.kcx);
-            cd s = zero();
-            if (keep) s = stage_input(a, stage, ky, i, (size_t)ky * NX + i);
-            const double kxv = a.kx_scale * (double)si;
-            cd r;
-            if (m == 0 || m == 1) {
-                const double ksq = kxv * kxv + kyv * kyv;
-                cd psi = ksq == 0.0 ? zero() : mk(s.x / ksq, s.y / ksq);
-                r = m == 0 ? psi : scale(psi, kxv);
-            } else {
-                r = m == 2 ? scale(s, kxv) : s;
+            if (e >= ZLO && e < ZHI) {
+                v[e] = zero();
+                continue;
             }
-            v[e] = r;
+            const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+            const cd psi = sv[slot * T + t];
+            const double kxv = a.kx_scale * (double)signed_index(t + T * e, NX);
+            const double ksq = kxv * kxv + kyv * kyv;
+            double f = m == 0 ? 1.0 : m == 1 ? kxv : m == 2 ? kxv * ksq : ksq;
+            v[e] = scale(psi, f);
         }
-        F::template run<+1>(v, sm, t, a.twx);
+        F::template run<+1>(v, sm, t, wb);
         if (active) {
             cd* out = a.I[m];
 #pragma unroll
             for (int e = 0; e < E; ++e) out[(size_t)(t + T * e) * a.ld_i + ky] = v[e];
         }
-        if constexpr (F::T > 1) __syncthreads();  // sm reused by the next field
     }
 }
 
 // -(ux dx w + uy dy w) of row x in natural layout (y = t + T e).
 template <int NY>
 __device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool active, cd* sm, int t,
-                                            double* acc) {
+                                            double* acc, const typename BFFT<NY>::Bases& wb) {
     using F = BFFT<NY>;
     constexpr int T = F::T, E = F::E;
     const size_t row = (size_t)x * a.ld_i;
@@ -138,7 +159,7 @@ __device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool activ
             // packed spectrum of (a + i b) over the full ky range
             v[e] = mirror ? mk(ah.x + bh.y, bh.x - ah.y) : mk(ah.x - bh.y, ah.y + bh.x);
         }
-        F::template run<+1>(v, sm, t, a.twy);
+        F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const double p = v[e].x * v[e].y;
@@ -160,21 +181,22 @@ __global__ void __launch_bounds__(256, 2) k3_phys(Ns2dArgs a) {
     if (a.flags->diverged) return;
     cd* sm = smem + g * SLOT;
     double* prow = reinterpret_cast<double*>(sm + F::SMEM);
+    const typename F::Bases wb = F::bases(t, a.twy);
     {
         double acc[E];
-        row_product<NY>(a, xa, active, sm, t, acc);
+        row_product<NY>(a, xa, active, sm, t, acc, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) prow[t + T * e] = acc[e];
     }
     cd v[E];
     {
         double acc[E];
-        row_product<NY>(a, xa + 1, active, sm, t, acc);
+        row_product<NY>(a, xa + 1, active, sm, t, acc, wb);
         // forward r2c of both rows packed: z = prod_a + i prod_b
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = mk(prow[t + T * e], acc[e]);
     }
-    F::template run<-1>(v, sm, t, a.twy);
+    F::template run<-1>(v, sm, t, wb);
 #pragma unroll
     for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
     __syncthreads();
@@ -283,30 +305,44 @@ __global__ void k4_decay(Ns2dArgs a) {
     }
 }
 
+template <int NX, bool PZ>
+cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T, E = F::E;
+    constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    constexpr int NS = PZ ? E - 4 : E;
+    const size_t smem = sizeof(cd) * (F::SMEM + NS * T) * LPC;
+    const int grid = (a.ky_in + LPC - 1) / LPC;
+    if (grid == 0) return cudaSuccess;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k1_xinv<NX, PZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = true;
+    }
+    k1_xinv<NX, PZ><<<grid, T * LPC, smem, s>>>(a, stage);
+    return cudaGetLastError();
+}
+
 template <int NX>
 cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
     using F = BFFT<NX>;
     constexpr int T = F::T;
     constexpr int LPC = T >= 256 ? 1 : 256 / T;
-    const size_t smem = sizeof(cd) * F::SMEM * LPC;
-    const int cols = inverse ? a.ky_in : a.ld_o;
-    const int grid = (cols + LPC - 1) / LPC;
-    if (grid == 0) return cudaSuccess;
     if (inverse) {
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(k1_xinv<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            init = true;
+        if constexpr (NX >= 64) {
+            if (a.pruned && a.kcx <= 6 * T - 1) return launch_k1<NX, true>(a, stage, s);
         }
-        k1_xinv<NX><<<grid, T * LPC, smem, s>>>(a, stage);
-    } else {
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(k4_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            init = true;
-        }
-        k4_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
+        return launch_k1<NX, false>(a, stage, s);
     }
+    const size_t smem = sizeof(cd) * F::SMEM * LPC;
+    const int grid = (a.ld_o + LPC - 1) / LPC;
+    if (grid == 0) return cudaSuccess;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k4_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = true;
+    }
+    k4_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
 
