@@ -27,6 +27,19 @@ namespace skg {
 
 namespace {
 
+// Row-pair interleaved layout of the x-space intermediates and tendency rows:
+// element (x, ky) of a [nx][ld] field lives at ((x/2) ld + ky) 2 + (x mod 2).
+// The y pass (k3_phys) works on row pairs, so each pair is one contiguous
+// block; the strided x passes touch 32-byte chunks (two adjacent x of one
+// ky column) instead of 16-byte ones.
+__device__ __forceinline__ size_t pidx(int x, int ky, int ld) {
+    return ((size_t)(x >> 1) * ld + ky) * 2 + (x & 1);
+}
+
+__device__ __forceinline__ cd* pick(const Ns2dArgs& a, int m) {
+    return m == 0 ? a.I[0] : m == 1 ? a.I[1] : m == 2 ? a.I[2] : a.I[3];
+}
+
 __device__ __forceinline__ bool finite2(cd v) { return isfinite(v.x) && isfinite(v.y); }
 
 // RK stage state at (kx index i, ky index j) from u and the previous k.
@@ -115,9 +128,9 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
         }
         F::template run<+1>(v, sm, t, wb);
         if (active) {
-            cd* out = a.I[m];
+            cd* out = pick(a, m);
 #pragma unroll
-            for (int e = 0; e < E; ++e) out[(size_t)(t + T * e) * a.ld_i + ky] = v[e];
+            for (int e = 0; e < E; ++e) out[pidx(t + T * e, ky, a.ld_i)] = v[e];
         }
     }
 }
@@ -128,11 +141,11 @@ __device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool activ
                                             double* acc, const typename BFFT<NY>::Bases& wb) {
     using F = BFFT<NY>;
     constexpr int T = F::T, E = F::E;
-    const size_t row = (size_t)x * a.ld_i;
+    const size_t row = (size_t)(x >> 1) * a.ld_i * 2 + (x & 1);
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
-        const cd* P = a.I[q == 0 ? 0 : 1];  // X[psi] | X[kx psi]
-        const cd* Q = a.I[q == 0 ? 2 : 3];  // X[kx w] | X[w]
+        const cd* P = pick(a, q == 0 ? 0 : 1);  // X[psi] | X[kx psi]
+        const cd* Q = pick(a, q == 0 ? 2 : 3);  // X[kx w] | X[w]
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -142,8 +155,8 @@ __device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool activ
             cd ah = zero(), bh = zero();
             if (active && ki < a.ky_in) {
                 const double kyv = a.ky_scale * (double)ki;
-                cd p = P[row + ki];
-                cd qq = Q[row + ki];
+                cd p = P[row + 2 * (size_t)ki];
+                cd qq = Q[row + 2 * (size_t)ki];
                 if (q == 0) {
                     ah = mk(-kyv * p.y, kyv * p.x);   // ux: i ky X[psi]
                     bh = muli(qq);                    // dx w: i X[kx w]
@@ -202,13 +215,12 @@ __global__ void __launch_bounds__(256, 2) k3_phys(Ns2dArgs a) {
     __syncthreads();
     if (active) {
         const double h = 0.5 * a.inv_n;
-        cd* ra = a.nl + (size_t)xa * a.ld_o;
-        cd* rb = ra + a.ld_o;
+        cd* rp = a.nl + (size_t)(xa >> 1) * a.ld_o * 2;  // row pair block
         for (int k = t; k < a.ld_o; k += T) {
             cd zk = sm[F::pad(k)];
             cd zm = sm[F::pad((NY - k) & (NY - 1))];
-            ra[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-            rb[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+            rp[2 * k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+            rp[2 * k + 1] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
         }
     }
 }
@@ -227,7 +239,7 @@ __global__ void __launch_bounds__(256, 2) k4_xfwd(Ns2dArgs a, int stage) {
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.nl[(size_t)(t + T * e) * a.ld_o + ky] : zero();
+        v[e] = active ? a.nl[pidx(t + T * e, ky, a.ld_o)] : zero();
     F::template run<-1>(v, sm, t, a.twx);
     if (!active) return;
     const bool final = a.rk2 ? stage == 2 : stage == 4;
