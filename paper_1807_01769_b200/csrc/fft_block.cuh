@@ -207,25 +207,34 @@ __device__ __forceinline__ void apply_twiddles(cd* u, cd w) {
     }
 }
 
-// Block FFT of a power-of-two length N in natural layout.
-template <int N>
+// Block FFT of a power-of-two length N in natural layout.  SPLIT exchanges
+// the real and imaginary parts in two rounds through an N-double buffer
+// (half the shared memory, twice the barriers).
+template <int N, bool SPLIT = false, int EMAX = 16>
 struct BFFT {
     static_assert((N & (N - 1)) == 0 && N >= 2, "power-of-two length");
-    static constexpr int E = N < 16 ? N : 16;  // elements per thread
+    static_assert(EMAX == 8 || EMAX == 16, "8 or 16 elements per thread");
+    static constexpr int E = N < EMAX ? N : EMAX;  // elements per thread
     static constexpr int T = N / E;            // threads per line
     static constexpr int SH = ilog2c(E);
     // Exchange buffer: N slots, XOR-swizzled on the 16-byte slot within each
     // 128-byte line so the stride-E writes of the first pass and the
     // unit-stride reads are both conflict-free (no padding).
-    static constexpr int SMEM = N;
+    static constexpr int SMEM = SPLIT ? (N + 1) / 2 : N;  // in cd (16-byte) units
     __device__ __forceinline__ static int pad(int i) {
         if constexpr (E >= 8) return i ^ ((i >> SH) & 7);
+        else return i;
+    }
+    // 8-byte slots: XOR the slot within each 128-byte line.
+    __device__ __forceinline__ static int pad8(int i) {
+        if constexpr (E >= 16) return i ^ ((i >> 4) & 15);
+        else if constexpr (E == 8) return i ^ ((i >> 4) & 7);
         else return i;
     }
 
     static constexpr int npasses() {
         int p = 0;
-        for (int ns = 1; ns < N; ns *= (N / ns >= 16 ? 16 : N / ns)) ++p;
+        for (int ns = 1; ns < N; ns *= (N / ns >= E ? E : N / ns)) ++p;
         return p;
     }
     static constexpr int NP = npasses();
@@ -241,7 +250,7 @@ struct BFFT {
         int ns = 1;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const int R = N / ns >= 16 ? 16 : N / ns;
+            const int R = N / ns >= E ? E : N / ns;
             if (p > 0) b.w[p - 1] = __ldg(&tw[(t & (ns - 1)) * (N / (ns * R))]);
             ns *= R;
         }
@@ -271,7 +280,7 @@ struct BFFT {
     template <int S, int Ns, int P>
     __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const Bases& wb) {
         constexpr int rem = N / Ns;
-        constexpr int R = rem >= 16 ? 16 : rem;
+        constexpr int R = rem >= E ? E : rem;
         constexpr int B = E / R;  // butterflies per thread in this pass (> 1 only in the last)
         constexpr bool last = (Ns * R == N);
         static_assert(E % R == 0, "radix must divide elements per thread");
@@ -289,7 +298,7 @@ struct BFFT {
                 apply_twiddles<S, R>(u, w);
             }
             dft<R, S>(u);
-            if constexpr (last) {
+            if constexpr (last || SPLIT) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) v[b + r * B] = u[r];
             } else {
@@ -299,10 +308,28 @@ struct BFFT {
             }
         }
         if constexpr (!last) {
-            __syncthreads();
+            if constexpr (SPLIT) {
+                // B == 1 here: element r goes to base + r Ns
+                double* sd = reinterpret_cast<double*>(sm);
+                const int base = (t / Ns) * Ns * R + (t & (Ns - 1));
 #pragma unroll
-            for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e)];
-            __syncthreads();
+                for (int r = 0; r < R; ++r) sd[pad8(base + r * Ns)] = v[r].x;
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e].x = sd[pad8(t + T * e)];
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < R; ++r) sd[pad8(base + r * Ns)] = v[r].y;
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e].y = sd[pad8(t + T * e)];
+                __syncthreads();
+            } else {
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e)];
+                __syncthreads();
+            }
             pass<S, Ns * R, P + 1>(v, sm, t, wb);
         }
     }

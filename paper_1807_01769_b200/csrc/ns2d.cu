@@ -135,17 +135,58 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
     }
 }
 
-// -(ux dx w + uy dy w) of row x in natural layout (y = t + T e).
-template <int NY>
-__device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool active, cd* sm, int t,
-                                            double* acc, const typename BFFT<NY>::Bases& wb) {
-    using F = BFFT<NY>;
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// y pass on a row pair (xa, xa+1).  Four inverse FFTs k = 0..3 over
+// (row, field pair) = (xa, q0), (xa, q1), (xa+1, q0), (xa+1, q1), where
+// q0 = (X[psi], X[kx w]) -> ux + i dx w and q1 = (X[kx psi], X[w]) -> uy + i dy w;
+// the input rows of FFT k+1 stream into a shared-memory stage (cp.async)
+// while FFT k runs.  Shared memory per group: split exchange (N doubles),
+// the finished row-a product (N doubles), stage (2 ld_i complex).
+template <int NY, int EM>
+__global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, EM>::T : 256,
+                                  EM == 8 ? 65536 / 64 / (BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, EM>::T : 256) : 2)
+    k3_phys(Ns2dArgs a) {
+    using F = BFFT<NY, true, EM>;
     constexpr int T = F::T, E = F::E;
-    const size_t row = (size_t)(x >> 1) * a.ld_i * 2 + (x & 1);
+    constexpr int G = T >= 256 ? 1 : 256 / T;
+    extern __shared__ cd smem[];
+    const int ld = a.ld_i;
+    const int slot = F::SMEM + NY / 2 + 2 * ld;
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const int xa = 2 * (blockIdx.x * G + g);
+    const bool active = xa < a.nx;
+    if (a.flags->diverged) return;
+    cd* sm = smem + g * slot;
+    double* prow = reinterpret_cast<double*>(sm + F::SMEM);
+    cd* st = sm + F::SMEM + NY / 2;
+    const typename F::Bases wb = F::bases(t, a.twy);
+
+    auto issue = [&](int k) {
+        if (!active) return;
+        const int x = xa + (k >> 1), q = k & 1;
+        const cd* P = pick(a, q ? 1 : 0);
+        const cd* Q = pick(a, q ? 3 : 2);
+        for (int i = t; i < a.ky_in; i += T) {
+            cp_async16(&st[i], P + pidx(x, i, ld));
+            cp_async16(&st[ld + i], Q + pidx(x, i, ld));
+        }
+    };
+    issue(0);
+    cp_async_commit();
+    double acc[E];
 #pragma unroll 1
-    for (int q = 0; q < 2; ++q) {
-        const cd* P = pick(a, q == 0 ? 0 : 1);  // X[psi] | X[kx psi]
-        const cd* Q = pick(a, q == 0 ? 2 : 3);  // X[kx w] | X[w]
+    for (int k = 0; k < 4; ++k) {
+        const int q = k & 1;
+        cp_async_wait_all();
+        __syncthreads();
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -155,8 +196,8 @@ __device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool activ
             cd ah = zero(), bh = zero();
             if (active && ki < a.ky_in) {
                 const double kyv = a.ky_scale * (double)ki;
-                cd p = P[row + 2 * (size_t)ki];
-                cd qq = Q[row + 2 * (size_t)ki];
+                const cd p = st[ki];
+                const cd qq = st[ld + ki];
                 if (q == 0) {
                     ah = mk(-kyv * p.y, kyv * p.x);   // ux: i ky X[psi]
                     bh = muli(qq);                    // dx w: i X[kx w]
@@ -172,53 +213,38 @@ __device__ __forceinline__ void row_product(const Ns2dArgs& a, int x, bool activ
             // packed spectrum of (a + i b) over the full ky range
             v[e] = mirror ? mk(ah.x + bh.y, bh.x - ah.y) : mk(ah.x - bh.y, ah.y + bh.x);
         }
+        __syncthreads();  // stage consumed
+        if (k < 3) issue(k + 1);
+        cp_async_commit();
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const double p = v[e].x * v[e].y;
-            acc[e] = q == 0 ? p : -(acc[e] + p);
+            const double p = v[e].x * v[e].y;  // ux dx w | uy dy w
+            if (q == 0) {
+                acc[e] = p;
+            } else {
+                const double fin = -(acc[e] + p);  // solvers.cpp:162-163
+                if (k == 1) prow[t + T * e] = fin;
+                else acc[e] = fin;
+            }
         }
     }
-}
-
-template <int NY>
-__global__ void __launch_bounds__(256, 2) k3_phys(Ns2dArgs a) {
-    using F = BFFT<NY>;
-    constexpr int T = F::T, E = F::E;
-    constexpr int G = T >= 256 ? 1 : 256 / T;
-    constexpr int SLOT = F::SMEM + NY / 2;  // exchange + one row of doubles
-    extern __shared__ cd smem[];
-    const int g = threadIdx.x / T, t = threadIdx.x % T;
-    const int xa = 2 * (blockIdx.x * G + g);
-    const bool active = xa < a.nx;
-    if (a.flags->diverged) return;
-    cd* sm = smem + g * SLOT;
-    double* prow = reinterpret_cast<double*>(sm + F::SMEM);
-    const typename F::Bases wb = F::bases(t, a.twy);
-    {
-        double acc[E];
-        row_product<NY>(a, xa, active, sm, t, acc, wb);
-#pragma unroll
-        for (int e = 0; e < E; ++e) prow[t + T * e] = acc[e];
-    }
+    // forward r2c of both rows packed: z = prod_a + i prod_b
     cd v[E];
-    {
-        double acc[E];
-        row_product<NY>(a, xa + 1, active, sm, t, acc, wb);
-        // forward r2c of both rows packed: z = prod_a + i prod_b
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = mk(prow[t + T * e], acc[e]);
-    }
+    for (int e = 0; e < E; ++e) v[e] = mk(prow[t + T * e], acc[e]);
     F::template run<-1>(v, sm, t, wb);
+    // exchange + prow form one contiguous N-complex buffer now
+    using FF = BFFT<NY, false, EM>;
 #pragma unroll
-    for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+    for (int e = 0; e < E; ++e) sm[FF::pad(t + T * e)] = v[e];
     __syncthreads();
     if (active) {
         const double h = 0.5 * a.inv_n;
         cd* rp = a.nl + (size_t)(xa >> 1) * a.ld_o * 2;  // row pair block
         for (int k = t; k < a.ld_o; k += T) {
-            cd zk = sm[F::pad(k)];
-            cd zm = sm[F::pad((NY - k) & (NY - 1))];
+            cd zk = sm[FF::pad(k)];
+            cd zm = sm[FF::pad((NY - k) & (NY - 1))];
             rp[2 * k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
             rp[2 * k + 1] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
         }
@@ -360,18 +386,19 @@ cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s)
 
 template <int NY>
 cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
-    using F = BFFT<NY>;
+    constexpr int EM = 16;
+    using F = BFFT<NY, true, EM>;
     constexpr int T = F::T;
     constexpr int G = T >= 256 ? 1 : 256 / T;
-    const size_t smem = sizeof(cd) * (F::SMEM + NY / 2) * G;
+    const size_t smem = sizeof(cd) * (F::SMEM + NY / 2 + 2 * a.ld_i) * G;
     const int pairs = a.nx / 2;
     const int grid = (pairs + G - 1) / G;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(k3_phys<NY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = true;
+    static size_t init = 0;
+    if (init < smem) {
+        cudaFuncSetAttribute(k3_phys<NY, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = smem;
     }
-    k3_phys<NY><<<grid, T * G, smem, s>>>(a);
+    k3_phys<NY, EM><<<grid, T * G, smem, s>>>(a);
     return cudaGetLastError();
 }
 

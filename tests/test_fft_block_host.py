@@ -28,11 +28,12 @@ def emu(tmp_path_factory):
 
 @pytest.mark.parametrize("n", [4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
 @pytest.mark.parametrize("sign", [-1, 1])
-def test_block_fft_matches_numpy(emu, n, sign):
+@pytest.mark.parametrize("split", [0, 1, 2, 3])
+def test_block_fft_matches_numpy(emu, n, sign, split):
     rng = np.random.default_rng(n)
     x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
     inp = "\n".join(f"{c.real:.17g} {c.imag:.17g}" for c in x)
-    r = subprocess.run([str(emu), str(n), str(sign)], input=inp, capture_output=True, text=True,
+    r = subprocess.run([str(emu), str(n), str(sign), str(split)], input=inp, capture_output=True, text=True,
                        timeout=120)
     assert r.returncode == 0
     y = np.array([complex(*map(float, l.split())) for l in r.stdout.splitlines()])
