@@ -277,8 +277,10 @@ struct BFFT {
     }
 
     // One pass, then recurse.
+    // salt (0..7) is XORed into the 16-byte slot index: lines interleaved
+    // lane-by-lane in one warp (strided-axis kernels) then hit distinct banks.
     template <int S, int Ns, int P>
-    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const Bases& wb) {
+    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const Bases& wb, int salt) {
         constexpr int rem = N / Ns;
         constexpr int R = rem >= E ? E : rem;
         constexpr int B = E / R;  // butterflies per thread in this pass (> 1 only in the last)
@@ -304,7 +306,7 @@ struct BFFT {
             } else {
                 const int base = (j / Ns) * Ns * R + jm;
 #pragma unroll
-                for (int r = 0; r < R; ++r) sm[pad(base + r * Ns)] = u[r];
+                for (int r = 0; r < R; ++r) sm[pad(base + r * Ns) ^ salt] = u[r];
             }
         }
         if constexpr (!last) {
@@ -327,20 +329,21 @@ struct BFFT {
             } else {
                 __syncthreads();
 #pragma unroll
-                for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e)];
+                for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e) ^ salt];
                 __syncthreads();
             }
-            pass<S, Ns * R, P + 1>(v, sm, t, wb);
+            pass<S, Ns * R, P + 1>(v, sm, t, wb, salt);
         }
     }
 
     template <int S>
-    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const Bases& wb) {
-        pass<S, 1, 0>(v, sm, t, wb);
+    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const Bases& wb, int salt = 0) {
+        pass<S, 1, 0>(v, sm, t, wb, salt);
     }
     template <int S>
-    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const cd* __restrict__ tw) {
-        pass<S, 1, 0>(v, sm, t, bases(t, tw));
+    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const cd* __restrict__ tw,
+                                               int salt = 0) {
+        pass<S, 1, 0>(v, sm, t, bases(t, tw), salt);
     }
 };
 

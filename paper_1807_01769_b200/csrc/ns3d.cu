@@ -1,0 +1,598 @@
+// ns3d.cu -- fused RK stage of the 3D rotational-form solver on sm_100a.
+//
+// Ns3dSolver::tendency (reference proj/src/solvers.cpp:299-339):
+//   w = curl v (grid.cpp:182-207); u, w <- 6 c2r; c = u x w (solvers.cpp:321-325);
+//   3 r2c; Leray projection (grid.cpp:227-249); dealias; mean 0.
+// One RK stage = five kernels, each one 1D FFT pass with the pointwise work
+// fused into its prologue / epilogue (SURVEY.md 8(a), ns3d mapping):
+//   k1_3d  x-inverse per (ky, kz) line: RK stage state (time_stepping.cpp:
+//          128-170) of vx, vy, vz -> X[vx], X[vy], X[vz], X[kx vy], X[kx vz]
+//   k2_3d  y-inverse per (x, kz) line: the three velocities and the three
+//          vorticity components (ky, kz factors applied here)
+//   k3_3d  z pass per pair of (x, y) rows: 6 c2r (3 packed complex FFTs),
+//          u x w, 3 r2c (2 packed FFTs per row pair + 1 shared), *1/N
+//   k2f_3d y-forward per (x, kz) line, kept ky only
+//   k4_3d  x-forward per (ky, kz) line, projection, dealias, mean 0, RK
+//          update and the check_finite guard (simulation.cpp:557-563)
+// Strided-axis kernels map consecutive lanes to consecutive kz lines (the
+// contiguous axis), so every global access is a run of >= 128 bytes; lines
+// sharing a warp get distinct shared-memory banks through the FFT salt.
+// "pruned" (dealiased state): only kept (ky, kz) lines / kept modes are
+// touched; otherwise every mode is processed with identical results.
+#include "skg_internal.h"
+
+namespace skg {
+
+namespace {
+
+__device__ __forceinline__ bool finite2(cd v) { return isfinite(v.x) && isfinite(v.y); }
+
+// ky of the kyi-th processed line of the x passes.
+__device__ __forceinline__ int ky_of(const Ns3dArgs& a, int kyi) {
+    if (!a.pruned) return kyi;
+    return kyi <= a.kcy ? kyi : a.ny - (2 * a.kcy + 1) + kyi;
+}
+
+__device__ __forceinline__ size_t sidx(const Ns3dArgs& a, int kx, int ky, int kz) {
+    return ((size_t)kx * a.ny + ky) * a.nh + kz;
+}
+
+// RK stage state of variable c at mode (i, ky, kz)  (time_stepping.cpp:128-170)
+__device__ __forceinline__ cd stage_input3(const Ns3dArgs& a, int stage, int c, int i, int ky,
+                                           int kz) {
+    const size_t idx = sidx(a, i, ky, kz) + c * a.vstride;
+    const cd u = a.u[idx];
+    if (stage <= 1) return u;
+    if (a.has_sigma) {
+        const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
+        if (stage == 2) return scale(add(u, scale(a.k1[idx], a.hdt)), e1);
+        if (stage == 3) return add(scale(u, e1), scale(a.k2[idx], a.hdt));
+        const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
+        return add(scale(u, e2), scale(a.k3[idx], a.dt * e1));
+    }
+    if (stage == 2) return add(u, scale(a.k1[idx], a.hdt));
+    if (stage == 3) return add(u, scale(a.k2[idx], a.hdt));
+    return add(u, scale(a.k3[idx], a.dt));
+}
+
+// Lines per CTA for the strided passes: lanes walk the contiguous kz axis.
+template <int N>
+struct Strided {
+    using F = BFFT<N>;
+    static constexpr int T = F::T;
+    static constexpr int C = T >= 256 ? 1 : 256 / T;
+};
+
+// ------------------------------------------------------------------ x-inverse
+template <int NX>
+__global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T, E = F::E, C = Strided<NX>::C;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x % C, t = threadIdx.x / C;
+    const int nkzb = (a.kz_in + C - 1) / C;
+    const int kyi = blockIdx.x / nkzb;
+    const int kz = (blockIdx.x % nkzb) * C + l;
+    const bool active = kz < a.kz_in;
+    if (a.flags->diverged) return;
+    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.flags->steps, 1);
+    const int ky = ky_of(a, kyi);
+    cd* sm = smem + l * F::SMEM;
+    const int salt = l & 7;
+    const typename F::Bases wb = F::bases(t, a.twx);
+#pragma unroll 1
+    for (int m = 0; m < 5; ++m) {
+        const int c = m < 3 ? m : m - 2;  // X[vx] X[vy] X[vz] X[kx vy] X[kx vz]
+        const bool kxm = m >= 3;
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = t + T * e;
+            const int si = signed_index(i, NX);
+            const bool keep = active && (!a.pruned || abs(si) <= a.kcx);
+            cd s = zero();
+            if (keep) {
+                s = stage_input3(a, stage, c, i, ky, kz);
+                if (kxm) s = scale(s, a.kx_scale * (double)si);
+            }
+            v[e] = s;
+        }
+        F::template run<+1>(v, sm, t, wb, salt);
+        if (active) {
+            cd* out = a.A + m * a.fstride;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                out[((size_t)(t + T * e) * a.ny + ky) * a.kz_in + kz] = v[e];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ y-inverse
+template <int NY>
+__global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T, E = F::E, C = Strided<NY>::C;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x % C, t = threadIdx.x / C;
+    const int nkzb = (a.kz_in + C - 1) / C;
+    const int x = blockIdx.x / nkzb;
+    const int kz = (blockIdx.x % nkzb) * C + l;
+    const bool active = kz < a.kz_in;
+    if (a.flags->diverged) return;
+    cd* sm = smem + l * F::SMEM;
+    const int salt = l & 7;
+    const typename F::Bases wb = F::bases(t, a.twy);
+    const double kzv = a.kz_scale * (double)kz;
+    const cd* A0 = a.A;
+    const cd* A1 = a.A + a.fstride;
+    const cd* A2 = a.A + 2 * a.fstride;
+    const cd* A3 = a.A + 3 * a.fstride;
+    const cd* A4 = a.A + 4 * a.fstride;
+#pragma unroll 1
+    for (int m = 0; m < 6; ++m) {
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = t + T * e;
+            const int sj = signed_index(j, NY);
+            const bool keep = active && (!a.pruned || abs(sj) <= a.kcy);
+            cd r = zero();
+            if (keep) {
+                const size_t q = ((size_t)x * a.ny + j) * a.kz_in + kz;
+                const double kyv = a.ky_scale * (double)sj;
+                switch (m) {
+                    case 0: r = A0[q]; break;  // vx
+                    case 1: r = A1[q]; break;  // vy
+                    case 2: r = A2[q]; break;  // vz
+                    case 3: {                  // wx = i (ky vz - kz vy)
+                        const cd p2 = A2[q], p1 = A1[q];
+                        r = muli(sub(scale(p2, kyv), scale(p1, kzv)));
+                    } break;
+                    case 4: {                  // wy = i (kz vx - kx vz)
+                        const cd p0 = A0[q], p4 = A4[q];
+                        r = muli(sub(scale(p0, kzv), p4));
+                    } break;
+                    default: {                 // wz = i (kx vy - ky vx)
+                        const cd p3 = A3[q], p0 = A0[q];
+                        r = muli(sub(p3, scale(p0, kyv)));
+                    } break;
+                }
+            }
+            v[e] = r;
+        }
+        F::template run<+1>(v, sm, t, wb, salt);
+        if (active) {
+            cd* out = a.B + m * a.fstride;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                out[((size_t)x * a.ny + (t + T * e)) * a.kz_in + kz] = v[e];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ z pass
+// Per group: one row pair (r, r+1) of (x, y) rows along z.
+template <int NZ>
+struct Z3 {
+    using F = BFFT<NZ>;
+    static constexpr int T = F::T;
+    static constexpr int G = T >= 128 ? 1 : 128 / T;
+    static constexpr int SLOT = F::SMEM + 5 * NZ / 2;  // exchange + 5 rows of doubles (cd units)
+};
+
+template <int NZ>
+__device__ __forceinline__ void load_packed(const Ns3dArgs& a, const cd* P, const cd* Q, size_t row,
+                                            bool active, int t, cd* v) {
+    using F = BFFT<NZ>;
+    constexpr int T = F::T, E = F::E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int idx = t + T * e;
+        const bool mirror = idx > NZ / 2;
+        const int ki = mirror ? NZ - idx : idx;
+        cd p = zero(), q = zero();
+        if (active && ki < a.kz_in) {
+            p = P[row + ki];
+            q = Q[row + ki];
+            if (ki == 0 || 2 * ki == NZ) {  // c2r ignores these imaginary parts
+                p.y = 0.0;
+                q.y = 0.0;
+            }
+        }
+        v[e] = mirror ? mk(p.x + q.y, q.x - p.y) : mk(p.x - q.y, p.y + q.x);
+    }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G) k3_3d(Ns3dArgs a) {
+    using F = BFFT<NZ>;
+    constexpr int T = F::T, E = F::E, G = Z3<NZ>::G;
+    extern __shared__ cd smem[];
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const long long r0 = 2ll * ((long long)blockIdx.x * G + g);
+    const bool active = r0 < (long long)a.nx * a.ny;
+    if (a.flags->diverged) return;
+    cd* sm = smem + g * Z3<NZ>::SLOT;
+    double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
+    const typename F::Bases wb = F::bases(t, a.twz);
+    const cd* B = a.B;
+    const size_t fs = a.fstride;
+    const double h = 0.5 * a.inv_n;
+#pragma unroll 1
+    for (int rr = 0; rr < 2; ++rr) {
+        const size_t row = (size_t)(r0 + rr) * a.kz_in;
+        cd v[E];
+        // w + i wx
+        load_packed<NZ>(a, B + 2 * fs, B + 3 * fs, row, active, t, v);
+        F::template run<+1>(v, sm, t, wb);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            st[0 * NZ + t + T * e] = v[e].x;
+            st[1 * NZ + t + T * e] = v[e].y;
+        }
+        // wy + i wz
+        load_packed<NZ>(a, B + 4 * fs, B + 5 * fs, row, active, t, v);
+        F::template run<+1>(v, sm, t, wb);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            st[2 * NZ + t + T * e] = v[e].x;
+            st[3 * NZ + t + T * e] = v[e].y;
+        }
+        // u + i v, then the cross product (solvers.cpp:321-325)
+        load_packed<NZ>(a, B + 0 * fs, B + 1 * fs, row, active, t, v);
+        F::template run<+1>(v, sm, t, wb);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int y = t + T * e;
+            const double ux = v[e].x, uy = v[e].y;
+            const double uz = st[0 * NZ + y], ox = st[1 * NZ + y];
+            const double oy = st[2 * NZ + y], oz = st[3 * NZ + y];
+            const double cx = uy * oz - uz * oy;
+            const double cy = uz * ox - ux * oz;
+            const double cz = ux * oy - uy * ox;
+            v[e] = mk(cx, cy);
+            st[(rr == 0 ? 4 : 0) * NZ + y] = cz;  // row b reuses the dead w row
+        }
+        F::template run<-1>(v, sm, t, wb);
+#pragma unroll
+        for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+        __syncthreads();
+        if (active) {
+            cd* o0 = a.A + (size_t)(r0 + rr) * a.kz_o;
+            cd* o1 = o0 + fs;
+            for (int k = t; k < a.kz_o; k += T) {
+                const cd zk = sm[F::pad(k)];
+                const cd zm = sm[F::pad((NZ - k) & (NZ - 1))];
+                o0[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+            }
+        }
+        __syncthreads();
+    }
+    cd v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = mk(st[4 * NZ + t + T * e], st[0 * NZ + t + T * e]);
+    F::template run<-1>(v, sm, t, wb);
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+    __syncthreads();
+    if (active) {
+        cd* oa = a.A + 2 * fs + (size_t)r0 * a.kz_o;
+        cd* ob = oa + a.kz_o;
+        for (int k = t; k < a.kz_o; k += T) {
+            const cd zk = sm[F::pad(k)];
+            const cd zm = sm[F::pad((NZ - k) & (NZ - 1))];
+            oa[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+            ob[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ y-forward
+template <int NY>
+__global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T, E = F::E, C = Strided<NY>::C;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x % C, t = threadIdx.x / C;
+    const int nkzb = (a.kz_o + C - 1) / C;
+    const int x = blockIdx.x / nkzb;
+    const int kz = (blockIdx.x % nkzb) * C + l;
+    const bool active = kz < a.kz_o;
+    if (a.flags->diverged) return;
+    cd* sm = smem + l * F::SMEM;
+    const int salt = l & 7;
+    const typename F::Bases wb = F::bases(t, a.twy);
+#pragma unroll 1
+    for (int m = 0; m < 3; ++m) {
+        const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            v[e] = active ? in[((size_t)x * a.ny + (t + T * e)) * a.kz_o + kz] : zero();
+        F::template run<-1>(v, sm, t, wb, salt);
+        if (active) {
+            cd* out = a.B + m * a.fstride;   // D fields live in B's memory
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int j = t + T * e;
+                if (abs(signed_index(j, NY)) > a.kcy) continue;  // masked: never read
+                out[((size_t)x * a.ny + j) * a.kz_o + kz] = v[e];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ x-forward + RK
+template <int NX>
+__global__ void __launch_bounds__(256, 1) k4_3d(Ns3dArgs a, int stage) {
+    using F = BFFT<NX>;
+    constexpr int T = F::T, E = F::E, C = Strided<NX>::C;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x % C, t = threadIdx.x / C;
+    const int nkzb = (a.kz_o + C - 1) / C;
+    const int kyi = blockIdx.x / nkzb;
+    const int kz = (blockIdx.x % nkzb) * C + l;
+    const bool active = kz < a.kz_o;
+    if (a.flags->diverged) return;
+    const int ky = ky_of(a, kyi);
+    const int sky = signed_index(ky, a.ny);
+    const bool keep_y = abs(sky) <= a.kcy;
+    cd* sm = smem + l * F::SMEM;
+    cd* slots = smem + C * F::SMEM;  // comps 0,1: slots[(c * E + e) * 256 + tid]
+    const int salt = l & 7;
+    const typename F::Bases wb = F::bases(t, a.twx);
+#pragma unroll 1
+    for (int m = 0; m < 3; ++m) {
+        const cd* in = a.B + m * a.fstride;
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            v[e] = (active && keep_y) ? in[((size_t)(t + T * e) * a.ny + ky) * a.kz_o + kz] : zero();
+        F::template run<-1>(v, sm, t, wb, salt);
+        if (m < 2) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) slots[(m * E + e) * 256 + threadIdx.x] = v[e];
+            continue;
+        }
+        if (!active) return;
+        const bool final = a.rk2 ? stage == 2 : stage == 4;
+        cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
+        const double kyv = a.ky_scale * (double)sky;
+        const double kzv = a.kz_scale * (double)kz;
+        int bad = 3;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = t + T * e;
+            const int si = signed_index(i, NX);
+            bool keep = keep_y && abs(si) <= a.kcx;
+            if (i == 0 && ky == 0 && kz == 0) keep = false;  // mean mode of the tendency is 0
+            if (!keep && a.pruned) continue;
+            cd c0 = zero(), c1 = zero(), c2 = zero();
+            if (keep) {
+                c0 = slots[(0 * E + e) * 256 + threadIdx.x];
+                c1 = slots[(1 * E + e) * 256 + threadIdx.x];
+                c2 = v[e];
+                // Leray projection (grid.cpp:227-249)
+                const double kxv = a.kx_scale * (double)si;
+                const double ksq = kxv * kxv + kyv * kyv + kzv * kzv;
+                if (ksq != 0.0) {
+                    const cd dot = add(add(scale(c0, kxv), scale(c1, kyv)), scale(c2, kzv));
+                    const cd s = mk(dot.x / ksq, dot.y / ksq);
+                    c0 = sub(c0, scale(s, kxv));
+                    c1 = sub(c1, scale(s, kyv));
+                    c2 = sub(c2, scale(s, kzv));
+                }
+            }
+            const cd kc[3] = {c0, c1, c2};
+            const size_t base = sidx(a, i, ky, kz);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const size_t idx = base + c * a.vstride;
+                const cd kv = kc[c];
+                if (!final) {
+                    kout[idx] = kv;
+                    continue;
+                }
+                const cd u = a.u[idx];
+                cd un;
+                if (a.has_sigma) {
+                    const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
+                    const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
+                    if (a.rk2) {
+                        un = add(scale(u, e2), scale(kv, a.dt * e1));
+                    } else {
+                        const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                        const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
+                        un = add(scale(u, e2), scale(sum, a.sdt));
+                    }
+                } else {
+                    cd delta;
+                    if (a.rk2) {
+                        delta = scale(kv, a.dt);
+                    } else {
+                        const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                        delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                    }
+                    un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
+                }
+                a.u[idx] = un;
+                if (!finite2(un) && c < bad) bad = c;
+            }
+        }
+        if (bad < 3) {
+            atomicMin(&a.flags->div_var, bad);
+            atomicExch(&a.flags->div_step, a.flags->steps);
+            atomicExch(&a.flags->diverged, 1);
+        }
+    }
+}
+
+// Unpruned final update of the kz planes above the cut (tendency zero there).
+__global__ void k4_3d_decay(Ns3dArgs a) {
+    if (a.flags->diverged) return;
+    const int nk = a.nh - a.kz_o;
+    const size_t total = (size_t)a.nx * a.ny * nk;
+    int bad = 3;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int kz = a.kz_o + (int)(q % nk);
+        const size_t r = q / nk;
+        const int ky = (int)(r % a.ny);
+        const int i = (int)(r / a.ny);
+        const size_t base = sidx(a, i, ky, kz);
+        for (int c = 0; c < 3; ++c) {
+            const size_t idx = base + c * a.vstride;
+            cd u = a.u[idx];
+            if (a.has_sigma) {
+                u = scale(u, a.e2x[i] * a.e2y[ky] * a.e2z[kz]);
+                a.u[idx] = u;
+            }
+            if (!finite2(u) && c < bad) bad = c;
+        }
+    }
+    if (bad < 3) {
+        atomicMin(&a.flags->div_var, bad);
+        atomicExch(&a.flags->div_step, a.flags->steps);
+        atomicExch(&a.flags->diverged, 1);
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+template <typename K>
+void set_smem(K kernel, size_t bytes, size_t& done) {
+    if (done < bytes) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        done = bytes;
+    }
+}
+
+template <int NX>
+cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    constexpr int C = Strided<NX>::C;
+    using F = BFFT<NX>;
+    if (inverse) {
+        const size_t smem = sizeof(cd) * F::SMEM * C;
+        static size_t done = 0;
+        set_smem(k1_3d<NX>, smem, done);
+        const int grid = a.ky_lines * ((a.kz_in + C - 1) / C);
+        k1_3d<NX><<<grid, F::T * C, smem, s>>>(a, stage);
+    } else {
+        const size_t smem = sizeof(cd) * (F::SMEM * C + 2 * F::E * 256);
+        static size_t done = 0;
+        set_smem(k4_3d<NX>, smem, done);
+        const int grid = a.ky_lines * ((a.kz_o + C - 1) / C);
+        k4_3d<NX><<<grid, F::T * C, smem, s>>>(a, stage);
+    }
+    return cudaGetLastError();
+}
+
+template <int NY>
+cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
+    constexpr int C = Strided<NY>::C;
+    using F = BFFT<NY>;
+    const size_t smem = sizeof(cd) * F::SMEM * C;
+    if (inverse) {
+        static size_t done = 0;
+        set_smem(k2_3d<NY>, smem, done);
+        const int grid = a.nx * ((a.kz_in + C - 1) / C);
+        k2_3d<NY><<<grid, F::T * C, smem, s>>>(a);
+    } else {
+        static size_t done = 0;
+        set_smem(k2f_3d<NY>, smem, done);
+        const int grid = a.nx * ((a.kz_o + C - 1) / C);
+        k2f_3d<NY><<<grid, F::T * C, smem, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+template <int NZ>
+cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
+    using Z = Z3<NZ>;
+    const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
+    static size_t done = 0;
+    set_smem(k3_3d<NZ>, smem, done);
+    const long long pairs = (long long)a.nx * a.ny / 2;
+    const int grid = (int)((pairs + Z::G - 1) / Z::G);
+    k3_3d<NZ><<<grid, Z::T * Z::G, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define SKG3_CASES(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
+
+cudaError_t dispatch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    switch (a.nx) {
+#define CASE(N) \
+    case N: return launch_x3<N>(a, stage, inverse, s);
+        SKG3_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t dispatch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
+    switch (a.ny) {
+#define CASE(N) \
+    case N: return launch_y3<N>(a, inverse, s);
+        SKG3_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t dispatch_z3(const Ns3dArgs& a, cudaStream_t s) {
+    switch (a.nz) {
+#define CASE(N) \
+    case N: return launch_z3<N>(a, s);
+        SKG3_CASES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+bool ns3d_supported(int nx, int ny, int nz) {
+    auto ok = [](int n) { return n >= 8 && n <= 1024 && (n & (n - 1)) == 0; };
+    return ok(nx) && ok(ny) && ok(nz);
+}
+
+cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
+                              const LaunchHook& hook) {
+    cudaError_t err;
+    const double B = sizeof(cd);
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    const double kyk = a.pruned ? 2.0 * a.kcy + 1 : (double)a.ny;  // ky read by k2
+    const double kxk = a.pruned ? 2.0 * a.kcx + 1 : (double)a.nx;
+    const double lines_in = (double)a.ky_lines * a.kz_in;
+    const double lines_o = (double)a.ky_lines * a.kz_o;
+    const double plane_in = (double)a.nx * a.ny * a.kz_in;
+    const double plane_o = (double)a.nx * a.ny * a.kz_o;
+    hook.begin(0);
+    if ((err = dispatch_x3(a, stage, true, s)) != cudaSuccess) return err;
+    hook.end(0, B * (3.0 * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + 5.0 * a.nx * lines_in));
+    hook.begin(3);
+    if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
+    hook.end(3, B * (5.0 * a.nx * kyk * a.kz_in + 6.0 * plane_in));
+    hook.begin(1);
+    if ((err = dispatch_z3(a, s)) != cudaSuccess) return err;
+    hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
+    hook.begin(3);
+    if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;
+    hook.end(3, B * (3.0 * plane_o + 3.0 * a.nx * kyk * a.kz_o));
+    hook.begin(2);
+    if ((err = dispatch_x3(a, stage, false, s)) != cudaSuccess) return err;
+    hook.end(2, B * (3.0 * a.nx * lines_o +
+                     3.0 * kxk * lines_o * (final ? (a.rk2 ? 3.0 : 5.0) : 1.0)));
+    *launches += 5;
+    if (final && !a.pruned && a.nh > a.kz_o) {
+        hook.begin(3);
+        k4_3d_decay<<<592, 256, 0, s>>>(a);
+        hook.end(3, B * 6.0 * a.nx * a.ny * (a.nh - a.kz_o));
+        *launches += 1;
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace skg

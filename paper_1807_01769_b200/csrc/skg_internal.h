@@ -81,28 +81,37 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
 bool ns2d_supported(int nx, int ny);
 
 // ---------------------------------------------------------------- ns3d
+// State and RK buffers keep the reference layout [kx][ky][kz] (kz the
+// half axis, nh = nz/2 + 1).  Intermediates (all row-major, kz fastest):
+//   A[5] after the x-inverse pass  (x, ky, kz)  kz < kz_in   X[vx] X[vy] X[vz] X[kx vy] X[kx vz]
+//   B[6] after the y-inverse pass  (x, y, kz)   kz < kz_in   u v w wx wy wz (still kz-spectral)
+//   C[3] after the z pass          (x, y, kz)   kz <= kcz    (u x w)^ in kz
+//   D[3] after the y-forward pass  (x, ky, kz)  kz <= kcz
+// C aliases A and D aliases B (each is dead when the other is produced).
 struct Ns3dArgs {
-    int nx, ny, nz, nh;     // nh = nz/2+1
+    int nx, ny, nz, nh;
     int kcx, kcy, kcz;
     int pruned, has_sigma, rk2;
-    // extents of the stored/processed index ranges
-    int ky_in, kz_in;       // (ky, kz) lines processed by the x-inverse pass
+    int kz_in;           // kz extent of A/B (kcz+1 pruned, nh full)
+    int kz_o;            // kz extent of C/D (= kcz+1)
+    int ky_lines;        // ky lines of the x passes (2kcy+1 pruned, ny full)
     double kx_scale, ky_scale, kz_scale;
     double inv_n;
     double dt, hdt, sdt;
     const double *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
-    cd* u[3];               // state, reference layout [kx][ky][kz]
-    cd* k1[3];
-    cd* k2[3];
-    cd* k3[3];
-    cd* A[5];               // x-pass outputs  [x][ky][kz]   (kz < kz_in)
-    cd* B[6];               // y-pass outputs  [x][y][kz]
-    cd* C[3];               // z-pass outputs  [x][y][kz]   (kz <= kcz)
-    cd* D[3];               // y-forward outputs [x][ky][kz]
+    cd* u;               // 3 variables, each nx*ny*nh (reference layout)
+    cd* k1;
+    cd* k2;
+    cd* k3;
+    size_t vstride;      // elements between variables of u/k1/k2/k3
+    cd* A;               // 5 fields, stride fstride
+    cd* B;               // 6 fields
+    size_t fstride;      // elements per intermediate field (nx*ny*nh)
     const cd *twx, *twy, *twz;
     DevFlags* flags;
 };
-cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches);
+cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
+                              const LaunchHook& hook);
 bool ns3d_supported(int nx, int ny, int nz);
 
 // ---------------------------------------------------------------- utilities (util.cu)

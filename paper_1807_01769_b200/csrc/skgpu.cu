@@ -242,6 +242,49 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     return a;
 }
 
+skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
+    skg::Ns3dArgs a{};
+    a.nx = c->n[0];
+    a.ny = c->n[1];
+    a.nz = c->n[2];
+    a.nh = c->nh;
+    a.kcx = c->kc[0];
+    a.kcy = c->kc[1];
+    a.kcz = c->kc[2];
+    a.pruned = c->pruned ? 1 : 0;
+    a.has_sigma = c->nu != 0.0;
+    a.rk2 = c->scheme == SKG_RK2;
+    a.kz_in = c->pruned ? c->kc[2] + 1 : c->nh;
+    a.kz_o = c->kc[2] + 1;
+    a.ky_lines = c->pruned ? 2 * c->kc[1] + 1 : c->n[1];
+    a.kx_scale = c->kscale[0];
+    a.ky_scale = c->kscale[1];
+    a.kz_scale = c->kscale[2];
+    a.inv_n = 1.0 / (double)c->P;
+    a.dt = dt;
+    a.hdt = 0.5 * dt;
+    a.sdt = dt / 6.0;
+    a.e1x = etab_ptr(c, 0, 0);
+    a.e1y = etab_ptr(c, 0, 1);
+    a.e1z = etab_ptr(c, 0, 2);
+    a.e2x = etab_ptr(c, 1, 0);
+    a.e2y = etab_ptr(c, 1, 1);
+    a.e2z = etab_ptr(c, 1, 2);
+    a.u = c->u;
+    a.k1 = c->k[0];
+    a.k2 = c->k[1];
+    a.k3 = c->k[2];
+    a.vstride = (size_t)c->S;
+    a.fstride = (size_t)c->n[0] * c->n[1] * c->nh;
+    a.A = c->inter;
+    a.B = c->inter + 5 * a.fstride;
+    a.twx = c->tw[0];
+    a.twy = c->tw[1];
+    a.twz = c->tw[2];
+    a.flags = c->flags;
+    return a;
+}
+
 int sync_and_check(skg_ctx* c, long nsteps, double dt) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     harvest(c);
@@ -280,7 +323,11 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             for (int st = 1; st <= nst; ++st)
                 CUDA_TRY(skg::ns2d_launch_stage(a, st, c->stream, &c->launches, hook));
     } else {
-        return fail(SKG_EUNSUPPORTED, "ns3d step not built");
+        skg::Ns3dArgs a = args3d(c, dt);
+        const skg::LaunchHook hook = hook_of(c);
+        for (long s = 0; s < nsteps; ++s)
+            for (int st = 1; st <= nst; ++st)
+                CUDA_TRY(skg::ns3d_launch_stage(a, st, c->stream, &c->launches, hook));
     }
     return SKG_OK;
 }
@@ -364,7 +411,8 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
     if (scheme != SKG_RK4 && scheme != SKG_RK2) return fail(SKG_ECONFIG, "unknown time scheme");
     if (sid == 2 && !skg::ns2d_supported(n[0], n[1]))
         return fail(SKG_EUNSUPPORTED, "ns2d kernels need power-of-two extents in [4, 8192]");
-    if (sid == 3) return fail(SKG_EUNSUPPORTED, "ns3d kernels not built yet");
+    if (sid == 3 && !skg::ns3d_supported(n[0], n[1], n[2]))
+        return fail(SKG_EUNSUPPORTED, "ns3d kernels need power-of-two extents in [8, 1024]");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -407,6 +455,7 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
     bool ok = alloc((void**)&c->u, sizeof(cd) * S * c->nvars);
     for (int i = 0; i < 3 && ok; ++i) ok = alloc((void**)&c->k[i], sizeof(cd) * S * c->nvars);
     if (sid == 2) c->inter_elems = 5 * S;  // 4 intermediates + tendency rows
+    else c->inter_elems = 11 * (size_t)n[0] * n[1] * c->nh;  // A[5] (C aliases) + B[6] (D aliases)
     ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
     ok = ok && alloc((void**)&c->io, sizeof(cd) * S * c->nvars);
     ok = ok && alloc((void**)&c->phys, sizeof(double) * (size_t)c->P);
@@ -546,7 +595,17 @@ int skg_tendency(skg_ctx* c, const double* in, double* out) {
         rc = store_state_to_io(c, c->k[0]);
         if (rc) return rc;
     } else {
-        return fail(SKG_EUNSUPPORTED, "ns3d tendency not built");
+        CUDA_TRY(cudaMemcpyAsync(c->k[2], c->io, sizeof(cd) * c->S * c->nvars,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        rc = refresh_exp(c, c->cached_dt > 0 ? c->cached_dt : 1.0);
+        if (rc) return rc;
+        skg::Ns3dArgs a = args3d(c, c->cached_dt);
+        a.u = c->k[2];
+        skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(skg::ns3d_launch_stage(a, 1, c->stream, &c->launches, hook_of(c)));
+        rc = store_state_to_io(c, c->k[0]);
+        if (rc) return rc;
     }
     CUDA_TRY(cudaMemcpyAsync(out, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToHost,
                              c->stream));
