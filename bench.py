@@ -210,7 +210,10 @@ def run_our_arm(args):
     P = int(np.prod(n))
     S = u0.size  # complex modes over all variables
     sim = api.Simulation(solver, n, nu, dt, device=local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library launches on it and the
+    # CUDA events below are recorded on the same stream
+    stream = torch.cuda.Stream(device=local)
+    assert stream.cuda_stream != 0
     sim.set_stream(stream.cuda_stream)
     sim.set_state(u0)
     pruned = sim.pruned
