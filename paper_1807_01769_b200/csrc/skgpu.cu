@@ -471,6 +471,9 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
         c->tw[d] = twiddle_table(device, n[d]);
         if (!c->tw[d]) return cleanup(SKG_ECUDA, "twiddle table allocation failed");
     }
+    // cudaMemset above runs on the legacy default stream, which does not order
+    // against the context's non-blocking stream: finish it before any kernel.
+    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(SKG_ECUDA, "device synchronize failed");
     c->pruned = true;  // zero state is dealiased
     *out = c;
     return SKG_OK;
