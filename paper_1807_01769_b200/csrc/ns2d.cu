@@ -36,8 +36,25 @@ __device__ __forceinline__ size_t pidx(int x, int ky, int ld) {
     return ((size_t)(x >> 1) * ld + ky) * 2 + (x & 1);
 }
 
+// Column-pair interleaved layout of the fast path's product spectra A, B:
+// element (x, ky) at ((ky/2) nx + x) 2 + (ky mod 2).  The y pass writes it
+// (strided stores, merged in L2), the x-forward pass reads each ky column
+// as one contiguous stream (strided loads would defeat DRAM row locality).
+__device__ __forceinline__ size_t cpidx(int x, int ky, int nx) {
+    return ((size_t)(ky >> 1) * nx + x) * 2 + (ky & 1);
+}
+
 __device__ __forceinline__ cd* pick(const Ns2dArgs& a, int m) {
     return m == 0 ? a.I[0] : m == 1 ? a.I[1] : m == 2 ? a.I[2] : a.I[3];
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 __device__ __forceinline__ bool finite2(cd v) { return isfinite(v.x) && isfinite(v.y); }
@@ -69,6 +86,19 @@ __device__ __forceinline__ cd stage_input(const Ns2dArgs& a, int stage, int ky, 
     }
 }
 
+// RK stage state from already-loaded u and previous k (time_stepping.cpp:128-170).
+__device__ __forceinline__ cd stage_combine(const Ns2dArgs& a, int stage, int ky, int i, cd u, cd k) {
+    if (stage <= 1) return u;
+    if (a.has_sigma) {
+        const double e1 = a.e1x[i] * a.e1y[ky];
+        if (stage == 2) return scale(add(u, scale(k, a.hdt)), e1);
+        if (stage == 3) return add(scale(u, e1), scale(k, a.hdt));
+        const double e2 = a.e2x[i] * a.e2y[ky];
+        return add(scale(u, e2), scale(k, a.dt * e1));
+    }
+    return add(u, scale(k, stage == 4 ? a.dt : a.hdt));
+}
+
 // PZ: the state is dealiased and the kept |kx| <= kcx < 6T, so the elements
 // e in [6, 10) of every thread (kx in [6T, 10T)) are exactly zero: they are
 // neither loaded nor stored, and the stage-state slots shrink from 16 to 12.
@@ -94,6 +124,25 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
     // psi, kx psi, kx |k|^2 psi, |k|^2 psi -- no division inside the loop.
     // (|k|^2 psi differs from w in the last bit and is 0 at k = 0, where w
     // only feeds columns multiplied by kx = 0 or ky = 0.)
+    // u and k_{j-1} of the column stream into shared memory with cp.async
+    // (u into the thread's slots, k into the still idle exchange buffer,
+    // same thread-private layout), so all loads are in flight at once.
+    const cd* kprev = stage == 2 ? a.k1 : stage == 3 ? a.k2 : a.k3;
+    cd* kv = sm;  // exchange buffer as k staging: kv[slot * T + t]
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= ZLO && e < ZHI) continue;
+        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+        const int i = t + T * e;
+        const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
+        if (keep) {
+            const size_t idx = (size_t)ky * NX + i;
+            cp_async16(&sv[slot * T + t], a.u + idx);
+            if (stage > 1) cp_async16(&kv[slot * T + t], kprev + idx);
+        }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         if (e >= ZLO && e < ZHI) continue;
@@ -103,13 +152,15 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
         const bool keep = active && (!a.pruned || abs(si) <= a.kcx);
         cd psi = zero();
         if (keep) {
-            const cd s = stage_input(a, stage, ky, i, (size_t)ky * NX + i);
+            const cd s = stage_combine(a, stage, ky, i, sv[slot * T + t],
+                                       stage > 1 ? kv[slot * T + t] : zero());
             const double kxv = a.kx_scale * (double)si;
             const double ksq = kxv * kxv + kyv * kyv;
             if (ksq != 0.0) psi = mk(s.x / ksq, s.y / ksq);
         }
         sv[slot * T + t] = psi;
     }
+    __syncthreads();  // k staging lived in the exchange buffer
 #pragma unroll 1
     for (int m = 0; m < NM; ++m) {
         cd v[E];
@@ -133,15 +184,6 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
             for (int e = 0; e < E; ++e) out[pidx(t + T * e, ky, a.ld_i)] = v[e];
         }
     }
-}
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // y pass on a row pair (xa, xa+1).  Four inverse FFTs k = 0..3 over
@@ -430,8 +472,8 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
             for (int k = t; k < a.ld_o; k += T) {
                 const cd zk = sm[F::pad(k)];
                 const cd zm = sm[F::pad((NY - k) & (NY - 1))];
-                outA[pidx(x, k, a.ld_o)] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-                outB[pidx(x, k, a.ld_o)] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+                outA[cpidx(x, k, a.nx)] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                outB[cpidx(x, k, a.nx)] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
             }
         }
     }
@@ -457,7 +499,7 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.I[2][pidx(t + T * e, ky, a.ld_o)] : zero();
+        v[e] = active ? a.I[2][cpidx(t + T * e, ky, NX)] : zero();
     F::template run<-1>(v, sm, t, wb);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -468,7 +510,7 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.I[3][pidx(t + T * e, ky, a.ld_o)] : zero();
+        v[e] = active ? a.I[3][cpidx(t + T * e, ky, NX)] : zero();
     F::template run<-1>(v, sm, t, wb);
     if (!active) return;
     const bool final = a.rk2 ? stage == 2 : stage == 4;
