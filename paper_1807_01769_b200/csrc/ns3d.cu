@@ -27,6 +27,29 @@ namespace {
 
 __device__ __forceinline__ bool finite2(cd v) { return isfinite(v.x) && isfinite(v.y); }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// RK stage state from loaded u and previous k (time_stepping.cpp:128-170).
+__device__ __forceinline__ cd stage_combine3(const Ns3dArgs& a, int stage, int i, int ky, int kz,
+                                             cd u, cd k) {
+    if (stage <= 1) return u;
+    if (a.has_sigma) {
+        const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
+        if (stage == 2) return scale(add(u, scale(k, a.hdt)), e1);
+        if (stage == 3) return add(scale(u, e1), scale(k, a.hdt));
+        const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
+        return add(scale(u, e2), scale(k, a.dt * e1));
+    }
+    return add(u, scale(k, stage == 4 ? a.dt : a.hdt));
+}
+
 // ky of the kyi-th processed line of the x passes.
 __device__ __forceinline__ int ky_of(const Ns3dArgs& a, int kyi) {
     if (!a.pruned) return kyi;
@@ -64,10 +87,16 @@ struct Strided {
 };
 
 // ------------------------------------------------------------------ x-inverse
-template <int NX>
+// Each velocity component's stage state is computed once (u and k_{j-1}
+// streamed into shared memory with cp.async) and kept in thread-private
+// slots for its one or two FFTs.  PZ: dealiased state with kcx < 6T, so the
+// per-thread elements e in [6, 10) are zero and need no slot.
+template <int NX, bool PZ>
 __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E, C = Strided<NX>::C;
+    constexpr int ZLO = PZ ? 6 : E, ZHI = PZ ? 10 : E;
+    constexpr int CT = T * C;  // threads per CTA
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_in + C - 1) / C;
@@ -78,31 +107,61 @@ __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
     if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.flags->steps, 1);
     const int ky = ky_of(a, kyi);
     cd* sm = smem + l * F::SMEM;
+    cd* slots = smem + C * F::SMEM;  // slots[slot * CT + tid]
+    cd* kst = smem;                  // k staging in the idle exchange buffers
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twx);
+    const cd* kprev = stage == 2 ? a.k1 : stage == 3 ? a.k2 : a.k3;
 #pragma unroll 1
-    for (int m = 0; m < 5; ++m) {
-        const int c = m < 3 ? m : m - 2;  // X[vx] X[vy] X[vz] X[kx vy] X[kx vz]
-        const bool kxm = m >= 3;
-        cd v[E];
+    for (int c = 0; c < 3; ++c) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+            if (e >= ZLO && e < ZHI) continue;
+            const int slot = e < ZLO ? e : e - (ZHI - ZLO);
             const int i = t + T * e;
-            const int si = signed_index(i, NX);
-            const bool keep = active && (!a.pruned || abs(si) <= a.kcx);
-            cd s = zero();
+            const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
             if (keep) {
-                s = stage_input3(a, stage, c, i, ky, kz);
-                if (kxm) s = scale(s, a.kx_scale * (double)si);
+                const size_t idx = sidx(a, i, ky, kz) + c * a.vstride;
+                cp_async16(&slots[slot * CT + threadIdx.x], a.u + idx);
+                if (stage > 1) cp_async16(&kst[slot * CT + threadIdx.x], kprev + idx);
             }
-            v[e] = s;
         }
-        F::template run<+1>(v, sm, t, wb, salt);
-        if (active) {
-            cd* out = a.A + m * a.fstride;
+        cp_async_commit();
+        cp_async_wait_all();
 #pragma unroll
-            for (int e = 0; e < E; ++e)
-                out[((size_t)(t + T * e) * a.ny + ky) * a.kz_in + kz] = v[e];
+        for (int e = 0; e < E; ++e) {
+            if (e >= ZLO && e < ZHI) continue;
+            const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+            const int i = t + T * e;
+            const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
+            cd s = zero();
+            if (keep)
+                s = stage_combine3(a, stage, i, ky, kz, slots[slot * CT + threadIdx.x],
+                                   stage > 1 ? kst[slot * CT + threadIdx.x] : zero());
+            slots[slot * CT + threadIdx.x] = s;
+        }
+        __syncthreads();  // k staging lived in the exchange buffers
+#pragma unroll 1
+        for (int q = 0; q < (c == 0 ? 1 : 2); ++q) {
+            const int m = q == 0 ? c : c + 2;  // X[v_c] or X[kx v_c]
+            cd v[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (e >= ZLO && e < ZHI) {
+                    v[e] = zero();
+                    continue;
+                }
+                const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+                const cd sv = slots[slot * CT + threadIdx.x];
+                v[e] = q == 0 ? sv : scale(sv, a.kx_scale * (double)signed_index(t + T * e, NX));
+            }
+            F::template run<+1>(v, sm, t, wb, salt);
+            if (active) {
+                cd* out = a.A + m * a.fstride;
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    out[((size_t)(t + T * e) * a.ny + ky) * a.kz_in + kz] = v[e];
+            }
         }
     }
 }
@@ -172,18 +231,19 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
 
 // ------------------------------------------------------------------ z pass
 // Per group: one row pair (r, r+1) of (x, y) rows along z.
+// 8 elements per thread (twice the warps per byte of shared memory).
 template <int NZ>
 struct Z3 {
-    using F = BFFT<NZ>;
+    using F = BFFT<NZ, false, 8>;
     static constexpr int T = F::T;
-    static constexpr int G = T >= 128 ? 1 : 128 / T;
+    static constexpr int G = T >= 256 ? 1 : 256 / T;
     static constexpr int SLOT = F::SMEM + 5 * NZ / 2;  // exchange + 5 rows of doubles (cd units)
 };
 
 template <int NZ>
 __device__ __forceinline__ void load_packed(const Ns3dArgs& a, const cd* P, const cd* Q, size_t row,
                                             bool active, int t, cd* v) {
-    using F = BFFT<NZ>;
+    using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -204,8 +264,8 @@ __device__ __forceinline__ void load_packed(const Ns3dArgs& a, const cd* P, cons
 }
 
 template <int NZ>
-__global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G) k3_3d(Ns3dArgs a) {
-    using F = BFFT<NZ>;
+__global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
+    using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E, G = Z3<NZ>::G;
     extern __shared__ cd smem[];
     const int g = threadIdx.x / T, t = threadIdx.x % T;
@@ -324,8 +384,11 @@ __global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
 }
 
 // ------------------------------------------------------------------ x-forward + RK
+// Components 0 and 1 are written back raw into their own D lines (in place,
+// L2-resident) and re-read by the same thread for the projection, so no
+// shared-memory slots are needed.
 template <int NX>
-__global__ void __launch_bounds__(256, 1) k4_3d(Ns3dArgs a, int stage) {
+__global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E, C = Strided<NX>::C;
     extern __shared__ cd smem[];
@@ -339,92 +402,94 @@ __global__ void __launch_bounds__(256, 1) k4_3d(Ns3dArgs a, int stage) {
     const int sky = signed_index(ky, a.ny);
     const bool keep_y = abs(sky) <= a.kcy;
     cd* sm = smem + l * F::SMEM;
-    cd* slots = smem + C * F::SMEM;  // comps 0,1: slots[(c * E + e) * 256 + tid]
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twx);
+    const bool io = active && keep_y;
+    const size_t lbase = (size_t)ky * a.kz_o + kz;     // + x * ny * kz_o
+    const size_t xstr = (size_t)a.ny * a.kz_o;
+    cd v[E];
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
-        const cd* in = a.B + m * a.fstride;
-        cd v[E];
+        cd* line = a.B + m * a.fstride + lbase;
 #pragma unroll
-        for (int e = 0; e < E; ++e)
-            v[e] = (active && keep_y) ? in[((size_t)(t + T * e) * a.ny + ky) * a.kz_o + kz] : zero();
+        for (int e = 0; e < E; ++e) v[e] = io ? line[(size_t)(t + T * e) * xstr] : zero();
         F::template run<-1>(v, sm, t, wb, salt);
-        if (m < 2) {
+        if (m < 2 && io) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) slots[(m * E + e) * 256 + threadIdx.x] = v[e];
-            continue;
+            for (int e = 0; e < E; ++e) line[(size_t)(t + T * e) * xstr] = v[e];
         }
-        if (!active) return;
-        const bool final = a.rk2 ? stage == 2 : stage == 4;
-        cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
-        const double kyv = a.ky_scale * (double)sky;
-        const double kzv = a.kz_scale * (double)kz;
-        int bad = 3;
+    }
+    if (!active) return;
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
+    const double kyv = a.ky_scale * (double)sky;
+    const double kzv = a.kz_scale * (double)kz;
+    const cd* l0 = a.B + lbase;
+    const cd* l1 = a.B + a.fstride + lbase;
+    int bad = 3;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int i = t + T * e;
-            const int si = signed_index(i, NX);
-            bool keep = keep_y && abs(si) <= a.kcx;
-            if (i == 0 && ky == 0 && kz == 0) keep = false;  // mean mode of the tendency is 0
-            if (!keep && a.pruned) continue;
-            cd c0 = zero(), c1 = zero(), c2 = zero();
-            if (keep) {
-                c0 = slots[(0 * E + e) * 256 + threadIdx.x];
-                c1 = slots[(1 * E + e) * 256 + threadIdx.x];
-                c2 = v[e];
-                // Leray projection (grid.cpp:227-249)
-                const double kxv = a.kx_scale * (double)si;
-                const double ksq = kxv * kxv + kyv * kyv + kzv * kzv;
-                if (ksq != 0.0) {
-                    const cd dot = add(add(scale(c0, kxv), scale(c1, kyv)), scale(c2, kzv));
-                    const cd s = mk(dot.x / ksq, dot.y / ksq);
-                    c0 = sub(c0, scale(s, kxv));
-                    c1 = sub(c1, scale(s, kyv));
-                    c2 = sub(c2, scale(s, kzv));
-                }
+    for (int e = 0; e < E; ++e) {
+        const int i = t + T * e;
+        const int si = signed_index(i, NX);
+        bool keep = keep_y && abs(si) <= a.kcx;
+        if (i == 0 && ky == 0 && kz == 0) keep = false;  // mean mode of the tendency is 0
+        if (!keep && a.pruned) continue;
+        cd c0 = zero(), c1 = zero(), c2 = zero();
+        if (keep) {
+            c0 = l0[(size_t)i * xstr];
+            c1 = l1[(size_t)i * xstr];
+            c2 = v[e];
+            // Leray projection (grid.cpp:227-249)
+            const double kxv = a.kx_scale * (double)si;
+            const double ksq = kxv * kxv + kyv * kyv + kzv * kzv;
+            if (ksq != 0.0) {
+                const cd dot = add(add(scale(c0, kxv), scale(c1, kyv)), scale(c2, kzv));
+                const cd sp = mk(dot.x / ksq, dot.y / ksq);
+                c0 = sub(c0, scale(sp, kxv));
+                c1 = sub(c1, scale(sp, kyv));
+                c2 = sub(c2, scale(sp, kzv));
             }
-            const cd kc[3] = {c0, c1, c2};
-            const size_t base = sidx(a, i, ky, kz);
+        }
+        const cd kc[3] = {c0, c1, c2};
+        const size_t base = sidx(a, i, ky, kz);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const size_t idx = base + c * a.vstride;
-                const cd kv = kc[c];
-                if (!final) {
-                    kout[idx] = kv;
-                    continue;
-                }
-                const cd u = a.u[idx];
-                cd un;
-                if (a.has_sigma) {
-                    const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
-                    const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
-                    if (a.rk2) {
-                        un = add(scale(u, e2), scale(kv, a.dt * e1));
-                    } else {
-                        const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                        const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
-                        un = add(scale(u, e2), scale(sum, a.sdt));
-                    }
+        for (int c = 0; c < 3; ++c) {
+            const size_t idx = base + c * a.vstride;
+            const cd kv = kc[c];
+            if (!final) {
+                kout[idx] = kv;
+                continue;
+            }
+            const cd u = a.u[idx];
+            cd un;
+            if (a.has_sigma) {
+                const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
+                const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
+                if (a.rk2) {
+                    un = add(scale(u, e2), scale(kv, a.dt * e1));
                 } else {
-                    cd delta;
-                    if (a.rk2) {
-                        delta = scale(kv, a.dt);
-                    } else {
-                        const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                        delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
-                    }
-                    un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
+                    const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                    const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
+                    un = add(scale(u, e2), scale(sum, a.sdt));
                 }
-                a.u[idx] = un;
-                if (!finite2(un) && c < bad) bad = c;
+            } else {
+                cd delta;
+                if (a.rk2) {
+                    delta = scale(kv, a.dt);
+                } else {
+                    const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                }
+                un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
             }
+            a.u[idx] = un;
+            if (!finite2(un) && c < bad) bad = c;
         }
-        if (bad < 3) {
-            atomicMin(&a.flags->div_var, bad);
-            atomicExch(&a.flags->div_step, a.flags->steps);
-            atomicExch(&a.flags->diverged, 1);
-        }
+    }
+    if (bad < 3) {
+        atomicMin(&a.flags->div_var, bad);
+        atomicExch(&a.flags->div_step, a.flags->steps);
+        atomicExch(&a.flags->diverged, 1);
     }
 }
 
@@ -472,13 +537,23 @@ cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s
     constexpr int C = Strided<NX>::C;
     using F = BFFT<NX>;
     if (inverse) {
-        const size_t smem = sizeof(cd) * F::SMEM * C;
-        static size_t done = 0;
-        set_smem(k1_3d<NX>, smem, done);
         const int grid = a.ky_lines * ((a.kz_in + C - 1) / C);
-        k1_3d<NX><<<grid, F::T * C, smem, s>>>(a, stage);
+        const bool pz = NX >= 64 && a.pruned && a.kcx <= 6 * F::T - 1;
+        if (pz) {
+            if constexpr (NX >= 64) {
+                const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - 4) * F::T * C);
+                static size_t done = 0;
+                set_smem(k1_3d<NX, true>, smem, done);
+                k1_3d<NX, true><<<grid, F::T * C, smem, s>>>(a, stage);
+            }
+        } else {
+            const size_t smem = sizeof(cd) * (F::SMEM * C + F::E * F::T * C);
+            static size_t done = 0;
+            set_smem(k1_3d<NX, false>, smem, done);
+            k1_3d<NX, false><<<grid, F::T * C, smem, s>>>(a, stage);
+        }
     } else {
-        const size_t smem = sizeof(cd) * (F::SMEM * C + 2 * F::E * 256);
+        const size_t smem = sizeof(cd) * F::SMEM * C;
         static size_t done = 0;
         set_smem(k4_3d<NX>, smem, done);
         const int grid = a.ky_lines * ((a.kz_o + C - 1) / C);
