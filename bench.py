@@ -222,10 +222,8 @@ def run_our_arm(args):
         if dist is not None:
             dist.barrier()
 
-    # ---- warm-up
+    # ---- warm-up (also captures the per-step CUDA graph)
     sim.step(args.warmup)
-    sim.reset_stats()
-    sim.set_timing(True)
     l0 = sim.launch_count
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
@@ -240,13 +238,28 @@ def run_our_arm(args):
     barrier()
     sim.sync()
     launches = sim.launch_count - l0
-    stats = sim.kernel_stats()
-    sim.set_timing(False)
     ms = start.elapsed_time(end)
     if dist is not None:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+
+    # ---- instrumented repeat: CUDA events around every launch (no graph),
+    # for the per-kernel durations of the roofline
+    k_inst = max(1, min(args.steps, args.instrumented_steps))
+    sim.reset_stats()
+    sim.set_timing(True)
+    s2 = torch.cuda.Event(enable_timing=True)
+    e2 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s2.record(stream)
+    sim.step_async(k_inst)
+    e2.record(stream)
+    torch.cuda.synchronize()
+    sim.sync()
+    stats = sim.kernel_stats()
+    sim.set_timing(False)
+    inst_ms_step = s2.elapsed_time(e2) / k_inst
     ms_step = ms / args.steps
     value = ws * P * args.steps / (ms / 1e3) / 1e9
 
@@ -260,7 +273,16 @@ def run_our_arm(args):
                    "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None,
                    "share": v[0] / sum(x[0] for x in stats.values())} for k, v in stats.items()
                if v[1]}
-    step_bytes = sum(v[2] for v in stats.values()) / args.steps
+    step_bytes = sum(v[2] for v in stats.values()) / k_inst
+    # SURVEY.md 8(d) "fused minimal-pass" model of BASELINE's roofline:
+    # 55 F (ns2d) / 181 F (ns3d) HBM bytes per RK4 step, F = 16 * modes per field
+    F = 16.0 * (S // (1 if solver == "ns2d" else 3))
+    fmp_bytes = (55.0 if solver == "ns2d" else 181.0) * F
+    fmp = {"bytes_per_step": fmp_bytes,
+           "t_roof_ms_at_8TBps": fmp_bytes / 8e12 * 1e3,
+           "frac_of_8TBps": (fmp_bytes / 8e12 * 1e3) / ms_step,
+           "frac_of_measured_peak": (fmp_bytes / (peak * 1e9) * 1e3) / ms_step,
+           "note": "BASELINE target: >= 0.60 on 1 B200 (SURVEY 8(d) model, unpruned bytes)"}
     traffic = load_traffic(args.config)
 
     # ---- e2e through the C ABI with host buffers
@@ -318,7 +340,10 @@ def run_our_arm(args):
                          "algorithmic_bytes_per_launch": dbytes / dn if dn else None,
                          "step_algorithmic_GB": step_bytes / 1e9,
                          "step_frac": (step_bytes / (ms_step / 1e3) / 1e9) / peak},
+            "fmp_roofline": fmp,
             "kernels": kernels,
+            "instrumented": {"steps": k_inst, "ms_per_step": inst_ms_step,
+                             "note": "per-kernel CUDA events (no graph); roofline.achieved uses these"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": S * 16,
                     "d2h_bytes_per_step": S * 16, "steps": e2e_steps,
                     "path": "skg_set_state(host) + skg_step(1) + skg_get_state(host)"},
@@ -344,6 +369,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--instrumented-steps", type=int, default=20)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

@@ -118,6 +118,14 @@ struct skg_ctx {
     double st_ms[4] = {0, 0, 0, 0};
     long st_n[4] = {0, 0, 0, 0};
     double st_bytes[4] = {0, 0, 0, 0};
+
+    // CUDA graph of one RK step (all stage kernels), replayed per step when
+    // timing is off; recaptured when dt, the fast-path decision or the
+    // stream change.
+    cudaGraphExec_t gexec = nullptr;
+    double g_dt = 0.0;
+    bool g_pruned = false;
+    cudaStream_t g_stream = nullptr;
 };
 
 namespace {
@@ -316,19 +324,53 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
     CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
-    if (c->solver == 2) {
-        skg::Ns2dArgs a = args2d(c, dt);
-        const skg::LaunchHook hook = hook_of(c);
-        for (long s = 0; s < nsteps; ++s)
-            for (int st = 1; st <= nst; ++st)
-                CUDA_TRY(skg::ns2d_launch_stage(a, st, c->stream, &c->launches, hook));
-    } else {
-        skg::Ns3dArgs a = args3d(c, dt);
-        const skg::LaunchHook hook = hook_of(c);
-        for (long s = 0; s < nsteps; ++s)
-            for (int st = 1; st <= nst; ++st)
-                CUDA_TRY(skg::ns3d_launch_stage(a, st, c->stream, &c->launches, hook));
+    const skg::LaunchHook hook = hook_of(c);
+    long launches_per_step = 0;
+    auto one_step = [&](long* counter) -> cudaError_t {
+        cudaError_t e = cudaSuccess;
+        if (c->solver == 2) {
+            skg::Ns2dArgs a = args2d(c, dt);
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st)
+                e = skg::ns2d_launch_stage(a, st, c->stream, counter, hook);
+        } else {
+            skg::Ns3dArgs a = args3d(c, dt);
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st)
+                e = skg::ns3d_launch_stage(a, st, c->stream, counter, hook);
+        }
+        return e;
+    };
+    long s = 0;
+    if (nsteps > 0) {  // first step eagerly (also sets kernel attributes)
+        const long before = c->launches;
+        CUDA_TRY(one_step(&c->launches));
+        launches_per_step = c->launches - before;
+        s = 1;
     }
+    if (nsteps - s >= 2 && !c->timing && c->stream != nullptr) {
+        if (c->gexec && (c->g_dt != dt || c->g_pruned != c->pruned || c->g_stream != c->stream)) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        if (!c->gexec) {
+            cudaGraph_t graph;
+            long dummy = 0;
+            CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = one_step(&dummy);
+            cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
+            CUDA_TRY(e);
+            CUDA_TRY(e2);
+            CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
+            cudaGraphDestroy(graph);
+            c->g_dt = dt;
+            c->g_pruned = c->pruned;
+            c->g_stream = c->stream;
+        }
+        for (; s < nsteps; ++s) {
+            CUDA_TRY(cudaGraphLaunch(c->gexec, c->stream));
+            c->launches += launches_per_step;
+        }
+    }
+    for (; s < nsteps; ++s) CUDA_TRY(one_step(&c->launches));
     return SKG_OK;
 }
 
@@ -494,6 +536,7 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->d_count);
     cudaFree(c->d_red);
     harvest(c);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
