@@ -64,6 +64,22 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
                double dealias_coef, double nu, int scheme, int device);
 int skg_destroy(skg_ctx* ctx);
 
+/*
+ * Slab-decomposed context (ns2d): the dealiased state is split
+ * over the kept ky columns, physical space over x rows; each RK stage runs
+ * x-inverse -> all-to-all -> y pass -> all-to-all -> x-forward, with the
+ * transposes as grouped NCCL send/recv (one block per peer) on the context
+ * stream.  This process runs partition `rank` of `world` on `device`;
+ * nccl_id = the 128 bytes of skg_nccl_unique_id() from rank 0, broadcast by
+ * the caller.  nccl_id == NULL runs ALL `world` partitions in this process
+ * on one device with device copies as the exchange (tests).  State I/O is
+ * the full reference layout on every rank; tendency/energy are not offered.
+ */
+int skg_nccl_unique_id(char* out128);
+int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+                    double dealias_coef, double nu, int scheme, int device, int rank, int world,
+                    const char* nccl_id);
+
 /* Launch all work on this CUDA stream (cudaStream_t passed as void*);
  * NULL restores the context's own stream. */
 int skg_set_stream(skg_ctx* ctx, void* stream);
@@ -134,7 +150,8 @@ long skg_launch_count(const skg_ctx* ctx);
 /* Per-kernel-class device timing for the roofline report: when enabled,
  * CUDA events bracket every hot-path launch on the context stream.
  * Classes: 0 x-inverse pass, 1 physical-space pass, 2 x-forward pass + RK,
- * 3 other (3D y passes, decay, utilities).  skg_kernel_stats returns the
+ * 3 other (3D y passes, decay, utilities), 4 all-to-all exchange (bytes =
+ * bytes sent to other ranks).  skg_kernel_stats returns the
  * accumulated device milliseconds, launch count and ALGORITHMIC bytes (the
  * HBM bytes the kernel must move: fields crossing the pass boundary, read or
  * written once) of one class since the last reset. */

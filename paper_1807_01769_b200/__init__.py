@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     fft_inverse,
     lib_path,
     load_library,
+    nccl_unique_id,
 )
 
 __all__ = [

@@ -32,7 +32,7 @@ EXPORTS = [
     "skg_iteration", "skg_time", "skg_tendency", "skg_fft_forward", "skg_fft_inverse",
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
-    "skg_reset_stats",
+    "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist",
 ]
 
 
@@ -83,6 +83,9 @@ def load_library():
     L.skg_create.argtypes = [C.POINTER(vp), C.c_char_p, C.c_int, ip, dp, C.c_double, C.c_double,
                              C.c_int, C.c_int]
     L.skg_destroy.argtypes = [vp]
+    L.skg_create_dist.argtypes = [C.POINTER(vp), C.c_char_p, C.c_int, ip, dp, C.c_double,
+                                  C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p]
+    L.skg_nccl_unique_id.argtypes = [C.c_char_p]
     L.skg_set_stream.argtypes = [vp, vp]
     for f in ("skg_spect_size", "skg_phys_size", "skg_iteration", "skg_launch_count"):
         getattr(L, f).argtypes = [vp]
@@ -148,6 +151,15 @@ def _check_shape(shape):
     return shape
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for skg_create_dist (rank 0 creates, the caller broadcasts)."""
+    buf = C.create_string_buffer(128)
+    rc = load_library().skg_nccl_unique_id(buf)
+    if rc:
+        _raise(rc)
+    return buf.raw
+
+
 def fft_forward(u: np.ndarray, device: int = 0) -> np.ndarray:
     """FftPlan::forward (fft.cpp:92-98) of a real field on the GPU."""
     u = np.ascontiguousarray(u, dtype=np.float64)
@@ -180,7 +192,11 @@ class Simulation:
     with fixed dt and forcing/output off (the bench protocol, bench.cpp:51-85)."""
 
     def __init__(self, solver: str, n, nu: float = 0.0, dt: float = 0.0, scheme: str = "RK4",
-                 L=None, dealias_coef: float = 2.0 / 3.0, device: int = 0):
+                 L=None, dealias_coef: float = 2.0 / 3.0, device: int = 0, world: int = 1,
+                 rank: int = 0, nccl_id: bytes | None = None):
+        """world > 1: slab decomposition (ns2d).  With nccl_id (from
+        nccl_unique_id() on rank 0) this process runs partition `rank` over
+        NCCL; without it all `world` partitions run here on one device."""
         L_ = load_library()
         self.solver = solver
         self.n = tuple(int(x) for x in n)
@@ -194,8 +210,16 @@ class Simulation:
         h = C.c_void_p()
         cn = (C.c_int * self.dims)(*self.n)
         cL = None if L is None else (C.c_double * self.dims)(*L)
-        rc = L_.skg_create(C.byref(h), solver.encode(), self.dims, cn, cL, float(dealias_coef),
-                           self.nu, SKG_RK2 if self.scheme == "RK2" else SKG_RK4, int(device))
+        sch = SKG_RK2 if self.scheme == "RK2" else SKG_RK4
+        if world > 1:
+            rc = L_.skg_create_dist(C.byref(h), solver.encode(), self.dims, cn, cL,
+                                    float(dealias_coef), self.nu, sch, int(device), int(rank),
+                                    int(world), nccl_id)
+        else:
+            rc = L_.skg_create(C.byref(h), solver.encode(), self.dims, cn, cL, float(dealias_coef),
+                               self.nu, sch, int(device))
+        self.world = int(world)
+        self.rank = int(rank)
         if rc:
             _raise(rc)
         self._h = h
@@ -320,7 +344,7 @@ class Simulation:
     def launch_count(self) -> int:
         return load_library().skg_launch_count(self._h)
 
-    KERNEL_CLASSES = ("x_inverse", "physical", "x_forward_rk", "other")
+    KERNEL_CLASSES = ("x_inverse", "physical", "x_forward_rk", "other", "exchange")
 
     def set_timing(self, on: bool) -> None:
         self._call("skg_set_timing", C.c_int(1 if on else 0))

@@ -111,10 +111,12 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
     constexpr int NS = E - (ZHI - ZLO);  // stage-state slots per thread
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
-    const int ky = blockIdx.x * LPC + l;
-    const bool active = ky < a.ky_in;
+    // NM == 2 (fast path): local column kyl of this partition; NM == 4: G = 1
+    const int kyl = blockIdx.x * LPC + l;
+    const int ky = (NM == 2 ? a.c0 : 0) + kyl;
+    const bool active = kyl < (NM == 2 ? a.ncols : a.ky_in);
     if (a.flags->diverged) return;
-    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.flags->steps, 1);
+    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     cd* sm = smem + l * (F::SMEM + NS * T);
     cd* sv = sm + F::SMEM;  // thread-private slots sv[slot * T + t]
     const double kyv = a.ky_scale * (double)ky;
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
         const int i = t + T * e;
         const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
         if (keep) {
-            const size_t idx = (size_t)ky * NX + i;
+            const size_t idx = (size_t)kyl * NX + i;
             cp_async16(&sv[slot * T + t], a.u + idx);
             if (stage > 1) cp_async16(&kv[slot * T + t], kprev + idx);
         }
@@ -179,9 +181,19 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
         }
         F::template run<+1>(v, sm, t, wb);
         if (active) {
-            cd* out = pick(a, m);
+            if constexpr (NM == 2) {
+                cd* out = m == 0 ? a.sI[0] : a.sI[1];
 #pragma unroll
-            for (int e = 0; e < E; ++e) out[pidx(t + T * e, ky, a.ld_i)] = v[e];
+                for (int e = 0; e < E; ++e) {
+                    const int x = t + T * e;
+                    const int q = x / a.nrl, xl = x - q * a.nrl;
+                    out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl >> 1) * a.ncols + kyl) * 2 + (xl & 1)] = v[e];
+                }
+            } else {
+                cd* out = pick(a, m);
+#pragma unroll
+                for (int e = 0; e < E; ++e) out[pidx(t + T * e, ky, a.ld_i)] = v[e];
+            }
         }
     }
 }
@@ -413,15 +425,20 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     cd* st = sm + F::SMEM;
     const typename F::Bases wb = F::bases(t, a.twy);
     const int stride = gridDim.x * G;
-    const cd* P = a.I[0];  // X[psi]
-    const cd* Q = a.I[1];  // X[kx psi]
-    cd* outA = a.I[2];     // FT_y(v^2 - u^2) / N
-    cd* outB = a.I[3];     // FT_y(u v) / N
+    const cd* P = a.rI[0];  // X[psi]
+    const cd* Q = a.rI[1];  // X[kx psi]
+    cd* outA = a.sA[0];     // FT_y(v^2 - u^2) / N
+    cd* outB = a.sA[1];     // FT_y(u v) / N
+    // x runs over this partition's local rows; input column ky comes from
+    // the receive block of its owner r' (layout of r')
     auto issue = [&](int x) {
-        if (x >= a.nx) return;
+        if (x >= a.nrl) return;
         for (int i = t; i < a.ky_in; i += T) {
-            cp_async16(&st[i], P + pidx(x, i, ld));
-            cp_async16(&st[ld + i], Q + pidx(x, i, ld));
+            const int ro = a.kowner[i];
+            const int cs = a.cstart[ro], nc = a.cstart[ro + 1] - cs;
+            const size_t q = (size_t)a.nrl * cs + ((size_t)(x >> 1) * nc + (i - cs)) * 2 + (x & 1);
+            cp_async16(&st[i], P + q);
+            cp_async16(&st[ld + i], Q + q);
         }
     };
     int x = blockIdx.x * G + g;
@@ -429,10 +446,10 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     cp_async_commit();
     const double h = 0.5 * a.inv_n;
     // every group runs the same number of iterations (barriers inside)
-    const int iters = (a.nx + stride - 1) / stride;
+    const int iters = (a.nrl + stride - 1) / stride;
 #pragma unroll 1
     for (int it = 0; it < iters; ++it, x += stride) {
-        const bool active = x < a.nx;
+        const bool active = x < a.nrl;
         cp_async_wait_all();
         __syncthreads();
         cd v[E];
@@ -472,8 +489,8 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
             for (int k = t; k < a.ld_o; k += T) {
                 const cd zk = sm[F::pad(k)];
                 const cd zm = sm[F::pad((NY - k) & (NY - 1))];
-                outA[cpidx(x, k, a.nx)] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-                outB[cpidx(x, k, a.nx)] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+                outA[cpidx(x, k, a.nrl)] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                outB[cpidx(x, k, a.nrl)] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
             }
         }
     }
@@ -489,17 +506,23 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
     constexpr int ZLO = 6, ZHI = 10, NS = E - (ZHI - ZLO);
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
-    const int ky = blockIdx.x * LPC + l;
-    const bool active = ky < a.ld_o;
+    const int kyl = blockIdx.x * LPC + l;  // local column
+    const int ky = a.c0 + kyl;
+    const bool active = kyl < a.ncols;
     if (a.flags->diverged) return;
     cd* sm = smem + l * (F::SMEM + NS * T);
     cd* sv = sm + F::SMEM;
     const typename F::Bases wb = F::bases(t, a.twx);
     const double kyv = a.ky_scale * (double)ky;
+    const size_t blk = (size_t)2 * ((a.ncols + 1) >> 1) * a.nrl;  // receive block per source
+    auto ridx = [&](int x) {
+        const int ro = x / a.nrl, xl = x - ro * a.nrl;
+        return ro * blk + ((size_t)(kyl >> 1) * a.nrl + xl) * 2 + (kyl & 1);
+    };
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.I[2][cpidx(t + T * e, ky, NX)] : zero();
+        v[e] = active ? a.rA[0][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -510,7 +533,7 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.I[3][cpidx(t + T * e, ky, NX)] : zero();
+        v[e] = active ? a.rA[1][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
     if (!active) return;
     const bool final = a.rk2 ? stage == 2 : stage == 4;
@@ -525,7 +548,7 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
         if (abs(si) > a.kcx || (i == 0 && ky == 0)) continue;
         const double kxv = a.kx_scale * (double)si;
         const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
-        const size_t idx = (size_t)ky * NX + i;
+        const size_t idx = (size_t)kyl * NX + i;
         if (!final) {
             kout[idx] = kv;
         } else {
@@ -569,7 +592,7 @@ cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
     constexpr int LPC = T >= 256 ? 1 : 256 / T;
     constexpr int NS = PZ ? E - 4 : E;
     const size_t smem = sizeof(cd) * (F::SMEM + NS * T) * LPC;
-    const int grid = (a.ky_in + LPC - 1) / LPC;
+    const int grid = ((NM == 2 ? a.ncols : a.ky_in) + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
     static bool init = false;
     if (!init) {
@@ -634,7 +657,7 @@ cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int groups = (a.nx + G - 1) / G;
+    const int groups = (a.nrl + G - 1) / G;
     const int grid = groups < 2 * nsm ? groups : 2 * nsm;
     k3b_phys<NY><<<grid, F::T * G, smem, s>>>(a);
     return cudaGetLastError();
@@ -652,7 +675,8 @@ cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream
         cudaFuncSetAttribute(k4b_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    const int grid = (a.ld_o + LPC - 1) / LPC;
+    const int grid = (a.ncols + LPC - 1) / LPC;
+    if (grid == 0) return cudaSuccess;
     k4b_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
@@ -717,6 +741,32 @@ bool ns2d_supported(int nx, int ny) {
     return ok(nx) && ok(ny);
 }
 
+bool ns2d_fast_ok(const Ns2dArgs& a) { return fast_ok(a); }
+
+cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
+                           const LaunchHook& hook) {
+    cudaError_t err;
+    const double B = sizeof(cd);
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    const double kept = (2.0 * a.kcx + 1.0) * a.ncols;  // modes of this partition
+    const double Kc = a.kcy + 1.0;
+    if (pass == 0) {
+        hook.begin(0);
+        err = dispatch_fast_x(a, stage, true, s);
+        hook.end(0, B * (kept * (stage == 1 ? 1.0 : 2.0) + 2.0 * a.nx * a.ncols));
+    } else if (pass == 1) {
+        hook.begin(1);
+        err = dispatch_fast_y(a, s);
+        hook.end(1, B * (4.0 * a.nrl * Kc));
+    } else {
+        hook.begin(2);
+        err = dispatch_fast_x(a, stage, false, s);
+        hook.end(2, B * (2.0 * a.nx * a.ncols + (final ? (a.rk2 ? 3.0 : 5.0) : 1.0) * kept));
+    }
+    ++*launches;
+    return err;
+}
+
 cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches,
                               const LaunchHook& hook) {
     cudaError_t err;
@@ -728,17 +778,8 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
     const double inter = (double)a.nx * a.ky_in;    // one intermediate field
     const double rows = (double)a.nx * a.ld_o;      // tendency rows
     if (fast_ok(a)) {
-        const double s_kept = (2.0 * a.kcx + 1.0) * (a.kcy + 1.0);
-        hook.begin(0);
-        if ((err = dispatch_fast_x(a, stage, true, s)) != cudaSuccess) return err;
-        hook.end(0, B * (s_kept * (stage == 1 ? 1.0 : 2.0) + 2.0 * inter));
-        hook.begin(1);
-        if ((err = dispatch_fast_y(a, s)) != cudaSuccess) return err;
-        hook.end(1, B * (2.0 * inter + 2.0 * rows));
-        hook.begin(2);
-        if ((err = dispatch_fast_x(a, stage, false, s)) != cudaSuccess) return err;
-        hook.end(2, B * (2.0 * rows + (final ? (a.rk2 ? 3.0 : 5.0) : 1.0) * s_kept));
-        *launches += 3;
+        for (int pass = 0; pass < 3; ++pass)
+            if ((err = ns2d_fast_pass(a, pass, stage, s, launches, hook)) != cudaSuccess) return err;
         return cudaSuccess;
     }
     hook.begin(0);

@@ -59,6 +59,24 @@ struct Ns2dArgs {
     const cd* twx;      // W_nx table
     const cd* twy;      // W_ny table
     DevFlags* flags;
+    // Slab decomposition of the dealiased fast path (G = 1 on one GPU):
+    // this partition owns the kept ky columns [c0, c0 + ncols) (c0 even) of
+    // the state and the x rows [r nrl, (r + 1) nrl) of physical space.
+    //   sI/rI: x-inverse outputs X[psi], X[kx psi]; send block for rank q =
+    //          rows(q) x own columns, pair-interleaved ((xl/2) ncols + kyl) 2 + xl%2;
+    //          receive block from r' at nrl * cstart[r'] with r's layout.
+    //   sA/rA: product spectra; send layout ((k/2) nrl + xl) 2 + k%2 (blocks in
+    //          pair order), receive block from r' at r' * 2 npairs nrl.
+    // With G = 1 send and receive alias and the layouts reduce to the
+    // single-GPU ones.
+    int G, r, c0, ncols, nrl;
+    int lead;           // this partition advances the step counter
+    const int* kowner;  // owning rank of each kept column (kcy + 1 entries)
+    const int* cstart;  // first column of each rank (G + 1 entries)
+    cd* sI[2];
+    cd* rI[2];
+    cd* sA[2];
+    cd* rA[2];
 };
 
 // Optional per-launch instrumentation: hook(user, cls, 0, 0) before a launch
@@ -78,6 +96,11 @@ struct LaunchHook {
 // tendency evaluation of u into k1 (no RK arithmetic).
 cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long* launches,
                               const LaunchHook& hook);
+// The three passes of the fast path separately (slab decomposition):
+// pass 0 x-inverse, 1 y pass, 2 x-forward + RK.
+bool ns2d_fast_ok(const Ns2dArgs& a);
+cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
+                           const LaunchHook& hook);
 bool ns2d_supported(int nx, int ny);
 
 // ---------------------------------------------------------------- ns3d

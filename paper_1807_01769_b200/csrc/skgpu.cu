@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/skgpu.h"
 #include "skg_internal.h"
 
@@ -64,6 +66,19 @@ int cut_index(int n, double L, double coef, bool half) {
 
 }  // namespace
 
+// One slab of the decomposed ns2d state (see Ns2dArgs): owned kept ky
+// columns [c0, c0 + ncols) in CM layout and the exchange buffers.
+struct Part {
+    int r = 0;
+    int c0 = 0, ncols = 0;
+    cd* u = nullptr;
+    cd* k[3] = {nullptr, nullptr, nullptr};
+    cd* sI[2] = {nullptr, nullptr};
+    cd* rI[2] = {nullptr, nullptr};
+    cd* sA[2] = {nullptr, nullptr};
+    cd* rA[2] = {nullptr, nullptr};
+};
+
 struct skg_ctx {
     int device = 0;
     int solver = 2;  // 2: ns2d, 3: ns3d
@@ -105,6 +120,17 @@ struct skg_ctx {
     long pending_steps = 0;
     double pending_dt = 0.0;
 
+    // slab decomposition (ns2d): G partitions; `parts` are the ones this
+    // process runs (all G in the single-process test mode, one with NCCL)
+    bool dist = false;
+    int G = 1, grank = 0, nrl = 0;
+    std::vector<int> cstart;  // G + 1 entries
+    std::vector<Part> parts;
+    int* d_kowner = nullptr;
+    int* d_cstart = nullptr;
+    cd* cmfull = nullptr;     // full CM staging for set/get_state
+    ncclComm_t comm = nullptr;
+
     // per-kernel-class event timing (skg_set_timing)
     struct Pending {
         cudaEvent_t a, b;
@@ -115,9 +141,9 @@ struct skg_ctx {
     std::vector<cudaEvent_t> pool;
     std::vector<Pending> pend;
     cudaEvent_t cur = nullptr;
-    double st_ms[4] = {0, 0, 0, 0};
-    long st_n[4] = {0, 0, 0, 0};
-    double st_bytes[4] = {0, 0, 0, 0};
+    double st_ms[5] = {0, 0, 0, 0, 0};
+    long st_n[5] = {0, 0, 0, 0, 0};
+    double st_bytes[5] = {0, 0, 0, 0, 0};
 
     // CUDA graph of one RK step (all stage kernels), replayed per step when
     // timing is off; recaptured when dt, the fast-path decision or the
@@ -247,6 +273,39 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     a.twx = c->tw[0];
     a.twy = c->tw[1];
     a.flags = c->flags;
+    // one partition covering everything: send and receive buffers alias
+    a.G = 1;
+    a.r = 0;
+    a.lead = 1;
+    a.c0 = 0;
+    a.ncols = c->kc[1] + 1;
+    a.nrl = c->n[0];
+    a.kowner = c->d_kowner;
+    a.cstart = c->d_cstart;
+    a.sI[0] = a.rI[0] = a.I[0];
+    a.sI[1] = a.rI[1] = a.I[1];
+    a.sA[0] = a.rA[0] = a.I[2];
+    a.sA[1] = a.rA[1] = a.I[3];
+    return a;
+}
+
+skg::Ns2dArgs args2d_part(skg_ctx* c, double dt, const Part& p) {
+    skg::Ns2dArgs a = args2d(c, dt);
+    a.u = p.u;
+    a.k1 = p.k[0];
+    a.k2 = p.k[1];
+    a.k3 = p.k[2];
+    a.G = c->G;
+    a.r = p.r;
+    a.c0 = p.c0;
+    a.ncols = p.ncols;
+    a.nrl = c->nrl;
+    for (int f = 0; f < 2; ++f) {
+        a.sI[f] = p.sI[f];
+        a.rI[f] = p.rI[f];
+        a.sA[f] = p.sA[f];
+        a.rA[f] = p.rA[f];
+    }
     return a;
 }
 
@@ -315,6 +374,98 @@ int sync_and_check(skg_ctx* c, long nsteps, double dt) {
     return SKG_OK;
 }
 
+// All-to-all of the slab decomposition.  which = 0: x-inverse outputs
+// (rows(q) x cols(r) from r to q), 1: product spectra (cols(q) x rows(r)).
+// Single-process mode: device-to-device copies; otherwise NCCL send/recv
+// on the context stream (grouped, one block per peer).
+int exchange(skg_ctx* c, int which) {
+    const int G = c->G;
+    const size_t nrl = (size_t)c->nrl;
+    auto ncol = [&](int q) { return c->cstart[q + 1] - c->cstart[q]; };
+    auto npair = [&](int q) { return (size_t)(ncol(q) + 1) / 2; };
+    // block (source r -> destination q): pointers and element count
+    auto block = [&](const Part& src, const Part& dst, int f, cd** from, cd** to, size_t* cnt) {
+        const int r = src.r, q = dst.r;
+        if (which == 0) {
+            *cnt = nrl * ncol(r);
+            *from = src.sI[f] + (size_t)q * nrl * ncol(r);
+            *to = dst.rI[f] + nrl * c->cstart[r];
+        } else {
+            *cnt = 2 * npair(q) * nrl;
+            *from = src.sA[f] + (size_t)(c->cstart[q] / 2) * 2 * nrl;
+            *to = dst.rA[f] + (size_t)r * 2 * npair(q) * nrl;
+        }
+    };
+    const skg::LaunchHook hook = hook_of(c);
+    hook.begin(4);
+    double bytes = 0.0;
+    if (c->comm == nullptr) {  // all partitions local
+        for (const Part& src : c->parts)
+            for (const Part& dst : c->parts)
+                for (int f = 0; f < 2; ++f) {
+                    cd *from, *to;
+                    size_t cnt;
+                    block(src, dst, f, &from, &to, &cnt);
+                    if (cnt == 0) continue;
+                    CUDA_TRY(cudaMemcpyAsync(to, from, cnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    if (src.r != dst.r) bytes += cnt * sizeof(cd);
+                }
+    } else {
+        const Part& me = c->parts[0];
+        const int r = me.r;
+        ncclResult_t nr = ncclGroupStart();
+        for (int q = 0; q < G && nr == ncclSuccess; ++q) {
+            for (int f = 0; f < 2 && nr == ncclSuccess; ++f) {
+                cd *sptr, *rptr;
+                size_t scnt, rcnt;
+                if (which == 0) {
+                    sptr = me.sI[f] + (size_t)q * nrl * ncol(r);
+                    scnt = nrl * ncol(r);
+                    rptr = me.rI[f] + nrl * c->cstart[q];
+                    rcnt = nrl * ncol(q);
+                } else {
+                    sptr = me.sA[f] + (size_t)(c->cstart[q] / 2) * 2 * nrl;
+                    scnt = 2 * npair(q) * nrl;
+                    rptr = me.rA[f] + (size_t)q * 2 * npair(r) * nrl;
+                    rcnt = 2 * npair(r) * nrl;
+                }
+                if (q == r) {
+                    if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    continue;
+                }
+                if (scnt) nr = ncclSend(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
+                if (nr == ncclSuccess && rcnt) nr = ncclRecv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                bytes += scnt * sizeof(cd);
+            }
+        }
+        ncclResult_t ne = ncclGroupEnd();
+        if (nr != ncclSuccess || ne != ncclSuccess)
+            return fail(SKG_ENCCL, std::string("all-to-all: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+    }
+    hook.end(4, bytes);
+    ++c->launches;
+    return SKG_OK;
+}
+
+int enqueue_dist_step(skg_ctx* c, double dt, long* counter) {
+    const int nst = c->scheme == SKG_RK2 ? 2 : 4;
+    const skg::LaunchHook hook = hook_of(c);
+    for (int st = 1; st <= nst; ++st) {
+        for (int pass = 0; pass < 3; ++pass) {
+            for (const Part& p : c->parts) {
+                skg::Ns2dArgs a = args2d_part(c, dt, p);
+                a.lead = p.r == 0 ? 1 : 0;
+                CUDA_TRY(skg::ns2d_fast_pass(a, pass, st, c->stream, counter, hook));
+            }
+            if (pass < 2) {
+                int rc = exchange(c, pass);
+                if (rc) return rc;
+            }
+        }
+    }
+    return SKG_OK;
+}
+
 int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     if (!(dt > 0.0)) return fail(SKG_ECONFIG, "step: nonpositive dt");
     if (nsteps < 0) return fail(SKG_ECONFIG, "step: negative step count");
@@ -326,6 +477,13 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
     long launches_per_step = 0;
+    if (c->dist) {
+        for (long s = 0; s < nsteps; ++s) {
+            int rc2 = enqueue_dist_step(c, dt, &c->launches);
+            if (rc2) return rc2;
+        }
+        return SKG_OK;
+    }
     auto one_step = [&](long* counter) -> cudaError_t {
         cudaError_t e = cudaSuccess;
         if (c->solver == 2) {
@@ -389,6 +547,17 @@ int decide_pruned(skg_ctx* c, const cd* d_ref_layout) {
 int load_state_from_io(skg_ctx* c) {
     int rc = decide_pruned(c, c->io);
     if (rc) return rc;
+    if (c->dist) {
+        if (!c->pruned)
+            return fail(SKG_EUNSUPPORTED,
+                        "slab-decomposed contexts need a dealiased state (masked modes exactly 0)");
+        CUDA_TRY(skg::launch_transpose_c(c->io, c->cmfull, c->n[0], c->nh, 0, c->stream, &c->launches));
+        for (const Part& p : c->parts)
+            if (p.ncols)
+                CUDA_TRY(cudaMemcpyAsync(p.u, c->cmfull + (size_t)p.c0 * c->n[0],
+                                         sizeof(cd) * p.ncols * c->n[0], cudaMemcpyDeviceToDevice, c->stream));
+        return SKG_OK;
+    }
     if (c->solver == 2) {
         CUDA_TRY(skg::launch_transpose_c(c->io, c->u, c->n[0], c->nh, 0, c->stream, &c->launches));
     } else {
@@ -399,6 +568,20 @@ int load_state_from_io(skg_ctx* c) {
 }
 
 int store_state_to_io(skg_ctx* c, const cd* src) {
+    if (c->dist) {  // gather the slabs (masked columns are exactly 0)
+        CUDA_TRY(cudaMemsetAsync(c->cmfull, 0, sizeof(cd) * c->S, c->stream));
+        for (const Part& p : c->parts)
+            if (p.ncols)
+                CUDA_TRY(cudaMemcpyAsync(c->cmfull + (size_t)p.c0 * c->n[0], p.u,
+                                         sizeof(cd) * p.ncols * c->n[0], cudaMemcpyDeviceToDevice, c->stream));
+        if (c->comm) {
+            const ncclResult_t nr = ncclAllReduce(c->cmfull, c->cmfull, 2 * (size_t)c->S, ncclDouble,
+                                                  ncclSum, c->comm, c->stream);
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+        }
+        CUDA_TRY(skg::launch_transpose_c(c->cmfull, c->io, c->nh, c->n[0], 0, c->stream, &c->launches));
+        return SKG_OK;
+    }
     if (c->solver == 2) {
         CUDA_TRY(skg::launch_transpose_c(src, c->io, c->nh, c->n[0], 0, c->stream, &c->launches));
     } else {
@@ -434,8 +617,33 @@ const char* skg_version(void) { return "skgpu 0.1.0 sm_100a"; }
 
 const char* skg_last_error(void) { return g_err.c_str(); }
 
+static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+                       double dealias_coef, double nu, int scheme, int device, int rank, int world,
+                       const char* nccl_id);
+
 int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                double dealias_coef, double nu, int scheme, int device) {
+    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, 0, 1, nullptr);
+}
+
+int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+                    double dealias_coef, double nu, int scheme, int device, int rank, int world,
+                    const char* nccl_id) {
+    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, rank, world, nccl_id);
+}
+
+int skg_nccl_unique_id(char* out128) {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+    return SKG_OK;
+}
+
+static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+                       double dealias_coef, double nu, int scheme, int device, int rank, int world,
+                       const char* nccl_id) {
     if (!out) return fail(SKG_ECONFIG, "create: null output pointer");
     *out = nullptr;
     std::string s = solver ? solver : "";
@@ -460,6 +668,11 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(SKG_ECUDA, "no CUDA device visible (the library has no CPU path)");
     if (device < 0 || device >= ndev) return fail(SKG_ECONFIG, "device ordinal out of range");
+    if (world < 1 || rank < 0 || rank >= world) return fail(SKG_ECONFIG, "bad rank / world size");
+    if (world > 1 && sid != 2)
+        return fail(SKG_EUNSUPPORTED, "slab decomposition is implemented for ns2d only");
+    if (world > 1 && n[0] % (2 * world))
+        return fail(SKG_ECONFIG, "nx must be divisible by 2 * world for the slab decomposition");
 
     auto c = new skg_ctx();
     c->device = device;
@@ -491,14 +704,64 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
     c->stream = c->own;
     const size_t S = (size_t)c->S;
     auto alloc = [&](void** p, size_t bytes) {
-        if (cudaMalloc(p, bytes) != cudaSuccess) return false;
-        return cudaMemset(*p, 0, bytes) == cudaSuccess;
+        if (cudaMalloc(p, bytes < 16 ? 16 : bytes) != cudaSuccess) return false;
+        return cudaMemset(*p, 0, bytes < 16 ? 16 : bytes) == cudaSuccess;
     };
-    bool ok = alloc((void**)&c->u, sizeof(cd) * S * c->nvars);
-    for (int i = 0; i < 3 && ok; ++i) ok = alloc((void**)&c->k[i], sizeof(cd) * S * c->nvars);
-    if (sid == 2) c->inter_elems = 5 * S;  // 4 intermediates + tendency rows
-    else c->inter_elems = 11 * (size_t)n[0] * n[1] * c->nh;  // A[5] (C aliases) + B[6] (D aliases)
-    ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
+    bool ok = true;
+    c->dist = world > 1;
+    c->G = world;
+    c->grank = rank;
+    if (sid == 2) {  // column partition of the kept ky columns, row partition of x
+        const int Kc = c->kc[1] + 1, PP = (Kc + 1) / 2;
+        if (PP < world) return cleanup(SKG_ECONFIG, "more ranks than kept ky column pairs");
+        c->cstart.resize(world + 1);
+        for (int q = 0; q < world; ++q) c->cstart[q] = 2 * (int)((long long)q * PP / world);
+        c->cstart[world] = Kc;
+        c->nrl = n[0] / world;
+        std::vector<int> owner(Kc);
+        for (int q = 0; q < world; ++q)
+            for (int k = c->cstart[q]; k < c->cstart[q + 1]; ++k) owner[k] = q;
+        ok = ok && alloc((void**)&c->d_kowner, sizeof(int) * Kc);
+        ok = ok && alloc((void**)&c->d_cstart, sizeof(int) * (world + 1));
+        if (ok) {
+            cudaMemcpy(c->d_kowner, owner.data(), sizeof(int) * Kc, cudaMemcpyHostToDevice);
+            cudaMemcpy(c->d_cstart, c->cstart.data(), sizeof(int) * (world + 1), cudaMemcpyHostToDevice);
+        }
+    }
+    if (c->dist) {
+        const int Kc = c->kc[1] + 1, PP = (Kc + 1) / 2;
+        const size_t nx = n[0], nrl = c->nrl;
+        for (int q = 0; q < world; ++q) {
+            if (nccl_id && q != rank) continue;  // NCCL: only this process's slab
+            Part p;
+            p.r = q;
+            p.c0 = c->cstart[q];
+            p.ncols = c->cstart[q + 1] - c->cstart[q];
+            const size_t npairs = (p.ncols + 1) / 2;
+            ok = ok && alloc((void**)&p.u, sizeof(cd) * p.ncols * nx);
+            for (int i = 0; i < 3; ++i) ok = ok && alloc((void**)&p.k[i], sizeof(cd) * p.ncols * nx);
+            for (int f = 0; f < 2; ++f) {
+                ok = ok && alloc((void**)&p.sI[f], sizeof(cd) * nx * p.ncols);
+                ok = ok && alloc((void**)&p.rI[f], sizeof(cd) * nrl * Kc);
+                ok = ok && alloc((void**)&p.sA[f], sizeof(cd) * 2 * PP * nrl);
+                ok = ok && alloc((void**)&p.rA[f], sizeof(cd) * world * 2 * npairs * nrl);
+            }
+            c->parts.push_back(p);
+        }
+        ok = ok && alloc((void**)&c->cmfull, sizeof(cd) * S);
+        if (ok && nccl_id) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            const ncclResult_t nr = ncclCommInitRank(&c->comm, world, id, rank);
+            if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
+        }
+    } else {
+        ok = ok && alloc((void**)&c->u, sizeof(cd) * S * c->nvars);
+        for (int i = 0; i < 3 && ok; ++i) ok = alloc((void**)&c->k[i], sizeof(cd) * S * c->nvars);
+        if (sid == 2) c->inter_elems = 5 * S;  // 4 intermediates + tendency rows
+        else c->inter_elems = 11 * (size_t)n[0] * n[1] * c->nh;  // A[5] (C aliases) + B[6] (D aliases)
+        ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
+    }
     ok = ok && alloc((void**)&c->io, sizeof(cd) * S * c->nvars);
     ok = ok && alloc((void**)&c->phys, sizeof(double) * (size_t)c->P);
     ok = ok && alloc((void**)&c->work, sizeof(cd) * S);
@@ -537,6 +800,20 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->d_red);
     harvest(c);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (Part& p : c->parts) {
+        cudaFree(p.u);
+        for (auto q : p.k) cudaFree(q);
+        for (int f = 0; f < 2; ++f) {
+            cudaFree(p.sI[f]);
+            cudaFree(p.rI[f]);
+            cudaFree(p.sA[f]);
+            cudaFree(p.rA[f]);
+        }
+    }
+    cudaFree(c->cmfull);
+    cudaFree(c->d_kowner);
+    cudaFree(c->d_cstart);
+    if (c->comm) ncclCommDestroy(c->comm);
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -618,6 +895,7 @@ int skg_step(skg_ctx* c, double dt, long nsteps) {
 }
 
 int skg_tendency(skg_ctx* c, const double* in, double* out) {
+    if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_tendency on a slab-decomposed context");
     CUDA_TRY(cudaSetDevice(c->device));
     if (c->pending_steps) {
         int rc = skg_sync(c);
@@ -766,7 +1044,7 @@ int skg_reset_stats(skg_ctx* c) {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     harvest(c);
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 5; ++i) {
         c->st_ms[i] = 0;
         c->st_n[i] = 0;
         c->st_bytes[i] = 0;
@@ -775,7 +1053,7 @@ int skg_reset_stats(skg_ctx* c) {
 }
 
 int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, double* bytes) {
-    if (cls < 0 || cls > 3) return fail(SKG_ESHAPE, "kernel class out of range");
+    if (cls < 0 || cls > 4) return fail(SKG_ESHAPE, "kernel class out of range");
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     harvest(c);
@@ -786,6 +1064,7 @@ int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, doub
 }
 
 int skg_energy(skg_ctx* c, double* energy, double* enstrophy) {
+    if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_energy on a slab-decomposed context");
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
                                 c->d_red, c->stream, &c->launches));
