@@ -209,7 +209,15 @@ def run_our_arm(args):
     solver, n, nu, dt, u0 = make_input(args.config)
     P = int(np.prod(n))
     S = u0.size  # complex modes over all variables
-    sim = api.Simulation(solver, n, nu, dt, device=local)
+    slab = ws > 1 and solver == "ns2d"
+    if slab:
+        # ns2d slab decomposition over the ranks (strong scaling of
+        # one grid), transposes as NCCL all-to-all inside libskgpu
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
+    else:
+        sim = api.Simulation(solver, n, nu, dt, device=local)
     # a dedicated (non-default) stream: the library launches on it and the
     # CUDA events below are recorded on the same stream
     stream = torch.cuda.Stream(device=local)
@@ -261,11 +269,12 @@ def run_our_arm(args):
     sim.set_timing(False)
     inst_ms_step = s2.elapsed_time(e2) / k_inst
     ms_step = ms / args.steps
-    value = ws * P * args.steps / (ms / 1e3) / 1e9
+    units = P if slab else ws * P  # grid points advanced per step by the whole job
+    value = units * args.steps / (ms / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel class
     peak, peak_src = load_peaks()
-    dom = max(stats, key=lambda k: stats[k][0])
+    dom = max((k for k in stats if k != "exchange"), key=lambda k: stats[k][0])
     dms, dn, dbytes = stats[dom]
     achieved = (dbytes / dn) / ((dms / dn) / 1e3) / 1e9 if dn else 0.0
     kernels = {k: {"ms_total": v[0], "launches": v[1],
@@ -273,7 +282,7 @@ def run_our_arm(args):
                    "GBps": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None,
                    "share": v[0] / sum(x[0] for x in stats.values())} for k, v in stats.items()
                if v[1]}
-    step_bytes = sum(v[2] for v in stats.values()) / k_inst
+    step_bytes = sum(v[2] for k, v in stats.items() if k != "exchange") / k_inst
     # SURVEY.md 8(d) "fused minimal-pass" model of BASELINE's roofline:
     # 55 F (ns2d) / 181 F (ns3d) HBM bytes per RK4 step, F = 16 * modes per field
     F = 16.0 * (S // (1 if solver == "ns2d" else 3))
@@ -303,7 +312,7 @@ def run_our_arm(args):
         t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
-    e2e_value = ws * P * e2e_steps / t_e2e / 1e9
+    e2e_value = units * e2e_steps / t_e2e / 1e9
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -324,13 +333,15 @@ def run_our_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded spectral Gaussian IC, BASELINE recipe)",
             "config": {
                 "workload": f"{args.config}: {solver} {'x'.join(map(str, n))} RK4 step, "
                             f"nu={nu}, dt={dt:.6g} (CFL 0.5)",
-                "solver": solver, "n": list(n), "global_batch": ws,
-                "parallelism": "replicas" if ws > 1 else "single-gpu",
+                "solver": solver, "n": list(n), "global_batch": 1 if slab else ws,
+                "parallelism": (f"slab{ws} (NCCL all-to-all)" if slab else
+                                "replicas (ns3d slab decomposition not built)" if ws > 1 else
+                                "single-gpu"),
                 "l2": "every field array > 126 MB L2; no flush needed",
                 "dealiased_fast_path": pruned,
             },
@@ -341,6 +352,10 @@ def run_our_arm(args):
                          "step_algorithmic_GB": step_bytes / 1e9,
                          "step_frac": (step_bytes / (ms_step / 1e3) / 1e9) / peak},
             "fmp_roofline": fmp,
+            "all_to_all": ({"bytes_per_step_per_gpu": stats["exchange"][2] / k_inst,
+                            "ms_per_step": stats["exchange"][0] / k_inst,
+                            "t_roof_ms_at_900GBps": stats["exchange"][2] / k_inst / 900e9 * 1e3}
+                           if slab else None),
             "kernels": kernels,
             "instrumented": {"steps": k_inst, "ms_per_step": inst_ms_step,
                              "note": "per-kernel CUDA events (no graph); roofline.achieved uses these"},
