@@ -1,0 +1,101 @@
+"""numpy model of the ns2d slab decomposition of libskgpu (csrc/skgpu.cu
+create_impl / exchange, csrc/ns2d.cu fast-path kernels): the same column /
+row partitions and the same pair-interleaved send/receive block layouts,
+exchanged with torch.distributed.all_to_all_single.  Used by
+tests/test_dist_cpu.py (gloo, world_size 2 and 4) to check the host-side
+decomposition logic against the undecomposed oracle tendency.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from oracle import spectral_np as O
+
+
+def partition(Kc, nx, G):
+    PP = (Kc + 1) // 2
+    cstart = [2 * (q * PP // G) for q in range(G)] + [Kc]
+    return cstart, nx // G
+
+
+def _a2a(send_blocks, recv_sizes):
+    """all_to_all_single of complex blocks (lists indexed by peer)."""
+    s = torch.from_numpy(np.concatenate([b.view(np.float64) for b in send_blocks]))
+    r = torch.empty(2 * sum(recv_sizes), dtype=torch.float64)
+    dist.all_to_all_single(r, s, output_split_sizes=[2 * x for x in recv_sizes],
+                           input_split_sizes=[b.size * 2 for b in send_blocks])
+    out, o = [], 0
+    rn = r.numpy().view(np.complex128)
+    for x in recv_sizes:
+        out.append(rn[o:o + x])
+        o += x
+    return out
+
+
+def slab_tendency(w_full, n, rank, G):
+    """Dealiased-path tendency of the full state, computed on the slab of
+    `rank`; returns this rank's kept columns of N_hat (CM layout [kyl][kx])."""
+    nx, ny = n
+    kx, ky = O.k_axes(n)
+    kcx = int(np.abs(kx[O.dealias_mask((nx, ny))[:, 0].astype(bool)]).max())
+    Kc = int(O.dealias_mask(n)[0].sum())
+    cstart, nrl = partition(Kc, nx, G)
+    c0, c1 = cstart[rank], cstart[rank + 1]
+    ncols = c1 - c0
+    # x-inverse of psi and kx psi on own columns (CM: column ky over kx)
+    W = w_full[0][:, c0:c1]                               # (nx, ncols)
+    KX = kx[:, None]
+    KY = ky[None, c0:c1]
+    ksq = KX ** 2 + KY ** 2
+    psi = np.where(ksq == 0, 0, W / np.where(ksq == 0, 1, ksq))
+    X0 = np.fft.ifft(psi, axis=0) * nx                    # (x, kyl)
+    X1 = np.fft.ifft(KX * psi, axis=0) * nx
+    # send block to q: rows(q) x own cols, ((xl/2) ncols + kyl) 2 + xl%2
+    def pack_I(X, q):
+        blk = X[q * nrl:(q + 1) * nrl, :]                 # (xl, kyl)
+        return blk.reshape(nrl // 2, 2, ncols).transpose(0, 2, 1).reshape(-1).copy()
+    rs = [nrl * (cstart[q + 1] - cstart[q]) for q in range(G)]
+    R0 = _a2a([pack_I(X0, q) for q in range(G)], rs)
+    R1 = _a2a([pack_I(X1, q) for q in range(G)], rs)
+    # y pass on own rows: assemble rows over all kept ky from the owners
+    def unpack_rows(R):
+        cols = []
+        for q in range(G):
+            nc = cstart[q + 1] - cstart[q]
+            cols.append(R[q].reshape(nrl // 2, nc, 2).transpose(0, 2, 1).reshape(nrl, nc))
+        return np.concatenate(cols, axis=1)               # (xl, Kc)
+    P0, P1 = unpack_rows(R0), unpack_rows(R1)
+    kyk = ky[:Kc][None, :]
+    uh = 1j * kyk * P0                                    # u: i ky X[psi]
+    vh = -1j * P1                                         # v: -i X[kx psi]
+    def c2r_rows(h):
+        full = np.zeros((nrl, ny // 2 + 1), complex)
+        full[:, :Kc] = h
+        full[:, 0] = full[:, 0].real
+        return np.fft.irfft(full, n=ny, axis=1) * ny
+    u, v = c2r_rows(uh), c2r_rows(vh)
+    A = np.fft.rfft(v * v - u * u, axis=1)[:, :Kc] / (nx * ny)
+    B = np.fft.rfft(u * v, axis=1)[:, :Kc] / (nx * ny)
+    # send to q: cols(q) x own rows, ((k/2) nrl + xl) 2 + k%2 in pair order
+    def pack_A(M, q):
+        a, b = cstart[q], cstart[q + 1]
+        np_q = (b - a + 1) // 2
+        blk = np.zeros((nrl, 2 * np_q), complex)
+        blk[:, :b - a] = M[:, a:b]
+        return blk.reshape(nrl, np_q, 2).transpose(1, 0, 2).reshape(-1).copy()
+    npair_r = (ncols + 1) // 2
+    RA = _a2a([pack_A(A, q) for q in range(G)], [2 * npair_r * nrl] * G)
+    RB = _a2a([pack_A(B, q) for q in range(G)], [2 * npair_r * nrl] * G)
+    def unpack_cols(R):
+        rows = [R[q].reshape(npair_r, nrl, 2).transpose(1, 0, 2).reshape(nrl, 2 * npair_r)[:, :ncols]
+                for q in range(G)]
+        return np.concatenate(rows, axis=0)               # (x, kyl)
+    Ah, Bh = np.fft.fft(unpack_cols(RA), axis=0), np.fft.fft(unpack_cols(RB), axis=0)
+    N = KX * KY * Ah + (KX ** 2 - KY ** 2) * Bh
+    keep = np.abs(kx)[:, None] <= kcx
+    N = np.where(keep, N, 0)
+    if c0 == 0:
+        N[0, 0] = 0
+    return N, c0, c1
