@@ -108,6 +108,15 @@ int skg_step(skg_ctx* ctx, double dt, long nsteps);
 int skg_step_async(skg_ctx* ctx, double dt, long nsteps);
 int skg_sync(skg_ctx* ctx);
 
+/* Simulation::run() with n_iters = nsteps (simulation.cpp:565-590): as
+ * skg_step, plus the per-step means the reference's OutputManager writes
+ * every step (output.cpp:204-214): series[3 i + {0,1,2}] = energy, enstrophy
+ * (0 for ns3d) and dissipation rate after step i (simulation.cpp:592-615),
+ * reduced on the device (fused into the final RK update on the dealiased
+ * path).  series may be NULL.  On divergence the entries after the failing
+ * step are 0. */
+int skg_run(skg_ctx* ctx, double dt, long nsteps, double* series);
+
 /* Iteration count and time, as Simulation::iteration()/t(). */
 long skg_iteration(const skg_ctx* ctx);
 double skg_time(const skg_ctx* ctx);

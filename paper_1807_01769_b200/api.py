@@ -32,7 +32,7 @@ EXPORTS = [
     "skg_iteration", "skg_time", "skg_tendency", "skg_fft_forward", "skg_fft_inverse",
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
-    "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist",
+    "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
 ]
 
 
@@ -97,6 +97,7 @@ def load_library():
     for f in ("skg_set_state", "skg_get_state", "skg_set_state_device", "skg_get_state_device"):
         getattr(L, f).argtypes = [vp, C.c_void_p]
     L.skg_step.argtypes = [vp, C.c_double, C.c_long]
+    L.skg_run.argtypes = [vp, C.c_double, C.c_long, C.c_void_p]
     L.skg_step_async.argtypes = [vp, C.c_double, C.c_long]
     L.skg_sync.argtypes = [vp]
     L.skg_tendency.argtypes = [vp, C.c_void_p, C.c_void_p]
@@ -290,9 +291,15 @@ class Simulation:
     def sync(self) -> None:
         self._call("skg_sync")
 
-    def run(self, n_iters: int) -> None:
-        """Simulation::run with n_iters (simulation.cpp:565-590)."""
-        self.step(n_iters)
+    def run(self, n_iters: int, dt: float | None = None):
+        """Simulation::run with n_iters (simulation.cpp:565-590).  Returns the
+        per-step means the reference's OutputManager records every step
+        (output.cpp:204-214): an (n_iters, 3) array of energy, enstrophy and
+        dissipation rate after each step."""
+        dt = self.dt if dt is None else float(dt)
+        series = np.zeros((int(n_iters), 3), np.float64)
+        self._call("skg_run", C.c_double(dt), C.c_long(int(n_iters)), _ptr(series))
+        return series
 
     def compute_tendency(self, spect: np.ndarray) -> np.ndarray:
         s = np.ascontiguousarray(spect, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)

@@ -535,12 +535,20 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
     for (int e = 0; e < E; ++e)
         v[e] = active ? a.rA[1][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
-    if (!active) return;
     const bool final = a.rk2 ? stage == 2 : stage == 4;
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     bool bad = false;
+    // per-step E, Z, eps of the new state (Simulation::energy / enstrophy /
+    // dissipation_rate, simulation.cpp:592-615; ns2d mode_energy solvers.cpp:211-218)
+    double sE = 0.0, sZ = 0.0, sD = 0.0;
+    const double pw = (ky == 0 || ky == a.nh - 1) ? 1.0 : 2.0;
+    if (final && a.diag && active && ky == 0 && t == 0) {
+        const cd u0 = a.u[(size_t)kyl * NX];  // mean mode: untouched, enstrophy only
+        sZ += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
+        if (!active) break;
         if (e >= ZLO && e < ZHI) continue;  // |kx| > kcx there
         const int slot = e < ZLO ? e : e - (ZHI - ZLO);
         const int i = t + T * e;
@@ -576,8 +584,18 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
             }
             a.u[idx] = un;
             bad |= !finite2(un);
+            if (a.diag) {
+                const double ksq = kxv * kxv + kyv * kyv;
+                const double n2 = un.x * un.x + un.y * un.y;
+                sZ += 0.5 * pw * n2;
+                if (ksq > 0.0) {
+                    sE += 0.5 * pw * n2 / ksq;
+                    if (a.has_sigma) sD += 2.0 * a.nu * ksq * (0.5 * pw * n2 / ksq);
+                }
+            }
         }
     }
+    if (final && a.diag) diag_accumulate(a.diag + 3 * (a.flags->steps - 1), sE, sZ, sD);
     if (bad) {
         atomicMin(&a.flags->div_var, 0);
         atomicExch(&a.flags->div_step, a.flags->steps);

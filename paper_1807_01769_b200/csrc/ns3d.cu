@@ -419,7 +419,6 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
             for (int e = 0; e < E; ++e) line[(size_t)(t + T * e) * xstr] = v[e];
         }
     }
-    if (!active) return;
     const bool final = a.rk2 ? stage == 2 : stage == 4;
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     const double kyv = a.ky_scale * (double)sky;
@@ -427,8 +426,19 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
     const cd* l0 = a.B + lbase;
     const cd* l1 = a.B + a.fstride + lbase;
     int bad = 3;
+    // per-step E and eps of the new state (Solver::mode_energy default,
+    // simulation.cpp:163-170; dissipation_rate simulation.cpp:608-615)
+    double sE = 0.0, sD = 0.0;
+    const double pw = (kz == 0 || kz == a.nh - 1) ? 1.0 : 2.0;
+    if (final && a.diag && active && ky == 0 && kz == 0 && t == 0) {
+        for (int c = 0; c < 3; ++c) {  // mean flow: untouched, energy only
+            const cd u0 = a.u[c * a.vstride];
+            sE += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
+        }
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
+        if (!active) break;
         const int i = t + T * e;
         const int si = signed_index(i, NX);
         bool keep = keep_y && abs(si) <= a.kcx;
@@ -484,8 +494,16 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
             }
             a.u[idx] = un;
             if (!finite2(un) && c < bad) bad = c;
+            if (a.diag) {
+                const double n2 = un.x * un.x + un.y * un.y;
+                const double kxv = a.kx_scale * (double)si;
+                const double ksq = kxv * kxv + kyv * kyv + kzv * kzv;
+                sE += 0.5 * pw * n2;
+                if (a.has_sigma) sD += 2.0 * a.nu * ksq * (0.5 * pw * n2);
+            }
         }
     }
+    if (final && a.diag) diag_accumulate(a.diag + 3 * (a.flags->steps - 1), sE, 0.0, sD);
     if (bad < 3) {
         atomicMin(&a.flags->div_var, bad);
         atomicExch(&a.flags->div_step, a.flags->steps);

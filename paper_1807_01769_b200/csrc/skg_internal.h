@@ -59,6 +59,8 @@ struct Ns2dArgs {
     const cd* twx;      // W_nx table
     const cd* twy;      // W_ny table
     DevFlags* flags;
+    double* diag;       // per-step (E, Z, eps) series, slot steps-1; nullptr = off
+    double nu;
     // Slab decomposition of the dealiased fast path (G = 1 on one GPU):
     // this partition owns the kept ky columns [c0, c0 + ncols) (c0 even) of
     // the state and the x rows [r nrl, (r + 1) nrl) of physical space.
@@ -132,7 +134,23 @@ struct Ns3dArgs {
     size_t fstride;      // elements per intermediate field (nx*ny*nh)
     const cd *twx, *twy, *twz;
     DevFlags* flags;
+    double* diag;           // per-step (E, Z, eps) series, slot steps-1; nullptr = off
+    double nu;
 };
+
+// Warp-sum three doubles and add them to slot[0..2] (all 32 lanes must call).
+__device__ __forceinline__ void diag_accumulate(double* slot, double e, double z, double d) {
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_down_sync(0xffffffffu, e, o);
+        z += __shfl_down_sync(0xffffffffu, z, o);
+        d += __shfl_down_sync(0xffffffffu, d, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (e != 0.0) atomicAdd(&slot[0], e);
+        if (z != 0.0) atomicAdd(&slot[1], z);
+        if (d != 0.0) atomicAdd(&slot[2], d);
+    }
+}
 cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
                               const LaunchHook& hook);
 bool ns3d_supported(int nx, int ny, int nz);
@@ -147,7 +165,8 @@ cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double
                              int axis, double* d_k, unsigned char* d_mask, cudaStream_t s,
                              long* launches);
 cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* kscale, int nvars,
-                          int solver2d, double* d_out, cudaStream_t s, long* launches);
+                          int solver2d, double* d_out, cudaStream_t s, long* launches,
+                          double nu = 0.0, const int* steps = nullptr, bool zero_first = true);
 
 // Plain transforms on the context grid / arbitrary shapes (fft_ops.cu).
 // u: row-major real (n0..n_{d-1}); uhat: row-major half spectrum.

@@ -130,6 +130,7 @@ struct skg_ctx {
     int* d_cstart = nullptr;
     cd* cmfull = nullptr;     // full CM staging for set/get_state
     ncclComm_t comm = nullptr;
+    double* diag = nullptr;   // per-step (E, Z, eps) series of skg_run (device)
 
     // per-kernel-class event timing (skg_set_timing)
     struct Pending {
@@ -149,6 +150,7 @@ struct skg_ctx {
     // timing is off; recaptured when dt, the fast-path decision or the
     // stream change.
     cudaGraphExec_t gexec = nullptr;
+    double* g_diag = nullptr;
     double g_dt = 0.0;
     bool g_pruned = false;
     cudaStream_t g_stream = nullptr;
@@ -273,6 +275,8 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     a.twx = c->tw[0];
     a.twy = c->tw[1];
     a.flags = c->flags;
+    a.diag = c->diag;
+    a.nu = c->nu;
     // one partition covering everything: send and receive buffers alias
     a.G = 1;
     a.r = 0;
@@ -349,6 +353,8 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.twy = c->tw[1];
     a.twz = c->tw[2];
     a.flags = c->flags;
+    a.diag = c->diag;
+    a.nu = c->nu;
     return a;
 }
 
@@ -486,15 +492,23 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     }
     auto one_step = [&](long* counter) -> cudaError_t {
         cudaError_t e = cudaSuccess;
+        bool fused = false;
         if (c->solver == 2) {
             skg::Ns2dArgs a = args2d(c, dt);
+            fused = skg::ns2d_fast_ok(a);
+            if (!fused) a.diag = nullptr;
             for (int st = 1; st <= nst && e == cudaSuccess; ++st)
                 e = skg::ns2d_launch_stage(a, st, c->stream, counter, hook);
         } else {
             skg::Ns3dArgs a = args3d(c, dt);
+            fused = c->pruned;
+            if (!fused) a.diag = nullptr;
             for (int st = 1; st <= nst && e == cudaSuccess; ++st)
                 e = skg::ns3d_launch_stage(a, st, c->stream, counter, hook);
         }
+        if (e == cudaSuccess && c->diag && !fused)  // unfused paths: one reduction per step
+            e = skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
+                                   c->diag, c->stream, counter, c->nu, &c->flags->steps, false);
         return e;
     };
     long s = 0;
@@ -505,7 +519,8 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
         s = 1;
     }
     if (nsteps - s >= 2 && !c->timing && c->stream != nullptr) {
-        if (c->gexec && (c->g_dt != dt || c->g_pruned != c->pruned || c->g_stream != c->stream)) {
+        if (c->gexec && (c->g_dt != dt || c->g_pruned != c->pruned || c->g_stream != c->stream ||
+                         c->g_diag != c->diag)) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
         }
@@ -520,6 +535,7 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
             cudaGraphDestroy(graph);
             c->g_dt = dt;
+            c->g_diag = c->diag;
             c->g_pruned = c->pruned;
             c->g_stream = c->stream;
         }
@@ -770,7 +786,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     ok = ok && alloc((void**)&c->etab, sizeof(double) * 2 * ext_total);
     ok = ok && alloc((void**)&c->flags, sizeof(skg::DevFlags));
     ok = ok && alloc((void**)&c->d_count, sizeof(unsigned long long));
-    ok = ok && alloc((void**)&c->d_red, 2 * sizeof(double));
+    ok = ok && alloc((void**)&c->d_red, 3 * sizeof(double));
     if (!ok) return cleanup(SKG_ECUDA, "device allocation failed (grid too large for this GPU?)");
     for (int d = 0; d < dims; ++d) {
         c->tw[d] = twiddle_table(device, n[d]);
@@ -892,6 +908,32 @@ int skg_step(skg_ctx* c, double dt, long nsteps) {
     int rc = enqueue_steps(c, dt, nsteps);
     if (rc) return rc;
     return sync_and_check(c, nsteps, dt);
+}
+
+int skg_run(skg_ctx* c, double dt, long nsteps, double* series) {
+    if (!series) return skg_step(c, dt, nsteps);
+    if (c->comm) return fail(SKG_EUNSUPPORTED, "skg_run series on a multi-process context");
+    if (nsteps <= 0) return skg_step(c, dt, nsteps);
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    double* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, sizeof(double) * 3 * nsteps));
+    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(double) * 3 * nsteps, c->stream));
+    c->diag = d;
+    int rc = enqueue_steps(c, dt, nsteps);
+    c->diag = nullptr;
+    if (rc == SKG_OK) rc = sync_and_check(c, nsteps, dt);
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(series, d, sizeof(double) * 3 * nsteps, cudaMemcpyDeviceToHost);
+    if (c->gexec && c->g_diag == d) {  // the graph baked this buffer in
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    cudaFree(d);
+    return rc;
 }
 
 int skg_tendency(skg_ctx* c, const double* in, double* out) {
@@ -1068,7 +1110,7 @@ int skg_energy(skg_ctx* c, double* energy, double* enstrophy) {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
                                 c->d_red, c->stream, &c->launches));
-    double h[2];
+    double h[3];
     CUDA_TRY(cudaMemcpyAsync(h, c->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (energy) *energy = h[0];

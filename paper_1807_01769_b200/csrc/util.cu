@@ -91,14 +91,16 @@ struct EnGeo {
     MaskGeo m;
     double ks[3];
     int solver2d;  // 1: ns2d on the CM layout ([ky][kx]); 0: reference layout
+    double nu;
 };
 
 // E and Z (Simulation::energy / enstrophy, simulation.cpp:592-615 with the
 // ns2d mode_energy / mode_enstrophy of solvers.cpp:211-230 and the default
 // Solver::mode_energy of simulation.cpp:163-170).
 __global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long long S,
-                              double* out) {
-    double e = 0.0, z = 0.0;
+                              double* out, const int* steps) {
+    if (steps) out += 3 * (*steps - 1);  // per-step series slot
+    double e = 0.0, z = 0.0, d = 0.0;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < S;
          q += (long long)gridDim.x * blockDim.x) {
         int ix[3];
@@ -120,21 +122,18 @@ __global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long
             cd x = f[v * S + q];
             const double nrm = x.x * x.x + x.y * x.y;
             if (g.solver2d) {
-                if (ksq > 0.0) e += 0.5 * w * nrm / ksq;
+                if (ksq > 0.0) {
+                    e += 0.5 * w * nrm / ksq;
+                    d += 2.0 * g.nu * ksq * (0.5 * w * nrm / ksq);
+                }
                 z += 0.5 * w * nrm;
             } else {
                 e += 0.5 * w * nrm;
+                d += 2.0 * g.nu * ksq * (0.5 * w * nrm);
             }
         }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        e += __shfl_down_sync(0xffffffffu, e, o);
-        z += __shfl_down_sync(0xffffffffu, z, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&out[0], e);
-        atomicAdd(&out[1], z);
-    }
+    diag_accumulate(out, e, z, d);
 }
 
 MaskGeo make_geo(int dims, const int* n, const int* kc) {
@@ -178,16 +177,18 @@ cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double
 }
 
 cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* kscale, int nvars,
-                          int solver2d, double* d_out, cudaStream_t s, long* launches) {
+                          int solver2d, double* d_out, cudaStream_t s, long* launches, double nu,
+                          const int* steps, bool zero_first) {
     int kc[3] = {0, 0, 0};
     EnGeo g{};
     g.m = make_geo(dims, n, kc);
     for (int d = 0; d < dims; ++d) g.ks[d] = kscale[d];
     g.solver2d = solver2d;
+    g.nu = nu;
     long long S = 1;
     for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.m.nh : n[d]);
-    cudaMemsetAsync(d_out, 0, 2 * sizeof(double), s);
-    energy_kernel<<<592, 256, 0, s>>>(f, g, nvars, S, d_out);
+    if (zero_first) cudaMemsetAsync(d_out, 0, 3 * sizeof(double), s);
+    energy_kernel<<<592, 256, 0, s>>>(f, g, nvars, S, d_out, steps);
     ++*launches;
     return cudaGetLastError();
 }

@@ -55,3 +55,14 @@ def test_slab_config_errors():
         api.Simulation("ns2d", (64, 64), 1e-3, 1e-3, world=64)   # 64 % (2*64) != 0
     with pytest.raises(api.UnsupportedError):
         api.Simulation("ns3d", (16, 16, 16), 1e-3, 1e-3, world=2)
+
+
+def test_slab_run_series():
+    n = (256, 256)
+    u0 = ic.ns2d_ic(n, seed=4)
+    one = api.Simulation("ns2d", n, 1e-3, 1e-3)
+    one.set_state(u0)
+    d = api.Simulation("ns2d", n, 1e-3, 1e-3, world=4)
+    d.set_state(u0)
+    a, b = d.run(5), one.run(5)
+    assert np.allclose(a, b, rtol=1e-12, atol=0)

@@ -192,3 +192,30 @@ def test_state_shape_error():
     g = api.Simulation("ns2d", (32, 32), 1e-3, 1e-3)
     with pytest.raises(api.ShapeError):
         g.set_state(np.zeros((1, 32, 16), complex))
+
+
+@pytest.mark.parametrize("n,noise", [((256, 256), False), ((64, 64), True)])
+def test_run_series_matches_reference(ref_lib, n, noise):
+    """Simulation::run's per-step means (output.cpp:204-214): E, Z, eps after
+    every step, fused on the dealiased path, a device reduction otherwise."""
+    if noise:
+        rng = np.random.default_rng(3)
+        u0 = O.forward(rng.standard_normal(n))[None]
+    else:
+        u0 = ic.ns2d_ic(n, seed=8)
+    nu, dt, steps = 1e-3, 1e-3, 6
+    r = ref_lib.RefSimulation("ns2d", n, nu, dt)
+    r.set_state(u0)
+    g = api.Simulation("ns2d", n, nu, dt)
+    g.set_state(u0)
+    series = g.run(steps)
+    ksq = O.k_sq(n)
+    w = O.parseval_w(n)
+    for i in range(steps):
+        r.step(1)
+        s = r.get_state()[0]
+        eps = float((np.where(ksq > 0, nu * w * np.abs(s) ** 2, 0.0)).sum())
+        assert abs(series[i, 0] - r.energy) < 1e-12 * r.energy
+        assert abs(series[i, 1] - r.enstrophy) < 1e-11 * r.enstrophy
+        assert abs(series[i, 2] - eps) < 1e-11 * eps
+    assert O.rel_l2(g.get_state(), r.get_state()) < PARITY

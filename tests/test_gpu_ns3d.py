@@ -159,3 +159,28 @@ def test_divergence_error_field_name():
         g.step(4)
     assert ei.value.iteration == 1
     assert ei.value.field in ("vx_fft", "vy_fft", "vz_fft")
+
+
+@pytest.mark.parametrize("noise", [False, True])
+def test_run_series_matches_reference(ref_lib, noise):
+    n = (32, 32, 32)
+    if noise:
+        rng = np.random.default_rng(3)
+        u0 = np.stack([O.forward(rng.standard_normal(n)) for _ in range(3)])
+    else:
+        u0 = ic.ns3d_ic(n, seed=8)
+    nu, dt, steps = 1e-2, 2e-3, 4
+    r = ref_lib.RefSimulation("ns3d", n, nu, dt)
+    r.set_state(u0)
+    g = api.Simulation("ns3d", n, nu, dt)
+    g.set_state(u0)
+    series = g.run(steps)
+    ksq = O.k_sq(n)
+    w = O.parseval_w(n)
+    for i in range(steps):
+        r.step(1)
+        s = r.get_state()
+        eps = float(sum((2 * nu * ksq * 0.5 * w * np.abs(s[c]) ** 2).sum() for c in range(3)))
+        assert abs(series[i, 0] - r.energy) < 1e-12 * r.energy
+        assert series[i, 1] == 0.0
+        assert abs(series[i, 2] - eps) < 1e-11 * eps
