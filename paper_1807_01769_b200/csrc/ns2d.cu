@@ -44,6 +44,10 @@ __device__ __forceinline__ size_t cpidx(int x, int ky, int nx) {
     return ((size_t)(ky >> 1) * nx + x) * 2 + (ky & 1);
 }
 
+// Rows interleaved per ky in the fast path's x-inverse outputs: the x-inverse
+// pass stores RG consecutive x of one column as one 16*RG-byte chunk.
+constexpr int RG = 4;
+
 __device__ __forceinline__ cd* pick(const Ns2dArgs& a, int m) {
     return m == 0 ? a.I[0] : m == 1 ? a.I[1] : m == 2 ? a.I[2] : a.I[3];
 }
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage
                 for (int e = 0; e < E; ++e) {
                     const int x = t + T * e;
                     const int q = x / a.nrl, xl = x - q * a.nrl;
-                    out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl >> 1) * a.ncols + kyl) * 2 + (xl & 1)] = v[e];
+                    out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG)] = v[e];
                 }
             } else {
                 cd* out = pick(a, m);
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
         for (int i = t; i < a.ky_in; i += T) {
             const int ro = a.kowner[i];
             const int cs = a.cstart[ro], nc = a.cstart[ro + 1] - cs;
-            const size_t q = (size_t)a.nrl * cs + ((size_t)(x >> 1) * nc + (i - cs)) * 2 + (x & 1);
+            const size_t q = (size_t)a.nrl * cs + ((size_t)(x / RG) * nc + (i - cs)) * RG + (x % RG);
             cp_async16(&st[i], P + q);
             cp_async16(&st[ld + i], Q + q);
         }

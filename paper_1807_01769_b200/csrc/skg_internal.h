@@ -65,7 +65,7 @@ struct Ns2dArgs {
     // this partition owns the kept ky columns [c0, c0 + ncols) (c0 even) of
     // the state and the x rows [r nrl, (r + 1) nrl) of physical space.
     //   sI/rI: x-inverse outputs X[psi], X[kx psi]; send block for rank q =
-    //          rows(q) x own columns, pair-interleaved ((xl/2) ncols + kyl) 2 + xl%2;
+    //          rows(q) x own columns, row-quad interleaved ((xl/4) ncols + kyl) 4 + xl%4;
     //          receive block from r' at nrl * cstart[r'] with r's layout.
     //   sA/rA: product spectra; send layout ((k/2) nrl + xl) 2 + k%2 (blocks in
     //          pair order), receive block from r' at r' * 2 npairs nrl.

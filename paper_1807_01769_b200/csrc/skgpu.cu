@@ -687,8 +687,8 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     if (world < 1 || rank < 0 || rank >= world) return fail(SKG_ECONFIG, "bad rank / world size");
     if (world > 1 && sid != 2)
         return fail(SKG_EUNSUPPORTED, "slab decomposition is implemented for ns2d only");
-    if (world > 1 && n[0] % (2 * world))
-        return fail(SKG_ECONFIG, "nx must be divisible by 2 * world for the slab decomposition");
+    if (world > 1 && n[0] % (4 * world))
+        return fail(SKG_ECONFIG, "nx must be divisible by 4 * world for the slab decomposition");
 
     auto c = new skg_ctx();
     c->device = device;

@@ -52,10 +52,10 @@ def slab_tendency(w_full, n, rank, G):
     psi = np.where(ksq == 0, 0, W / np.where(ksq == 0, 1, ksq))
     X0 = np.fft.ifft(psi, axis=0) * nx                    # (x, kyl)
     X1 = np.fft.ifft(KX * psi, axis=0) * nx
-    # send block to q: rows(q) x own cols, ((xl/2) ncols + kyl) 2 + xl%2
+    # send block to q: rows(q) x own cols, ((xl/4) ncols + kyl) 4 + xl%4
     def pack_I(X, q):
         blk = X[q * nrl:(q + 1) * nrl, :]                 # (xl, kyl)
-        return blk.reshape(nrl // 2, 2, ncols).transpose(0, 2, 1).reshape(-1).copy()
+        return blk.reshape(nrl // 4, 4, ncols).transpose(0, 2, 1).reshape(-1).copy()
     rs = [nrl * (cstart[q + 1] - cstart[q]) for q in range(G)]
     R0 = _a2a([pack_I(X0, q) for q in range(G)], rs)
     R1 = _a2a([pack_I(X1, q) for q in range(G)], rs)
@@ -64,7 +64,7 @@ def slab_tendency(w_full, n, rank, G):
         cols = []
         for q in range(G):
             nc = cstart[q + 1] - cstart[q]
-            cols.append(R[q].reshape(nrl // 2, nc, 2).transpose(0, 2, 1).reshape(nrl, nc))
+            cols.append(R[q].reshape(nrl // 4, nc, 4).transpose(0, 2, 1).reshape(nrl, nc))
         return np.concatenate(cols, axis=1)               # (xl, Kc)
     P0, P1 = unpack_rows(R0), unpack_rows(R1)
     kyk = ky[:Kc][None, :]

@@ -38,7 +38,7 @@ def _worker(rank, world, port, n, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, (64, 64)), (4, (128, 64)), (2, (32, 128))])
+@pytest.mark.parametrize("world,n", [(2, (64, 64)), (4, (128, 64)), (2, (32, 128)), (4, (64, 64))])
 def test_slab_decomposition_gloo(world, n):
     mgr = mp.Manager()
     out = mgr.dict()
