@@ -23,6 +23,10 @@
 
 #include "skg_internal.h"
 
+#ifndef SKG_FAST_X_EM
+#define SKG_FAST_X_EM 16
+#endif
+
 namespace skg {
 
 namespace {
@@ -106,12 +110,24 @@ __device__ __forceinline__ cd stage_combine(const Ns2dArgs& a, int stage, int ky
 // PZ: the state is dealiased and the kept |kx| <= kcx < 6T, so the elements
 // e in [6, 10) of every thread (kx in [6T, 10T)) are exactly zero: they are
 // neither loaded nor stored, and the stage-state slots shrink from 16 to 12.
-template <int NX, bool PZ, int NM>
-__global__ void __launch_bounds__(256, PZ ? 2 : 1) k1_xinv(Ns2dArgs a, int stage) {
-    using F = BFFT<NX>;
+// EM = 8 elements per thread: twice the threads per line, a quarter fewer
+// registers, one more shared-memory exchange; the zero band is then e in [3, 5).
+template <int N, int EM>
+struct XCfg {
+    using F = BFFT<N, false, EM>;
+    static constexpr int T = F::T;
+    static constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    static constexpr int CT = T * LPC;
+    static constexpr int ZLO = EM == 16 ? 6 : 3, ZHI = EM == 16 ? 10 : 5;
+};
+
+template <int NX, bool PZ, int NM, int EM = 16>
+__global__ void __launch_bounds__(XCfg<NX, EM>::CT, (PZ || EM == 8) ? 2 : 1)
+    k1_xinv(Ns2dArgs a, int stage) {
+    using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
-    constexpr int LPC = T >= 256 ? 1 : 256 / T;
-    constexpr int ZLO = PZ ? 6 : E, ZHI = PZ ? 10 : E;
+    constexpr int LPC = XCfg<NX, EM>::LPC;
+    constexpr int ZLO = PZ ? XCfg<NX, EM>::ZLO : E, ZHI = PZ ? XCfg<NX, EM>::ZHI : E;
     constexpr int NS = E - (ZHI - ZLO);  // stage-state slots per thread
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
@@ -502,12 +518,12 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
 
 // x-forward of the two product spectra per kept ky column, combination
 // kx ky A + (kx^2 - ky^2) B, dealias + mean 0 + RK epilogue (as k4_xfwd).
-template <int NX>
-__global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
-    using F = BFFT<NX>;
+template <int NX, int EM = 16>
+__global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int stage) {
+    using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
-    constexpr int LPC = T >= 256 ? 1 : 256 / T;
-    constexpr int ZLO = 6, ZHI = 10, NS = E - (ZHI - ZLO);
+    constexpr int LPC = XCfg<NX, EM>::LPC;
+    constexpr int ZLO = XCfg<NX, EM>::ZLO, ZHI = XCfg<NX, EM>::ZHI, NS = E - (ZHI - ZLO);
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
     const int kyl = blockIdx.x * LPC + l;  // local column
@@ -607,21 +623,22 @@ __global__ void __launch_bounds__(256, 2) k4b_xfwd(Ns2dArgs a, int stage) {
     }
 }
 
-template <int NX, bool PZ, int NM>
+template <int NX, bool PZ, int NM, int EM = 16>
 cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
-    using F = BFFT<NX>;
+    using C = XCfg<NX, EM>;
+    using F = typename C::F;
     constexpr int T = F::T, E = F::E;
-    constexpr int LPC = T >= 256 ? 1 : 256 / T;
-    constexpr int NS = PZ ? E - 4 : E;
+    constexpr int LPC = C::LPC;
+    constexpr int NS = PZ ? E - (C::ZHI - C::ZLO) : E;
     const size_t smem = sizeof(cd) * (F::SMEM + NS * T) * LPC;
     const int grid = ((NM == 2 ? a.ncols : a.ky_in) + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k1_xinv<NX, PZ, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k1_xinv<NX, PZ, NM, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    k1_xinv<NX, PZ, NM><<<grid, T * LPC, smem, s>>>(a, stage);
+    k1_xinv<NX, PZ, NM, EM><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
 
@@ -685,21 +702,27 @@ cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// elements per thread of the fast path's x passes
+template <int NX>
+constexpr int fast_em() { return NX >= 4096 ? SKG_FAST_X_EM : 16; }
+
 template <int NX>
 cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
-    if (inverse) return launch_k1<NX, true, 2>(a, stage, s);
-    using F = BFFT<NX>;
+    constexpr int EM = fast_em<NX>();
+    if (inverse) return launch_k1<NX, true, 2, EM>(a, stage, s);
+    using C = XCfg<NX, EM>;
+    using F = typename C::F;
     constexpr int T = F::T;
-    constexpr int LPC = T >= 256 ? 1 : 256 / T;
-    const size_t smem = sizeof(cd) * (F::SMEM + (F::E - 4) * T) * LPC;
+    constexpr int LPC = C::LPC;
+    const size_t smem = sizeof(cd) * (F::SMEM + (F::E - (C::ZHI - C::ZLO)) * T) * LPC;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k4b_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k4b_xfwd<NX, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    k4b_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
+    k4b_xfwd<NX, EM><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
 
