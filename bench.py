@@ -209,9 +209,9 @@ def run_our_arm(args):
     solver, n, nu, dt, u0 = make_input(args.config)
     P = int(np.prod(n))
     S = u0.size  # complex modes over all variables
-    slab = ws > 1 and solver == "ns2d"
+    slab = ws > 1
     if slab:
-        # ns2d slab decomposition over the ranks (strong scaling of
+        # slab decomposition over the ranks (strong scaling of
         # one grid), transposes as NCCL all-to-all inside libskgpu
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -339,9 +339,7 @@ def run_our_arm(args):
                 "workload": f"{args.config}: {solver} {'x'.join(map(str, n))} RK4 step, "
                             f"nu={nu}, dt={dt:.6g} (CFL 0.5)",
                 "solver": solver, "n": list(n), "global_batch": 1 if slab else ws,
-                "parallelism": (f"slab{ws} (NCCL all-to-all)" if slab else
-                                "replicas (ns3d slab decomposition not built)" if ws > 1 else
-                                "single-gpu"),
+                "parallelism": f"slab{ws} (NCCL all-to-all)" if slab else "single-gpu",
                 "l2": "every field array > 126 MB L2; no flush needed",
                 "dealiased_fast_path": pruned,
             },

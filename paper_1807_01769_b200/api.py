@@ -195,7 +195,7 @@ class Simulation:
     def __init__(self, solver: str, n, nu: float = 0.0, dt: float = 0.0, scheme: str = "RK4",
                  L=None, dealias_coef: float = 2.0 / 3.0, device: int = 0, world: int = 1,
                  rank: int = 0, nccl_id: bytes | None = None):
-        """world > 1: slab decomposition (ns2d).  With nccl_id (from
+        """world > 1: slab decomposition (ns2d and ns3d).  With nccl_id (from
         nccl_unique_id() on rank 0) this process runs partition `rank` over
         NCCL; without it all `world` partitions run here on one device."""
         L_ = load_library()

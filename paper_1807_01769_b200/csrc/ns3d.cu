@@ -56,8 +56,14 @@ __device__ __forceinline__ int ky_of(const Ns3dArgs& a, int kyi) {
     return kyi <= a.kcy ? kyi : a.ny - (2 * a.kcy + 1) + kyi;
 }
 
-__device__ __forceinline__ size_t sidx(const Ns3dArgs& a, int kx, int ky, int kz) {
-    return ((size_t)kx * a.ny + ky) * a.nh + kz;
+// state index of mode (kx, line ys of the state layout, kz)
+__device__ __forceinline__ size_t sidx(const Ns3dArgs& a, int kx, int ys, int kz) {
+    return ((size_t)kx * a.ystate + ys) * a.nh + kz;
+}
+
+// compact kept index of a kept ky (0..kcy, then ny-kcy..ny-1)
+__device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
+    return ky <= a.kcy ? ky : ky - (a.ny - (2 * a.kcy + 1));
 }
 
 // RK stage state of variable c at mode (i, ky, kz)  (time_stepping.cpp:128-170)
@@ -100,12 +106,13 @@ __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_in + C - 1) / C;
-    const int kyi = blockIdx.x / nkzb;
+    const int kyi = a.kys + blockIdx.x / nkzb;
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_in;
     if (a.flags->diverged) return;
-    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.flags->steps, 1);
+    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     const int ky = ky_of(a, kyi);
+    const int ys = a.G == 1 ? ky : kyi - a.kys;
     cd* sm = smem + l * F::SMEM;
     cd* slots = smem + C * F::SMEM;  // slots[slot * CT + tid]
     cd* kst = smem;                  // k staging in the idle exchange buffers
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
             const int i = t + T * e;
             const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
             if (keep) {
-                const size_t idx = sidx(a, i, ky, kz) + c * a.vstride;
+                const size_t idx = sidx(a, i, ys, kz) + c * a.vstride;
                 cp_async16(&slots[slot * CT + threadIdx.x], a.u + idx);
                 if (stage > 1) cp_async16(&kst[slot * CT + threadIdx.x], kprev + idx);
             }
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
                 cd* out = a.A + m * a.fstride;
 #pragma unroll
                 for (int e = 0; e < E; ++e)
-                    out[((size_t)(t + T * e) * a.ny + ky) * a.kz_in + kz] = v[e];
+                    out[((size_t)(t + T * e) * a.ystate + ys) * a.kz_in + kz] = v[e];
             }
         }
     }
@@ -182,11 +189,13 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
     const double kzv = a.kz_scale * (double)kz;
-    const cd* A0 = a.A;
-    const cd* A1 = a.A + a.fstride;
-    const cd* A2 = a.A + 2 * a.fstride;
-    const cd* A3 = a.A + 3 * a.fstride;
-    const cd* A4 = a.A + 4 * a.fstride;
+    const cd* Ab = a.G == 1 ? a.A : a.rA;
+    const size_t afs = a.G == 1 ? a.fstride : a.rfs;
+    const cd* A0 = Ab;
+    const cd* A1 = Ab + afs;
+    const cd* A2 = Ab + 2 * afs;
+    const cd* A3 = Ab + 3 * afs;
+    const cd* A4 = Ab + 4 * afs;
 #pragma unroll 1
     for (int m = 0; m < 6; ++m) {
         cd v[E];
@@ -197,7 +206,15 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
             const bool keep = active && (!a.pruned || abs(sj) <= a.kcy);
             cd r = zero();
             if (keep) {
-                const size_t q = ((size_t)x * a.ny + j) * a.kz_in + kz;
+                size_t q;
+                if (a.G == 1) {
+                    q = ((size_t)x * a.ny + j) * a.kz_in + kz;
+                } else {  // receive block of the line's owner, layout [xl][kyl][kz]
+                    const int kyi = ky_compact(a, j);
+                    const int ro = a.kowner[kyi];
+                    const int ks = a.kstart[ro], nk = a.kstart[ro + 1] - ks;
+                    q = (size_t)a.nrl * ks * a.kz_in + ((size_t)x * nk + (kyi - ks)) * a.kz_in + kz;
+                }
                 const double kyv = a.ky_scale * (double)sj;
                 switch (m) {
                     case 0: r = A0[q]; break;  // vx
@@ -270,7 +287,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     extern __shared__ cd smem[];
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const long long r0 = 2ll * ((long long)blockIdx.x * G + g);
-    const bool active = r0 < (long long)a.nx * a.ny;
+    const bool active = r0 < (long long)a.nrl * a.ny;
     if (a.flags->diverged) return;
     cd* sm = smem + g * Z3<NZ>::SLOT;
     double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
@@ -372,12 +389,20 @@ __global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
             v[e] = active ? in[((size_t)x * a.ny + (t + T * e)) * a.kz_o + kz] : zero();
         F::template run<-1>(v, sm, t, wb, salt);
         if (active) {
-            cd* out = a.B + m * a.fstride;   // D fields live in B's memory
+            cd* out = a.G == 1 ? a.B + m * a.fstride   // D fields live in B's memory
+                               : a.sD + m * a.rfs;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int j = t + T * e;
                 if (abs(signed_index(j, NY)) > a.kcy) continue;  // masked: never read
-                out[((size_t)x * a.ny + j) * a.kz_o + kz] = v[e];
+                if (a.G == 1) {
+                    out[((size_t)x * a.ny + j) * a.kz_o + kz] = v[e];
+                } else {  // send block of the line's owner q, layout [xl][kyl_q][kz]
+                    const int kyi = ky_compact(a, j);
+                    const int q = a.kowner[kyi];
+                    const int ks = a.kstart[q], nk = a.kstart[q + 1] - ks;
+                    out[(size_t)a.nrl * ks * a.kz_o + ((size_t)x * nk + (kyi - ks)) * a.kz_o + kz] = v[e];
+                }
             }
         }
     }
@@ -394,19 +419,20 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_o + C - 1) / C;
-    const int kyi = blockIdx.x / nkzb;
+    const int kyi = a.kys + blockIdx.x / nkzb;
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_o;
     if (a.flags->diverged) return;
     const int ky = ky_of(a, kyi);
+    const int ys = a.G == 1 ? ky : kyi - a.kys;
     const int sky = signed_index(ky, a.ny);
     const bool keep_y = abs(sky) <= a.kcy;
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twx);
     const bool io = active && keep_y;
-    const size_t lbase = (size_t)ky * a.kz_o + kz;     // + x * ny * kz_o
-    const size_t xstr = (size_t)a.ny * a.kz_o;
+    const size_t lbase = (size_t)ys * a.kz_o + kz;     // + x * ystate * kz_o
+    const size_t xstr = (size_t)a.ystate * a.kz_o;
     cd v[E];
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
@@ -432,7 +458,7 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
     const double pw = (kz == 0 || kz == a.nh - 1) ? 1.0 : 2.0;
     if (final && a.diag && active && ky == 0 && kz == 0 && t == 0) {
         for (int c = 0; c < 3; ++c) {  // mean flow: untouched, energy only
-            const cd u0 = a.u[c * a.vstride];
+            const cd u0 = a.u[sidx(a, 0, ys, 0) + c * a.vstride];
             sE += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
         }
     }
@@ -461,7 +487,7 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
             }
         }
         const cd kc[3] = {c0, c1, c2};
-        const size_t base = sidx(a, i, ky, kz);
+        const size_t base = sidx(a, i, ys, kz);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const size_t idx = base + c * a.vstride;
@@ -555,7 +581,7 @@ cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s
     constexpr int C = Strided<NX>::C;
     using F = BFFT<NX>;
     if (inverse) {
-        const int grid = a.ky_lines * ((a.kz_in + C - 1) / C);
+        const int grid = a.nkyl * ((a.kz_in + C - 1) / C);
         const bool pz = NX >= 64 && a.pruned && a.kcx <= 6 * F::T - 1;
         if (pz) {
             if constexpr (NX >= 64) {
@@ -574,7 +600,7 @@ cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s
         const size_t smem = sizeof(cd) * F::SMEM * C;
         static size_t done = 0;
         set_smem(k4_3d<NX>, smem, done);
-        const int grid = a.ky_lines * ((a.kz_o + C - 1) / C);
+        const int grid = a.nkyl * ((a.kz_o + C - 1) / C);
         k4_3d<NX><<<grid, F::T * C, smem, s>>>(a, stage);
     }
     return cudaGetLastError();
@@ -588,12 +614,12 @@ cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     if (inverse) {
         static size_t done = 0;
         set_smem(k2_3d<NY>, smem, done);
-        const int grid = a.nx * ((a.kz_in + C - 1) / C);
+        const int grid = a.nrl * ((a.kz_in + C - 1) / C);
         k2_3d<NY><<<grid, F::T * C, smem, s>>>(a);
     } else {
         static size_t done = 0;
         set_smem(k2f_3d<NY>, smem, done);
-        const int grid = a.nx * ((a.kz_o + C - 1) / C);
+        const int grid = a.nrl * ((a.kz_o + C - 1) / C);
         k2f_3d<NY><<<grid, F::T * C, smem, s>>>(a);
     }
     return cudaGetLastError();
@@ -605,7 +631,7 @@ cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
     const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
     static size_t done = 0;
     set_smem(k3_3d<NZ>, smem, done);
-    const long long pairs = (long long)a.nx * a.ny / 2;
+    const long long pairs = (long long)a.nrl * a.ny / 2;
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
     k3_3d<NZ><<<grid, Z::T * Z::G, smem, s>>>(a);
     return cudaGetLastError();
@@ -650,41 +676,57 @@ bool ns3d_supported(int nx, int ny, int nz) {
     return ok(nx) && ok(ny) && ok(nz);
 }
 
-cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
-                              const LaunchHook& hook) {
+cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
+                      const LaunchHook& hook) {
+    // Bytes models use this rank's share: nkyl kept lines (x passes) and
+    // nrl x rows (y/z passes); G = 1 gives the whole grid.
     cudaError_t err;
     const double B = sizeof(cd);
     const bool final = a.rk2 ? stage == 2 : stage == 4;
     const double kyk = a.pruned ? 2.0 * a.kcy + 1 : (double)a.ny;  // ky read by k2
     const double kxk = a.pruned ? 2.0 * a.kcx + 1 : (double)a.nx;
-    const double lines_in = (double)a.ky_lines * a.kz_in;
-    const double lines_o = (double)a.ky_lines * a.kz_o;
-    const double plane_in = (double)a.nx * a.ny * a.kz_in;
-    const double plane_o = (double)a.nx * a.ny * a.kz_o;
-    hook.begin(0);
-    if ((err = dispatch_x3(a, stage, true, s)) != cudaSuccess) return err;
-    hook.end(0, B * (3.0 * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + 5.0 * a.nx * lines_in));
-    hook.begin(3);
-    if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
-    hook.end(3, B * (5.0 * a.nx * kyk * a.kz_in + 6.0 * plane_in));
-    hook.begin(1);
-    if ((err = dispatch_z3(a, s)) != cudaSuccess) return err;
-    hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
-    hook.begin(3);
-    if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;
-    hook.end(3, B * (3.0 * plane_o + 3.0 * a.nx * kyk * a.kz_o));
-    hook.begin(2);
-    if ((err = dispatch_x3(a, stage, false, s)) != cudaSuccess) return err;
-    hook.end(2, B * (3.0 * a.nx * lines_o +
-                     3.0 * kxk * lines_o * (final ? (a.rk2 ? 3.0 : 5.0) : 1.0)));
-    *launches += 5;
-    if (final && !a.pruned && a.nh > a.kz_o) {
-        hook.begin(3);
-        k4_3d_decay<<<592, 256, 0, s>>>(a);
-        hook.end(3, B * 6.0 * a.nx * a.ny * (a.nh - a.kz_o));
+    const double lines_in = (double)a.nkyl * a.kz_in;
+    const double lines_o = (double)a.nkyl * a.kz_o;
+    const double plane_in = (double)a.nrl * a.ny * a.kz_in;
+    const double plane_o = (double)a.nrl * a.ny * a.kz_o;
+    if (pass == 0) {
+        hook.begin(0);
+        if ((err = dispatch_x3(a, stage, true, s)) != cudaSuccess) return err;
+        hook.end(0, B * (3.0 * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + 5.0 * a.nx * lines_in));
         *launches += 1;
-        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    } else if (pass == 1) {
+        hook.begin(3);
+        if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
+        hook.end(3, B * (5.0 * a.nrl * kyk * a.kz_in + 6.0 * plane_in));
+        hook.begin(1);
+        if ((err = dispatch_z3(a, s)) != cudaSuccess) return err;
+        hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
+        hook.begin(3);
+        if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;
+        hook.end(3, B * (3.0 * plane_o + 3.0 * a.nrl * kyk * a.kz_o));
+        *launches += 3;
+    } else {
+        hook.begin(2);
+        if ((err = dispatch_x3(a, stage, false, s)) != cudaSuccess) return err;
+        hook.end(2, B * (3.0 * a.nx * lines_o +
+                         3.0 * kxk * lines_o * (final ? (a.rk2 ? 3.0 : 5.0) : 1.0)));
+        *launches += 1;
+        if (final && !a.pruned && a.nh > a.kz_o) {
+            hook.begin(3);
+            k4_3d_decay<<<592, 256, 0, s>>>(a);
+            hook.end(3, B * 6.0 * a.nx * a.ny * (a.nh - a.kz_o));
+            *launches += 1;
+            if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        }
     }
+    return cudaSuccess;
+}
+
+cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
+                              const LaunchHook& hook) {
+    cudaError_t err;
+    for (int pass = 0; pass < 3; ++pass)
+        if ((err = ns3d_pass(a, pass, stage, s, launches, hook)) != cudaSuccess) return err;
     return cudaSuccess;
 }
 

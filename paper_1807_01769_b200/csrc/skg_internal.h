@@ -136,6 +136,21 @@ struct Ns3dArgs {
     DevFlags* flags;
     double* diag;           // per-step (E, Z, eps) series, slot steps-1; nullptr = off
     double nu;
+    // Slab decomposition (G = 1 on one GPU): this rank owns the kept ky
+    // lines [kys, kys + nkyl) (compact kept index kyi: 0..kcy, then the
+    // negative ky) of the state and the x rows [r nrl, (r + 1) nrl) of the
+    // y/z passes.  The state and the x-pass intermediates are indexed
+    // ((x * ystate + ys) * kz + ...) with ystate = ny, ys = ky when G = 1 and
+    // ystate = nkyl, ys = kyi - kys otherwise (send/receive blocks of the
+    // two all-to-alls are then contiguous x ranges).  y-pass reads of A and
+    // writes of D go through the owner table of each kept line.
+    int G, r, lead, kys, nkyl, nrl;
+    int ystate;
+    const int* kowner;      // owner rank of each compact kept ky line (2 kcy + 1)
+    const int* kstart;      // first compact line of each rank (G + 1)
+    cd* rA;                 // received x-inverse outputs (5 fields, stride rfs), G > 1
+    cd* sD;                 // y-forward outputs to send (3 fields, stride rfs), G > 1
+    size_t rfs;
 };
 
 // Warp-sum three doubles and add them to slot[0..2] (all 32 lanes must call).
@@ -153,6 +168,9 @@ __device__ __forceinline__ void diag_accumulate(double* slot, double e, double z
 }
 cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
                               const LaunchHook& hook);
+// Slab pieces: pass 0 x-inverse, 1 y-inverse + z + y-forward, 2 x-forward + RK.
+cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
+                      const LaunchHook& hook);
 bool ns3d_supported(int nx, int ny, int nz);
 
 // ---------------------------------------------------------------- utilities (util.cu)

@@ -6,6 +6,7 @@
 // small per-axis tables (twiddles, exp factors, dealias cut indices) and
 // enqueues kernels; every per-mode operation runs in sm_100a kernels.  There is
 // no CPU fallback: a missing device or an unsupported extent is an error.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -66,8 +67,12 @@ int cut_index(int n, double L, double coef, bool half) {
 
 }  // namespace
 
-// One slab of the decomposed ns2d state (see Ns2dArgs): owned kept ky
-// columns [c0, c0 + ncols) in CM layout and the exchange buffers.
+// One slab of the decomposed state.  ns2d (see Ns2dArgs): owned kept ky
+// columns [c0, c0 + ncols) in CM layout and the exchange buffers.  ns3d (see
+// Ns3dArgs): owned compact kept ky lines [c0, c0 + ncols) of the state
+// ([kx][kyl][kz], 3 components of vs elements), the x-pass/y-pass
+// intermediates A (5 fields) / B (6 fields) of fs elements each, and the
+// receive (rA) / send (sD) blocks of the two all-to-alls (rfs per field).
 struct Part {
     int r = 0;
     int c0 = 0, ncols = 0;
@@ -77,6 +82,11 @@ struct Part {
     cd* rI[2] = {nullptr, nullptr};
     cd* sA[2] = {nullptr, nullptr};
     cd* rA[2] = {nullptr, nullptr};
+    cd* A3 = nullptr;
+    cd* B3 = nullptr;
+    cd* rA3 = nullptr;
+    cd* sD3 = nullptr;
+    size_t vs = 0, fs = 0, rfs = 0;
 };
 
 struct skg_ctx {
@@ -355,6 +365,38 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.flags = c->flags;
     a.diag = c->diag;
     a.nu = c->nu;
+    a.G = 1;
+    a.r = 0;
+    a.lead = 1;
+    a.kys = 0;
+    a.nkyl = a.ky_lines;
+    a.nrl = a.nx;
+    a.ystate = a.ny;
+    a.kowner = c->d_kowner;
+    a.kstart = c->d_cstart;
+    return a;
+}
+
+skg::Ns3dArgs args3d_part(skg_ctx* c, double dt, const Part& p) {
+    skg::Ns3dArgs a = args3d(c, dt);
+    a.u = p.u;
+    a.k1 = p.k[0];
+    a.k2 = p.k[1];
+    a.k3 = p.k[2];
+    a.vstride = p.vs;
+    a.fstride = p.fs;
+    a.A = p.A3;
+    a.B = p.B3;
+    a.rA = p.rA3;
+    a.sD = p.sD3;
+    a.rfs = p.rfs;
+    a.G = c->G;
+    a.r = p.r;
+    a.lead = p.r == 0 ? 1 : 0;
+    a.kys = p.c0;
+    a.nkyl = p.ncols;
+    a.nrl = c->nrl;
+    a.ystate = p.ncols;
     return a;
 }
 
@@ -384,7 +426,10 @@ int sync_and_check(skg_ctx* c, long nsteps, double dt) {
 // (rows(q) x cols(r) from r to q), 1: product spectra (cols(q) x rows(r)).
 // Single-process mode: device-to-device copies; otherwise NCCL send/recv
 // on the context stream (grouped, one block per peer).
+int exchange3(skg_ctx* c, int which);
+
 int exchange(skg_ctx* c, int which) {
+    if (c->solver == 3) return exchange3(c, which);
     const int G = c->G;
     const size_t nrl = (size_t)c->nrl;
     auto ncol = [&](int q) { return c->cstart[q + 1] - c->cstart[q]; };
@@ -453,12 +498,76 @@ int exchange(skg_ctx* c, int which) {
     return SKG_OK;
 }
 
+// ns3d all-to-alls.  which = 0: x-inverse outputs, 5 fields, block r -> q =
+// rows(q) x lines(r) ([xl][kyl_r][kz_in]); 1: y-forward outputs, 3 fields,
+// block r -> q = rows(r) x lines(q) ([xl][kyl_q][kz_o]).
+int exchange3(skg_ctx* c, int which) {
+    const int G = c->G;
+    const size_t nrl = (size_t)c->nrl;
+    const size_t kz = (size_t)c->kc[2] + 1;  // kz_in = kz_o (pruned)
+    auto nl = [&](int q) { return (size_t)(c->cstart[q + 1] - c->cstart[q]); };
+    const int nf = which == 0 ? 5 : 3;
+    // block from rank r (buffers src) to rank q (buffers dst), field f
+    auto src_ptr = [&](const Part& src, int q, int f) {
+        return which == 0 ? src.A3 + f * src.fs + (size_t)q * nrl * nl(src.r) * kz
+                          : src.sD3 + f * src.rfs + nrl * c->cstart[q] * kz;
+    };
+    auto dst_ptr = [&](const Part& dst, int r, int f) {
+        return which == 0 ? dst.rA3 + f * dst.rfs + nrl * c->cstart[r] * kz
+                          : dst.B3 + f * dst.fs + (size_t)r * nrl * nl(dst.r) * kz;
+    };
+    auto count = [&](int r, int q) { return nrl * kz * (which == 0 ? nl(r) : nl(q)); };
+    const skg::LaunchHook hook = hook_of(c);
+    hook.begin(4);
+    double bytes = 0.0;
+    if (c->comm == nullptr) {
+        for (const Part& src : c->parts)
+            for (const Part& dst : c->parts)
+                for (int f = 0; f < nf; ++f) {
+                    const size_t cnt = count(src.r, dst.r);
+                    if (!cnt) continue;
+                    CUDA_TRY(cudaMemcpyAsync(dst_ptr(dst, src.r, f), src_ptr(src, dst.r, f),
+                                             cnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    if (src.r != dst.r) bytes += cnt * sizeof(cd);
+                }
+    } else {
+        const Part& me = c->parts[0];
+        const int r = me.r;
+        ncclResult_t nr = ncclGroupStart();
+        for (int q = 0; q < G && nr == ncclSuccess; ++q) {
+            for (int f = 0; f < nf && nr == ncclSuccess; ++f) {
+                const size_t scnt = count(r, q), rcnt = count(q, r);
+                cd* sptr = src_ptr(me, q, f);
+                cd* rptr = dst_ptr(me, q, f);
+                if (q == r) {
+                    if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    continue;
+                }
+                if (scnt) nr = ncclSend(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
+                if (nr == ncclSuccess && rcnt) nr = ncclRecv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                bytes += scnt * sizeof(cd);
+            }
+        }
+        ncclResult_t ne = ncclGroupEnd();
+        if (nr != ncclSuccess || ne != ncclSuccess)
+            return fail(SKG_ENCCL, std::string("all-to-all: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+    }
+    hook.end(4, bytes);
+    ++c->launches;
+    return SKG_OK;
+}
+
 int enqueue_dist_step(skg_ctx* c, double dt, long* counter) {
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
     for (int st = 1; st <= nst; ++st) {
         for (int pass = 0; pass < 3; ++pass) {
             for (const Part& p : c->parts) {
+                if (c->solver == 3) {
+                    skg::Ns3dArgs a = args3d_part(c, dt, p);
+                    CUDA_TRY(skg::ns3d_pass(a, pass, st, c->stream, counter, hook));
+                    continue;
+                }
                 skg::Ns2dArgs a = args2d_part(c, dt, p);
                 a.lead = p.r == 0 ? 1 : 0;
                 CUDA_TRY(skg::ns2d_fast_pass(a, pass, st, c->stream, counter, hook));
@@ -559,6 +668,31 @@ int decide_pruned(skg_ctx* c, const cd* d_ref_layout) {
     return SKG_OK;
 }
 
+// ns3d slab <-> reference layout: the compact lines [c0, c0 + ncols) of a
+// part are at most two runs of global ky (positive, then negative ky).
+int copy_slab3(skg_ctx* c, const Part& p, bool to_part) {
+    const int kcy = c->kc[1], ny = c->n[1], nx = c->n[0];
+    const size_t nh = (size_t)c->nh, row = nh * sizeof(cd);
+    const int runs[2][2] = {{0, kcy + 1}, {kcy + 1, 2 * kcy + 1}};  // compact ranges
+    for (int b = 0; b < 2; ++b) {
+        const int lo = std::max(runs[b][0], p.c0), hi = std::min(runs[b][1], p.c0 + p.ncols);
+        if (lo >= hi) continue;
+        const int gy = b == 0 ? lo : lo + ny - (2 * kcy + 1);
+        for (int v = 0; v < 3; ++v) {
+            cd* io = c->io + (size_t)v * c->S + (size_t)gy * nh;
+            cd* st = p.u + (size_t)v * p.vs + (size_t)(lo - p.c0) * nh;
+            const size_t io_pitch = (size_t)ny * row, st_pitch = (size_t)p.ncols * row;
+            if (to_part)
+                CUDA_TRY(cudaMemcpy2DAsync(st, st_pitch, io, io_pitch, (hi - lo) * row, nx,
+                                           cudaMemcpyDeviceToDevice, c->stream));
+            else
+                CUDA_TRY(cudaMemcpy2DAsync(io, io_pitch, st, st_pitch, (hi - lo) * row, nx,
+                                           cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+    return SKG_OK;
+}
+
 // reference layout (io) -> internal state
 int load_state_from_io(skg_ctx* c) {
     int rc = decide_pruned(c, c->io);
@@ -567,6 +701,13 @@ int load_state_from_io(skg_ctx* c) {
         if (!c->pruned)
             return fail(SKG_EUNSUPPORTED,
                         "slab-decomposed contexts need a dealiased state (masked modes exactly 0)");
+        if (c->solver == 3) {
+            for (const Part& p : c->parts) {
+                int rc2 = copy_slab3(c, p, true);
+                if (rc2) return rc2;
+            }
+            return SKG_OK;
+        }
         CUDA_TRY(skg::launch_transpose_c(c->io, c->cmfull, c->n[0], c->nh, 0, c->stream, &c->launches));
         for (const Part& p : c->parts)
             if (p.ncols)
@@ -584,6 +725,19 @@ int load_state_from_io(skg_ctx* c) {
 }
 
 int store_state_to_io(skg_ctx* c, const cd* src) {
+    if (c->dist && c->solver == 3) {  // gather the slabs (masked lines are exactly 0)
+        CUDA_TRY(cudaMemsetAsync(c->io, 0, sizeof(cd) * c->S * 3, c->stream));
+        for (const Part& p : c->parts) {
+            int rc2 = copy_slab3(c, p, false);
+            if (rc2) return rc2;
+        }
+        if (c->comm) {
+            const ncclResult_t nr = ncclAllReduce(c->io, c->io, 2 * 3 * (size_t)c->S, ncclDouble,
+                                                  ncclSum, c->comm, c->stream);
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+        }
+        return SKG_OK;
+    }
     if (c->dist) {  // gather the slabs (masked columns are exactly 0)
         CUDA_TRY(cudaMemsetAsync(c->cmfull, 0, sizeof(cd) * c->S, c->stream));
         for (const Part& p : c->parts)
@@ -685,9 +839,9 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         return fail(SKG_ECUDA, "no CUDA device visible (the library has no CPU path)");
     if (device < 0 || device >= ndev) return fail(SKG_ECONFIG, "device ordinal out of range");
     if (world < 1 || rank < 0 || rank >= world) return fail(SKG_ECONFIG, "bad rank / world size");
-    if (world > 1 && sid != 2)
-        return fail(SKG_EUNSUPPORTED, "slab decomposition is implemented for ns2d only");
-    if (world > 1 && n[0] % (4 * world))
+    if (world > 1 && sid == 3 && n[0] % world)
+        return fail(SKG_ECONFIG, "nx must be divisible by world for the slab decomposition");
+    if (world > 1 && sid == 2 && n[0] % (4 * world))
         return fail(SKG_ECONFIG, "nx must be divisible by 4 * world for the slab decomposition");
 
     auto c = new skg_ctx();
@@ -744,7 +898,46 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
             cudaMemcpy(c->d_cstart, c->cstart.data(), sizeof(int) * (world + 1), cudaMemcpyHostToDevice);
         }
     }
-    if (c->dist) {
+    if (sid == 3 && c->dist) {  // contiguous runs of compact kept ky lines, x rows
+        const int Kyc = 2 * c->kc[1] + 1;
+        if (Kyc < world) return cleanup(SKG_ECONFIG, "more ranks than kept ky lines");
+        c->cstart.resize(world + 1);
+        for (int q = 0; q <= world; ++q) c->cstart[q] = (int)((long long)q * Kyc / world);
+        c->nrl = n[0] / world;
+        std::vector<int> owner(Kyc);
+        for (int q = 0; q < world; ++q)
+            for (int k = c->cstart[q]; k < c->cstart[q + 1]; ++k) owner[k] = q;
+        ok = ok && alloc((void**)&c->d_kowner, sizeof(int) * Kyc);
+        ok = ok && alloc((void**)&c->d_cstart, sizeof(int) * (world + 1));
+        if (ok) {
+            cudaMemcpy(c->d_kowner, owner.data(), sizeof(int) * Kyc, cudaMemcpyHostToDevice);
+            cudaMemcpy(c->d_cstart, c->cstart.data(), sizeof(int) * (world + 1), cudaMemcpyHostToDevice);
+        }
+        const size_t nx = n[0], ny = n[1], nh = c->nh, nrl = c->nrl;
+        for (int q = 0; q < world; ++q) {
+            if (nccl_id && q != rank) continue;
+            Part p;
+            p.r = q;
+            p.c0 = c->cstart[q];
+            p.ncols = c->cstart[q + 1] - c->cstart[q];
+            p.vs = nx * p.ncols * nh;
+            p.fs = std::max(p.vs, nrl * ny * nh);
+            p.rfs = nrl * Kyc * nh;
+            ok = ok && alloc((void**)&p.u, sizeof(cd) * 3 * p.vs);
+            for (int i = 0; i < 3; ++i) ok = ok && alloc((void**)&p.k[i], sizeof(cd) * 3 * p.vs);
+            ok = ok && alloc((void**)&p.A3, sizeof(cd) * 5 * p.fs);
+            ok = ok && alloc((void**)&p.B3, sizeof(cd) * 6 * p.fs);
+            ok = ok && alloc((void**)&p.rA3, sizeof(cd) * 5 * p.rfs);
+            ok = ok && alloc((void**)&p.sD3, sizeof(cd) * 3 * p.rfs);
+            c->parts.push_back(p);
+        }
+        if (ok && nccl_id) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            const ncclResult_t nr = ncclCommInitRank(&c->comm, world, id, rank);
+            if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
+        }
+    } else if (c->dist) {
         const int Kc = c->kc[1] + 1, PP = (Kc + 1) / 2;
         const size_t nx = n[0], nrl = c->nrl;
         for (int q = 0; q < world; ++q) {
@@ -825,6 +1018,10 @@ int skg_destroy(skg_ctx* c) {
             cudaFree(p.sA[f]);
             cudaFree(p.rA[f]);
         }
+        cudaFree(p.A3);
+        cudaFree(p.B3);
+        cudaFree(p.rA3);
+        cudaFree(p.sD3);
     }
     cudaFree(c->cmfull);
     cudaFree(c->d_kowner);

@@ -99,3 +99,71 @@ def slab_tendency(w_full, n, rank, G):
     if c0 == 0:
         N[0, 0] = 0
     return N, c0, c1
+
+
+# ------------------------------------------------------------------ ns3d
+def partition3(Kyc, nx, G):
+    """Compact kept ky lines [kstart[q], kstart[q+1]) and x rows nx / G of
+    rank q (csrc/skgpu.cu create_impl, ns3d branch)."""
+    return [q * Kyc // G for q in range(G + 1)], nx // G
+
+
+def slab3d_tendency(v_full, n, rank, G):
+    """Dealiased-path ns3d tendency computed on the slab of `rank` with the
+    block layouts of csrc/skgpu.cu exchange3 and csrc/ns3d.cu (send blocks of
+    the x-inverse [xl][kyl_r][kz], of the y-forward [xl][kyl_q][kz]); returns
+    this rank's lines (3, nx, nkyl, kzc) and their global ky indices."""
+    nx, ny, nz = n
+    kx, ky, kz = O.k_axes(n)
+    mask = O.dealias_mask(n).astype(bool)
+    kcy = int(np.abs(ky[mask[0, :, 0]]).max() / (ky[1] - ky[0]) + 0.5)
+    kcz = int(mask[0, 0].sum()) - 1
+    Kyc, kzc = 2 * kcy + 1, kcz + 1
+    gky = np.array(list(range(kcy + 1)) + list(range(ny - kcy, ny)))   # compact -> global
+    kstart, nrl = partition3(Kyc, nx, G)
+    c0, c1 = kstart[rank], kstart[rank + 1]
+    nl = [kstart[q + 1] - kstart[q] for q in range(G)]
+    V = v_full[:, :, gky[c0:c1], :kzc]                     # (3, nx, nkyl, kzc)
+    KX = kx[:, None, None]
+    # x-inverse: vx, vy, vz, kx vy, kx vz
+    F = [V[0], V[1], V[2], KX * V[1], KX * V[2]]
+    X = [np.fft.ifft(f, axis=0) * nx for f in F]           # (x, kyl, kz)
+    sizes = [nrl * nl[q] * kzc for q in range(G)]
+    R = [_a2a([x[q * nrl:(q + 1) * nrl].reshape(-1).copy() for q in range(G)], sizes) for x in X]
+    def lines(Rf):   # (xl, Kyc, kz) from the owners' blocks
+        return np.concatenate([Rf[q].reshape(nrl, nl[q], kzc) for q in range(G)], axis=1)
+    P = [lines(Rf) for Rf in R]
+    KY = ky[gky][None, :, None]
+    KZ = kz[:kzc][None, None, :]
+    spec = [P[0], P[1], P[2],
+            1j * KY * P[2] - 1j * KZ * P[1],               # wx
+            1j * KZ * P[0] - 1j * P[4],                    # wy = i kz vx - i kx vz
+            1j * P[3] - 1j * KY * P[0]]                    # wz = i kx vy - i ky vx
+    def to_phys(h):
+        full = np.zeros((nrl, ny, nz // 2 + 1), complex)
+        full[:, gky, :kzc] = h
+        y = np.fft.ifft(full, axis=1) * ny
+        y[..., 0] = y[..., 0].real
+        y[..., -1] = y[..., -1].real
+        return np.fft.irfft(y, n=nz, axis=2) * nz
+    ux, uy, uz, ox, oy, oz = (to_phys(h) for h in spec)
+    cross = [uy * oz - uz * oy, uz * ox - ux * oz, ux * oy - uy * ox]
+    def to_spec(c):
+        s = np.fft.fft(np.fft.rfft(c, axis=2)[..., :kzc], axis=1)[:, gky, :] / (nx * ny * nz)
+        return s                                            # (xl, Kyc, kz)
+    D = [to_spec(c) for c in cross]
+    sizes = [nrl * nl[rank] * kzc] * G
+    RD = [_a2a([d[:, kstart[q]:kstart[q + 1]].reshape(-1).copy() for q in range(G)], sizes) for d in D]
+    out = [np.fft.fft(np.concatenate([r[q].reshape(nrl, nl[rank], kzc) for q in range(G)], axis=0), axis=0)
+           for r in RD]
+    KYl = ky[gky[c0:c1]][None, :, None]
+    ksq = KX ** 2 + KYl ** 2 + KZ ** 2
+    nzm = ksq != 0
+    s = (KX * out[0] + KYl * out[1] + KZ * out[2]) / np.where(nzm, ksq, 1.0)
+    out = [np.where(nzm, out[0] - KX * s, out[0]), np.where(nzm, out[1] - KYl * s, out[1]),
+           np.where(nzm, out[2] - KZ * s, out[2])]
+    keep = mask[:, gky[c0:c1], :kzc]
+    out = np.stack([np.where(keep, o, 0) for o in out])
+    if c0 == 0:
+        out[:, 0, 0, 0] = 0
+    return out, gky[c0:c1], kzc

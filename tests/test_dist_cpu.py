@@ -1,4 +1,4 @@
-"""Multi-process (gloo, world_size 2 and 4) check of the ns2d slab
+"""Multi-process (gloo, world_size 2 and 4) check of the ns2d / ns3d slab
 decomposition's host-side logic: partitions, block layouts and the two
 all-to-all transposes (tests/dist_slab_np.py mirrors csrc/skgpu.cu and the
 fast-path kernels' indexing) against the undecomposed oracle tendency."""
@@ -43,6 +43,33 @@ def test_slab_decomposition_gloo(world, n):
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _port(), n, out), nprocs=world, join=True)
+    assert len(out) == world
+    for r in range(world):
+        assert out[r] < 1e-12, (r, out[r])
+
+
+def _worker3(rank, world, port, n, out):
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    sys.path[:0] = [str(here), str(here.parent)]
+    import torch.distributed as dist
+    from dist_slab_np import slab3d_tendency
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    v = ic.ns3d_ic(n, seed=5)
+    N, gky, kzc = slab3d_tendency(v, n, rank, world)
+    ref = O.tendency_ns3d(v, n)[:, :, gky, :kzc]
+    out[rank] = max(O.rel_l2(N[c], ref[c]) for c in range(3))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, (16, 16, 16)), (4, (16, 32, 16)), (2, (32, 16, 8))])
+def test_slab3d_decomposition_gloo(world, n):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker3, args=(world, _port(), n, out), nprocs=world, join=True)
     assert len(out) == world
     for r in range(world):
         assert out[r] < 1e-12, (r, out[r])

@@ -1,4 +1,4 @@
-"""Slab decomposition on ONE GPU: all `world` partitions of the ns2d state
+"""Slab decomposition on ONE GPU: all `world` partitions of the ns2d / ns3d state
 run in one process with device copies standing in for the NCCL all-to-all
 (the same kernels and block layouts as the multi-process NCCL path).  The
 result must reproduce the single-partition path and the reference."""
@@ -53,8 +53,58 @@ def test_slab_needs_dealiased_state():
 def test_slab_config_errors():
     with pytest.raises(api.ConfigError):
         api.Simulation("ns2d", (64, 64), 1e-3, 1e-3, world=64)   # 64 % (2*64) != 0
-    with pytest.raises(api.UnsupportedError):
-        api.Simulation("ns3d", (16, 16, 16), 1e-3, 1e-3, world=2)
+    with pytest.raises(api.ConfigError):
+        api.Simulation("ns3d", (16, 16, 16), 1e-3, 1e-3, world=3)  # nx % world
+    with pytest.raises(api.ConfigError):
+        api.Simulation("ns3d", (16, 16, 16), 1e-3, 1e-3, world=16)  # 11 kept ky lines
+
+
+@pytest.mark.parametrize("n,world", [((32, 32, 32), 2), ((64, 64, 64), 4), ((64, 32, 128), 8),
+                                     ((128, 128, 128), 8), ((16, 64, 32), 16)])
+def test_slab3d_matches_single_partition(n, world):
+    u0 = ic.ns3d_ic(n, seed=7)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    one = api.Simulation("ns3d", n, 1e-3, dt)
+    one.set_state(u0)
+    one.step(3)
+    d = api.Simulation("ns3d", n, 1e-3, dt, world=world)
+    d.set_state(u0)
+    d.step(3)
+    a, b = d.get_state(), one.get_state()
+    for v in range(3):
+        assert O.rel_l2(a[v], b[v]) < 1e-14
+    assert d.iteration == 3
+
+
+def test_slab3d_matches_reference(ref_lib):
+    n = (64, 64, 64)
+    u0 = ic.ns3d_ic(n, seed=9)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    r = ref_lib.RefSimulation("ns3d", n, 1e-3, dt)
+    r.set_state(u0)
+    r.step(10)
+    d = api.Simulation("ns3d", n, 1e-3, dt, world=4)
+    d.set_state(u0)
+    d.step(10)
+    s, rs = d.get_state(), r.get_state()
+    assert max(O.rel_l2(s[v], rs[v]) for v in range(3)) < 1e-10
+
+
+def test_slab3d_run_series_and_divergence():
+    n = (32, 32, 32)
+    u0 = ic.ns3d_ic(n, seed=4)
+    one = api.Simulation("ns3d", n, 1e-2, 1e-3)
+    one.set_state(u0)
+    d = api.Simulation("ns3d", n, 1e-2, 1e-3, world=2)
+    d.set_state(u0)
+    a, b = d.run(4), one.run(4)
+    assert np.allclose(a, b, rtol=1e-12, atol=0)
+    bad = u0.copy()
+    bad[2, 1, 1, 1] = np.nan
+    d.set_state(bad)
+    with pytest.raises(api.DivergenceError) as ei:
+        d.step(3)
+    assert ei.value.iteration == d.iteration
 
 
 def test_slab_run_series():
