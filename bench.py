@@ -48,7 +48,11 @@ CONFIGS = {
     "ns2d_1024": ("ns2d", (1024, 1024), 1e-4, 1e-3, 10),
     "ns3d_128": ("ns3d", (128, 128, 128), 1e-3, None, 10),
     "ns3d_512": ("ns3d", (512, 512, 512), 2e-4, None, 10),
+    # one B200 in the compact (kept-modes) layout; IC generated at 128^3 and
+    # spectrally embedded (all of its energy lies below |k| = 64)
+    "ns3d_1024": ("ns3d", (1024, 1024, 1024), 1e-4, None, 5),
 }
+COARSE_IC = {"ns3d_1024": (128, 128, 128)}
 
 
 def dist_env():
@@ -136,6 +140,12 @@ class ClockSampler:
 def make_input(cfg_name):
     from paper_1807_01769_b200 import ic
     solver, n, nu, dt, _ = CONFIGS[cfg_name]
+    if cfg_name in COARSE_IC:
+        small = COARSE_IC[cfg_name]
+        v = ic.initial_state(solver, small, seed=1234)
+        if dt is None:  # same max|u| (band-limited field), finer spacing
+            dt = ic.cfl_dt(solver, small, v, cfl=0.5) * small[0] / n[0]
+        return solver, n, nu, dt, ic.embed(v, n)
     u0 = ic.initial_state(solver, n, seed=1234)
     if dt is None:
         dt = ic.cfl_dt(solver, n, u0, cfl=0.5)
@@ -158,6 +168,11 @@ def cpu_reference_rate(solver, n, nu, dt, u0, steps, warmup, threads):
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
+        return 0
+    if args.config in COARSE_IC:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"{args.config}: one reference step needs hundreds of GB of host memory "
+                          "and minutes (bounded-sample rule); the ns3d_512 arm is the CPU reference"}))
         return 0
     solver, n, nu, dt, u0 = make_input(args.config)
     P = int(np.prod(n))
@@ -217,7 +232,7 @@ def run_our_arm(args):
         dist.broadcast_object_list(obj, src=0)
         sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
     else:
-        sim = api.Simulation(solver, n, nu, dt, device=local)
+        sim = api.Simulation(solver, n, nu, dt, device=local, compact=args.config in COARSE_IC)
     # a dedicated (non-default) stream: the library launches on it and the
     # CUDA events below are recorded on the same stream
     stream = torch.cuda.Stream(device=local)
@@ -316,7 +331,11 @@ def run_our_arm(args):
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
-    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline and args.config in COARSE_IC:
+        cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+               "sample": "not run: one reference step at this size needs hundreds of GB of host "
+                         "memory and minutes; see the ns3d_512 line"}
+    elif ws == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
             times = cpu_reference_rate(solver, n, nu, dt, u0, args.cpu_steps, 1, threads)

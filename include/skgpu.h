@@ -65,15 +65,19 @@ int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const 
 int skg_destroy(skg_ctx* ctx);
 
 /*
- * Slab-decomposed context (ns2d): the dealiased state is split
- * over the kept ky columns, physical space over x rows; each RK stage runs
- * x-inverse -> all-to-all -> y pass -> all-to-all -> x-forward, with the
- * transposes as grouped NCCL send/recv (one block per peer) on the context
- * stream.  This process runs partition `rank` of `world` on `device`;
- * nccl_id = the 128 bytes of skg_nccl_unique_id() from rank 0, broadcast by
- * the caller.  nccl_id == NULL runs ALL `world` partitions in this process
- * on one device with device copies as the exchange (tests).  State I/O is
- * the full reference layout on every rank; tendency/energy are not offered.
+ * Slab-decomposed context (ns2d, ns3d): the dealiased state is
+ * split over the kept ky columns (ns2d) / kept ky lines (ns3d), physical
+ * space over x rows; each RK stage runs x-inverse -> all-to-all -> y (and z)
+ * passes -> all-to-all -> x-forward, with the transposes as grouped NCCL
+ * send/recv (one block per peer) on the context stream.  This process runs
+ * partition `rank` of `world` on `device`; nccl_id = the 128 bytes of
+ * skg_nccl_unique_id() from rank 0, broadcast by the caller.  nccl_id ==
+ * NULL runs ALL `world` partitions in this process on one device with device
+ * copies as the exchange (tests).  ns3d with world == 1 is the compact
+ * single-GPU layout: state and intermediates hold only the kept (ky, kz)
+ * lines (about 2.4x less memory than skg_create; 1024^3 fits one B200).
+ * State I/O is the full reference layout on every rank; tendency/energy are
+ * not offered; the state must be dealiased (SKG_EUNSUPPORTED otherwise).
  */
 int skg_nccl_unique_id(char* out128);
 int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,

@@ -194,10 +194,12 @@ class Simulation:
 
     def __init__(self, solver: str, n, nu: float = 0.0, dt: float = 0.0, scheme: str = "RK4",
                  L=None, dealias_coef: float = 2.0 / 3.0, device: int = 0, world: int = 1,
-                 rank: int = 0, nccl_id: bytes | None = None):
+                 rank: int = 0, nccl_id: bytes | None = None, compact: bool = False):
         """world > 1: slab decomposition (ns2d and ns3d).  With nccl_id (from
         nccl_unique_id() on rank 0) this process runs partition `rank` over
-        NCCL; without it all `world` partitions run here on one device."""
+        NCCL; without it all `world` partitions run here on one device.
+        compact (ns3d, world 1): the kept-modes-only layout of the slab path
+        on one GPU (dealiased states only; 1024^3 fits one B200)."""
         L_ = load_library()
         self.solver = solver
         self.n = tuple(int(x) for x in n)
@@ -212,7 +214,7 @@ class Simulation:
         cn = (C.c_int * self.dims)(*self.n)
         cL = None if L is None else (C.c_double * self.dims)(*L)
         sch = SKG_RK2 if self.scheme == "RK2" else SKG_RK4
-        if world > 1:
+        if world > 1 or (compact and solver == "ns3d"):
             rc = L_.skg_create_dist(C.byref(h), solver.encode(), self.dims, cn, cL,
                                     float(dealias_coef), self.nu, sch, int(device), int(rank),
                                     int(world), nccl_id)

@@ -151,13 +151,22 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, (PZ || EM == 8) ? 2 : 1)
     // same thread-private layout), so all loads are in flight at once.
     const cd* kprev = stage == 2 ? a.k1 : stage == 3 ? a.k2 : a.k3;
     cd* kv = sm;  // exchange buffer as k staging: kv[slot * T + t]
+    if ((a.opt & 8) && l == 0) {  // the columns one wave ahead
+        const int nk = (blockIdx.x + a.wave) * LPC;
+        const int ncol = NM == 2 ? a.ncols : a.ky_in;
+        if (nk < ncol) {
+            const size_t c = ncol - nk < LPC ? ncol - nk : LPC;
+            l2_prefetch(a.u + (size_t)nk * NX, sizeof(cd) * NX * c, t, T);
+            if (stage > 1) l2_prefetch(kprev + (size_t)nk * NX, sizeof(cd) * NX * c, t, T);
+        }
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         if (e >= ZLO && e < ZHI) continue;
         const int slot = e < ZLO ? e : e - (ZHI - ZLO);
         const int i = t + T * e;
         const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
-        if (keep) {
+        if (keep && !(a.opt & 32)) {  // opt 32 diagnostic: no loads
             const size_t idx = (size_t)kyl * NX + i;
             cp_async16(&sv[slot * T + t], a.u + idx);
             if (stage > 1) cp_async16(&kv[slot * T + t], kprev + idx);
@@ -178,7 +187,10 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, (PZ || EM == 8) ? 2 : 1)
                                        stage > 1 ? kv[slot * T + t] : zero());
             const double kxv = a.kx_scale * (double)si;
             const double ksq = kxv * kxv + kyv * kyv;
-            if (ksq != 0.0) psi = mk(s.x / ksq, s.y / ksq);
+            if (ksq != 0.0) {  // one reciprocal instead of two IEEE divisions
+                const double r = __drcp_rn(ksq);
+                psi = mk(s.x * r, s.y * r);
+            }
         }
         sv[slot * T + t] = psi;
     }
@@ -539,10 +551,36 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
         const int ro = x / a.nrl, xl = x - ro * a.nrl;
         return ro * blk + ((size_t)(kyl >> 1) * a.nrl + xl) * 2 + (kyl & 1);
     };
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    if (active && (a.opt & 1)) {  // field B of this column (all source blocks)
+        for (int ro = 0; ro < a.G; ++ro)
+            l2_prefetch(a.rA[1] + ro * blk + (size_t)(kyl >> 1) * a.nrl * 2, sizeof(cd) * 2 * a.nrl, t, T);
+    }
+    if (active && final && (a.opt & 2)) {  // RK epilogue operands
+        const size_t col = (size_t)kyl * NX;
+        l2_prefetch(a.u + col, sizeof(cd) * NX, t, T);
+        if (!a.rk2) {
+            l2_prefetch(a.k1 + col, sizeof(cd) * NX, t, T);
+            l2_prefetch(a.k2 + col, sizeof(cd) * NX, t, T);
+            l2_prefetch(a.k3 + col, sizeof(cd) * NX, t, T);
+        }
+    }
+    if ((a.opt & 4) && l == 0) {  // both fields of the column one wave ahead
+        const int nk = (blockIdx.x + a.wave) * LPC;
+        if (nk < a.ncols) {
+            const int c = a.ncols - nk < LPC ? a.ncols - nk : LPC;
+            const size_t np = (size_t)((nk + c - 1) >> 1) - (nk >> 1) + 1;
+            for (int ro = 0; ro < a.G; ++ro)
+                for (int f = 0; f < 2; ++f)
+                    l2_prefetch(a.rA[f] + ro * blk + (size_t)(nk >> 1) * a.nrl * 2,
+                                sizeof(cd) * 2 * a.nrl * np, t, T);
+        }
+    }
     cd v[E];
+    const bool noload = (a.opt & 16) != 0;  // diagnostic: FFT cost without the loads
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.rA[0][ridx(t + T * e)] : zero();
+        v[e] = noload ? mk(e, t) : active ? a.rA[0][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -553,9 +591,8 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = active ? a.rA[1][ridx(t + T * e)] : zero();
+        v[e] = noload ? mk(t, e) : active ? a.rA[1][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
-    const bool final = a.rk2 ? stage == 2 : stage == 4;
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     bool bad = false;
     // per-step E, Z, eps of the new state (Simulation::energy / enstrophy /
@@ -609,8 +646,9 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
                 const double n2 = un.x * un.x + un.y * un.y;
                 sZ += 0.5 * pw * n2;
                 if (ksq > 0.0) {
-                    sE += 0.5 * pw * n2 / ksq;
-                    if (a.has_sigma) sD += 2.0 * a.nu * ksq * (0.5 * pw * n2 / ksq);
+                    const double en = 0.5 * pw * n2 * __drcp_rn(ksq);
+                    sE += en;
+                    if (a.has_sigma) sD += 2.0 * a.nu * ksq * en;
                 }
             }
         }

@@ -58,7 +58,7 @@ __device__ __forceinline__ int ky_of(const Ns3dArgs& a, int kyi) {
 
 // state index of mode (kx, line ys of the state layout, kz)
 __device__ __forceinline__ size_t sidx(const Ns3dArgs& a, int kx, int ys, int kz) {
-    return ((size_t)kx * a.ystate + ys) * a.nh + kz;
+    return ((size_t)kx * a.ystate + ys) * a.sz + kz;
 }
 
 // compact kept index of a kept ky (0..kcy, then ny-kcy..ny-1)
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
     if (a.flags->diverged) return;
     if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     const int ky = ky_of(a, kyi);
-    const int ys = a.G == 1 ? ky : kyi - a.kys;
+    const int ys = a.slab ? kyi - a.kys : ky;
     cd* sm = smem + l * F::SMEM;
     cd* slots = smem + C * F::SMEM;  // slots[slot * CT + tid]
     cd* kst = smem;                  // k staging in the idle exchange buffers
@@ -189,8 +189,8 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
     const double kzv = a.kz_scale * (double)kz;
-    const cd* Ab = a.G == 1 ? a.A : a.rA;
-    const size_t afs = a.G == 1 ? a.fstride : a.rfs;
+    const cd* Ab = a.slab ? a.rA : a.A;
+    const size_t afs = a.slab ? a.rfs : a.fstride;
     const cd* A0 = Ab;
     const cd* A1 = Ab + afs;
     const cd* A2 = Ab + 2 * afs;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
             cd r = zero();
             if (keep) {
                 size_t q;
-                if (a.G == 1) {
+                if (!a.slab) {
                     q = ((size_t)x * a.ny + j) * a.kz_in + kz;
                 } else {  // receive block of the line's owner, layout [xl][kyl][kz]
                     const int kyi = ky_compact(a, j);
@@ -257,9 +257,28 @@ struct Z3 {
     static constexpr int SLOT = F::SMEM + 5 * NZ / 2;  // exchange + 5 rows of doubles (cd units)
 };
 
+// Raw inputs of one packed c2r (fields P, Q of a row; kept kz only).
 template <int NZ>
-__device__ __forceinline__ void load_packed(const Ns3dArgs& a, const cd* P, const cd* Q, size_t row,
-                                            bool active, int t, cd* v) {
+__device__ __forceinline__ void fetch_pair(const Ns3dArgs& a, const cd* P, const cd* Q, size_t row,
+                                           bool active, int t, cd* p, cd* q) {
+    using F = typename Z3<NZ>::F;
+    constexpr int T = F::T, E = F::E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int idx = t + T * e;
+        const int ki = idx > NZ / 2 ? NZ - idx : idx;
+        p[e] = zero();
+        q[e] = zero();
+        if (active && ki < a.kz_in) {
+            p[e] = P[row + ki];
+            q[e] = Q[row + ki];
+        }
+    }
+}
+
+// Hermitian-extended P + i Q (two c2r as one complex FFT).
+template <int NZ>
+__device__ __forceinline__ void pack_pair(int t, const cd* p, const cd* q, cd* v) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E;
 #pragma unroll
@@ -267,27 +286,25 @@ __device__ __forceinline__ void load_packed(const Ns3dArgs& a, const cd* P, cons
         const int idx = t + T * e;
         const bool mirror = idx > NZ / 2;
         const int ki = mirror ? NZ - idx : idx;
-        cd p = zero(), q = zero();
-        if (active && ki < a.kz_in) {
-            p = P[row + ki];
-            q = Q[row + ki];
-            if (ki == 0 || 2 * ki == NZ) {  // c2r ignores these imaginary parts
-                p.y = 0.0;
-                q.y = 0.0;
-            }
+        cd pp = p[e], qq = q[e];
+        if (ki == 0 || 2 * ki == NZ) {  // c2r ignores these imaginary parts
+            pp.y = 0.0;
+            qq.y = 0.0;
         }
-        v[e] = mirror ? mk(p.x + q.y, q.x - p.y) : mk(p.x - q.y, p.y + q.x);
+        v[e] = mirror ? mk(pp.x + qq.y, qq.x - pp.y) : mk(pp.x - qq.y, pp.y + qq.x);
     }
 }
 
-template <int NZ>
+// PF: the raw inputs of the next packed FFT are loaded into registers while
+// the current one runs (6 inverse FFTs per row pair, one exposed load).
+template <int NZ, bool PF>
 __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E, G = Z3<NZ>::G;
     extern __shared__ cd smem[];
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const long long r0 = 2ll * ((long long)blockIdx.x * G + g);
-    const bool active = r0 < (long long)a.nrl * a.ny;
+    const bool active = r0 < (long long)a.nrl * a.ny && !(a.opt & 16);
     if (a.flags->diverged) return;
     cd* sm = smem + g * Z3<NZ>::SLOT;
     double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
@@ -295,12 +312,24 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     const cd* B = a.B;
     const size_t fs = a.fstride;
     const double h = 0.5 * a.inv_n;
+    // input field pairs of the three packed inverse FFTs of a row
+    const cd* FP[3] = {B + 2 * fs, B + 4 * fs, B + 0 * fs};
+    const cd* FQ[3] = {B + 3 * fs, B + 5 * fs, B + 1 * fs};
+    if (active && !(a.opt & 2)) {  // the row pair of all six fields into L2 up front
+        const size_t bytes = sizeof(cd) * 2 * a.kz_in;
+        for (int f = 0; f < 6; ++f)
+            l2_prefetch(B + f * fs + (size_t)r0 * a.kz_in, bytes, t, T);
+    }
+    cd p[E], q[E];
+    if (PF) fetch_pair<NZ>(a, FP[0], FQ[0], (size_t)r0 * a.kz_in, active, t, p, q);
 #pragma unroll 1
     for (int rr = 0; rr < 2; ++rr) {
         const size_t row = (size_t)(r0 + rr) * a.kz_in;
         cd v[E];
         // w + i wx
-        load_packed<NZ>(a, B + 2 * fs, B + 3 * fs, row, active, t, v);
+        if (!PF) fetch_pair<NZ>(a, FP[0], FQ[0], row, active, t, p, q);
+        pack_pair<NZ>(t, p, q, v);
+        if (PF) fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -308,7 +337,9 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[1 * NZ + t + T * e] = v[e].y;
         }
         // wy + i wz
-        load_packed<NZ>(a, B + 4 * fs, B + 5 * fs, row, active, t, v);
+        if (!PF) fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
+        pack_pair<NZ>(t, p, q, v);
+        if (PF) fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -316,7 +347,9 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[3 * NZ + t + T * e] = v[e].y;
         }
         // u + i v, then the cross product (solvers.cpp:321-325)
-        load_packed<NZ>(a, B + 0 * fs, B + 1 * fs, row, active, t, v);
+        if (!PF) fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
+        pack_pair<NZ>(t, p, q, v);
+        if (PF && rr == 0) fetch_pair<NZ>(a, FP[0], FQ[0], row + a.kz_in, active, t, p, q);
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -389,13 +422,13 @@ __global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
             v[e] = active ? in[((size_t)x * a.ny + (t + T * e)) * a.kz_o + kz] : zero();
         F::template run<-1>(v, sm, t, wb, salt);
         if (active) {
-            cd* out = a.G == 1 ? a.B + m * a.fstride   // D fields live in B's memory
-                               : a.sD + m * a.rfs;
+            cd* out = a.slab ? a.sD + m * a.rfs
+                             : a.B + m * a.fstride;  // D fields live in B's memory
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int j = t + T * e;
                 if (abs(signed_index(j, NY)) > a.kcy) continue;  // masked: never read
-                if (a.G == 1) {
+                if (!a.slab) {
                     out[((size_t)x * a.ny + j) * a.kz_o + kz] = v[e];
                 } else {  // send block of the line's owner q, layout [xl][kyl_q][kz]
                     const int kyi = ky_compact(a, j);
@@ -424,7 +457,7 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
     const bool active = kz < a.kz_o;
     if (a.flags->diverged) return;
     const int ky = ky_of(a, kyi);
-    const int ys = a.G == 1 ? ky : kyi - a.kys;
+    const int ys = a.slab ? kyi - a.kys : ky;
     const int sky = signed_index(ky, a.ny);
     const bool keep_y = abs(sky) <= a.kcy;
     cd* sm = smem + l * F::SMEM;
@@ -480,7 +513,8 @@ __global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
             const double ksq = kxv * kxv + kyv * kyv + kzv * kzv;
             if (ksq != 0.0) {
                 const cd dot = add(add(scale(c0, kxv), scale(c1, kyv)), scale(c2, kzv));
-                const cd sp = mk(dot.x / ksq, dot.y / ksq);
+                const double rk = __drcp_rn(ksq);
+                const cd sp = mk(dot.x * rk, dot.y * rk);
                 c0 = sub(c0, scale(sp, kxv));
                 c1 = sub(c1, scale(sp, kyv));
                 c2 = sub(c2, scale(sp, kzv));
@@ -625,16 +659,21 @@ cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int NZ>
-cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
+template <int NZ, bool PF>
+cudaError_t launch_z3_v(const Ns3dArgs& a, cudaStream_t s) {
     using Z = Z3<NZ>;
     const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
     static size_t done = 0;
-    set_smem(k3_3d<NZ>, smem, done);
+    set_smem(k3_3d<NZ, PF>, smem, done);
     const long long pairs = (long long)a.nrl * a.ny / 2;
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
-    k3_3d<NZ><<<grid, Z::T * Z::G, smem, s>>>(a);
+    k3_3d<NZ, PF><<<grid, Z::T * Z::G, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+template <int NZ>
+cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
+    return (a.opt & 1) ? launch_z3_v<NZ, true>(a, s) : launch_z3_v<NZ, false>(a, s);
 }
 
 #define SKG3_CASES(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)

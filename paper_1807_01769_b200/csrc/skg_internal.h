@@ -35,6 +35,8 @@ __host__ __device__ __forceinline__ int signed_index(int i, int n) { return i <=
 // are row-major [x][ky] with row stride ld (only the ky columns that can be
 // non-zero are stored).
 struct Ns2dArgs {
+    int opt;            // tuning bits (SKG_OPT, read once on the host)
+    int wave;           // resident CTAs of the x passes (next-wave prefetch)
     int nx, ny, nh;
     int kcx, kcy;       // dealias: keep |kx_i| <= kcx and ky_i <= kcy
     int ky_in;          // columns read by the x-inverse pass (kcy+1 pruned, nh full)
@@ -114,6 +116,7 @@ bool ns2d_supported(int nx, int ny);
 //   D[3] after the y-forward pass  (x, ky, kz)  kz <= kcz
 // C aliases A and D aliases B (each is dead when the other is produced).
 struct Ns3dArgs {
+    int opt;                // tuning bits (SKG_OPT)
     int nx, ny, nz, nh;
     int kcx, kcy, kcz;
     int pruned, has_sigma, rk2;
@@ -136,22 +139,36 @@ struct Ns3dArgs {
     DevFlags* flags;
     double* diag;           // per-step (E, Z, eps) series, slot steps-1; nullptr = off
     double nu;
-    // Slab decomposition (G = 1 on one GPU): this rank owns the kept ky
-    // lines [kys, kys + nkyl) (compact kept index kyi: 0..kcy, then the
-    // negative ky) of the state and the x rows [r nrl, (r + 1) nrl) of the
-    // y/z passes.  The state and the x-pass intermediates are indexed
-    // ((x * ystate + ys) * kz + ...) with ystate = ny, ys = ky when G = 1 and
-    // ystate = nkyl, ys = kyi - kys otherwise (send/receive blocks of the
-    // two all-to-alls are then contiguous x ranges).  y-pass reads of A and
-    // writes of D go through the owner table of each kept line.
+    // Slab layout (slab = 1; G partitions, G = 1 is the compact single-GPU
+    // layout): this rank owns the kept ky lines [kys, kys + nkyl) (compact
+    // kept index kyi: 0..kcy, then the negative ky) of the state and the x
+    // rows [r nrl, (r + 1) nrl) of the y/z passes.  The state and the x-pass
+    // intermediates are indexed ((x * ystate + ys) * kz + ...) with
+    // ystate = ny, ys = ky in the full layout (slab = 0) and ystate = nkyl,
+    // ys = kyi - kys in the slab layout (send/receive blocks of the two
+    // all-to-alls are then contiguous x ranges; state lines hold only the
+    // kept kz).  y-pass reads of A and writes of D go through the owner
+    // table of each kept line.
     int G, r, lead, kys, nkyl, nrl;
+    int slab;               // 1: partitioned layout (any G, including one partition)
     int ystate;
+    int sz;                 // kz extent of a state line (nh; kz_in = kcz + 1 in slab layout)
     const int* kowner;      // owner rank of each compact kept ky line (2 kcy + 1)
     const int* kstart;      // first compact line of each rank (G + 1)
     cd* rA;                 // received x-inverse outputs (5 fields, stride rfs), G > 1
     cd* sD;                 // y-forward outputs to send (3 fields, stride rfs), G > 1
     size_t rfs;
 };
+
+// L2 prefetch of [p, p + bytes) (bytes a multiple of 16, p 16-byte aligned),
+// split in 4 KB bulk requests over the calling threads.
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes, int t, int nt) {
+    const char* c = static_cast<const char*>(p);
+    for (size_t off = (size_t)t * 4096; off < bytes; off += (size_t)nt * 4096) {
+        const unsigned n = (unsigned)(bytes - off < 4096 ? bytes - off : 4096);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(c + off), "r"(n) : "memory");
+    }
+}
 
 // Warp-sum three doubles and add them to slot[0..2] (all 32 lanes must call).
 __device__ __forceinline__ void diag_accumulate(double* slot, double e, double z, double d) {

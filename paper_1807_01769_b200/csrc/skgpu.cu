@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -91,6 +92,7 @@ struct Part {
 
 struct skg_ctx {
     int device = 0;
+    int nsm = 148;
     int solver = 2;  // 2: ns2d, 3: ns3d
     int dims = 2;
     int n[3] = {1, 1, 1};
@@ -252,8 +254,24 @@ const double* etab_ptr(const skg_ctx* c, int which, int axis) {
     return c->etab + off;
 }
 
+int env_opt() {
+    static const int v = [] {
+        const char* e = std::getenv("SKG_OPT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+int sm_count(int device) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n;
+}
+
 skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     skg::Ns2dArgs a{};
+    a.opt = env_opt();
+    a.wave = 2 * c->nsm;
     a.nx = c->n[0];
     a.ny = c->n[1];
     a.nh = c->nh;
@@ -325,6 +343,7 @@ skg::Ns2dArgs args2d_part(skg_ctx* c, double dt, const Part& p) {
 
 skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     skg::Ns3dArgs a{};
+    a.opt = env_opt();
     a.nx = c->n[0];
     a.ny = c->n[1];
     a.nz = c->n[2];
@@ -374,6 +393,8 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.ystate = a.ny;
     a.kowner = c->d_kowner;
     a.kstart = c->d_cstart;
+    a.slab = 0;
+    a.sz = c->nh;
     return a;
 }
 
@@ -397,6 +418,8 @@ skg::Ns3dArgs args3d_part(skg_ctx* c, double dt, const Part& p) {
     a.nkyl = p.ncols;
     a.nrl = c->nrl;
     a.ystate = p.ncols;
+    a.slab = 1;
+    a.sz = c->kc[2] + 1;
     return a;
 }
 
@@ -503,6 +526,7 @@ int exchange(skg_ctx* c, int which) {
 // block r -> q = rows(r) x lines(q) ([xl][kyl_q][kz_o]).
 int exchange3(skg_ctx* c, int which) {
     const int G = c->G;
+    if (G == 1) return SKG_OK;  // one partition: receive buffers alias the send buffers
     const size_t nrl = (size_t)c->nrl;
     const size_t kz = (size_t)c->kc[2] + 1;  // kz_in = kz_o (pruned)
     auto nl = [&](int q) { return (size_t)(c->cstart[q + 1] - c->cstart[q]); };
@@ -672,22 +696,24 @@ int decide_pruned(skg_ctx* c, const cd* d_ref_layout) {
 // part are at most two runs of global ky (positive, then negative ky).
 int copy_slab3(skg_ctx* c, const Part& p, bool to_part) {
     const int kcy = c->kc[1], ny = c->n[1], nx = c->n[0];
-    const size_t nh = (size_t)c->nh, row = nh * sizeof(cd);
+    const size_t nh = (size_t)c->nh, kzc = (size_t)c->kc[2] + 1;
     const int runs[2][2] = {{0, kcy + 1}, {kcy + 1, 2 * kcy + 1}};  // compact ranges
     for (int b = 0; b < 2; ++b) {
         const int lo = std::max(runs[b][0], p.c0), hi = std::min(runs[b][1], p.c0 + p.ncols);
         if (lo >= hi) continue;
         const int gy = b == 0 ? lo : lo + ny - (2 * kcy + 1);
         for (int v = 0; v < 3; ++v) {
+            // kept kz of lines [gy, gy + hi - lo) for every kx: (kz, line, kx) boxes
             cd* io = c->io + (size_t)v * c->S + (size_t)gy * nh;
-            cd* st = p.u + (size_t)v * p.vs + (size_t)(lo - p.c0) * nh;
-            const size_t io_pitch = (size_t)ny * row, st_pitch = (size_t)p.ncols * row;
-            if (to_part)
-                CUDA_TRY(cudaMemcpy2DAsync(st, st_pitch, io, io_pitch, (hi - lo) * row, nx,
-                                           cudaMemcpyDeviceToDevice, c->stream));
-            else
-                CUDA_TRY(cudaMemcpy2DAsync(io, io_pitch, st, st_pitch, (hi - lo) * row, nx,
-                                           cudaMemcpyDeviceToDevice, c->stream));
+            cd* st = p.u + (size_t)v * p.vs + (size_t)(lo - p.c0) * kzc;
+            cudaPitchedPtr pio = make_cudaPitchedPtr(io, nh * sizeof(cd), kzc * sizeof(cd), ny);
+            cudaPitchedPtr pst = make_cudaPitchedPtr(st, kzc * sizeof(cd), kzc * sizeof(cd), p.ncols);
+            cudaMemcpy3DParms m{};
+            m.srcPtr = to_part ? pio : pst;
+            m.dstPtr = to_part ? pst : pio;
+            m.extent = make_cudaExtent(kzc * sizeof(cd), hi - lo, nx);
+            m.kind = cudaMemcpyDeviceToDevice;
+            CUDA_TRY(cudaMemcpy3DAsync(&m, c->stream));
         }
     }
     return SKG_OK;
@@ -761,6 +787,15 @@ int store_state_to_io(skg_ctx* c, const cd* src) {
     return SKG_OK;
 }
 
+// physical-space and scratch buffers of the transform operators and the
+// grid dump, allocated on first use (the step itself never needs them)
+int ensure_fft_bufs(skg_ctx* c) {
+    if (c->phys && c->work) return SKG_OK;
+    CUDA_TRY(cudaMalloc(&c->phys, sizeof(double) * (size_t)c->P));
+    CUDA_TRY(cudaMalloc(&c->work, sizeof(cd) * (size_t)c->S));
+    return SKG_OK;
+}
+
 struct TwCache {
     std::mutex mu;
     std::map<std::pair<int, int>, cd*> tabs;  // (device, n) -> table
@@ -789,17 +824,18 @@ const char* skg_last_error(void) { return g_err.c_str(); }
 
 static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                        double dealias_coef, double nu, int scheme, int device, int rank, int world,
-                       const char* nccl_id);
+                       const char* nccl_id, bool slab_one);
 
 int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                double dealias_coef, double nu, int scheme, int device) {
-    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, 0, 1, nullptr);
+    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, 0, 1, nullptr, false);
 }
 
 int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                     double dealias_coef, double nu, int scheme, int device, int rank, int world,
                     const char* nccl_id) {
-    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, rank, world, nccl_id);
+    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, rank, world, nccl_id,
+                       world == 1);
 }
 
 int skg_nccl_unique_id(char* out128) {
@@ -813,7 +849,7 @@ int skg_nccl_unique_id(char* out128) {
 
 static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                        double dealias_coef, double nu, int scheme, int device, int rank, int world,
-                       const char* nccl_id) {
+                       const char* nccl_id, bool slab_one) {
     if (!out) return fail(SKG_ECONFIG, "create: null output pointer");
     *out = nullptr;
     std::string s = solver ? solver : "";
@@ -869,6 +905,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         return fail(code, msg);
     };
     if (cudaSetDevice(device) != cudaSuccess) return cleanup(SKG_ECUDA, "cudaSetDevice failed");
+    c->nsm = sm_count(device);
     if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(SKG_ECUDA, "stream creation failed");
     c->stream = c->own;
@@ -878,7 +915,9 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         return cudaMemset(*p, 0, bytes < 16 ? 16 : bytes) == cudaSuccess;
     };
     bool ok = true;
-    c->dist = world > 1;
+    // slab layout: several partitions, or the compact one-partition ns3d
+    // layout requested through skg_create_dist(world = 1)
+    c->dist = world > 1 || (sid == 3 && slab_one);
     c->G = world;
     c->grank = rank;
     if (sid == 2) {  // column partition of the kept ky columns, row partition of x
@@ -913,22 +952,30 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
             cudaMemcpy(c->d_kowner, owner.data(), sizeof(int) * Kyc, cudaMemcpyHostToDevice);
             cudaMemcpy(c->d_cstart, c->cstart.data(), sizeof(int) * (world + 1), cudaMemcpyHostToDevice);
         }
-        const size_t nx = n[0], ny = n[1], nh = c->nh, nrl = c->nrl;
+        // state lines and intermediates hold only the kept kz (slab layouts
+        // need a dealiased state); one partition: no exchange buffers
+        const size_t nx = n[0], ny = n[1], kzc = (size_t)c->kc[2] + 1, nrl = c->nrl;
         for (int q = 0; q < world; ++q) {
             if (nccl_id && q != rank) continue;
             Part p;
             p.r = q;
             p.c0 = c->cstart[q];
             p.ncols = c->cstart[q + 1] - c->cstart[q];
-            p.vs = nx * p.ncols * nh;
-            p.fs = std::max(p.vs, nrl * ny * nh);
-            p.rfs = nrl * Kyc * nh;
+            p.vs = nx * p.ncols * kzc;
+            p.fs = std::max(p.vs, nrl * ny * kzc);
+            p.rfs = nrl * Kyc * kzc;
             ok = ok && alloc((void**)&p.u, sizeof(cd) * 3 * p.vs);
             for (int i = 0; i < 3; ++i) ok = ok && alloc((void**)&p.k[i], sizeof(cd) * 3 * p.vs);
             ok = ok && alloc((void**)&p.A3, sizeof(cd) * 5 * p.fs);
             ok = ok && alloc((void**)&p.B3, sizeof(cd) * 6 * p.fs);
-            ok = ok && alloc((void**)&p.rA3, sizeof(cd) * 5 * p.rfs);
-            ok = ok && alloc((void**)&p.sD3, sizeof(cd) * 3 * p.rfs);
+            if (world > 1) {
+                ok = ok && alloc((void**)&p.rA3, sizeof(cd) * 5 * p.rfs);
+                ok = ok && alloc((void**)&p.sD3, sizeof(cd) * 3 * p.rfs);
+            } else {
+                p.rA3 = p.A3;
+                p.rfs = p.fs;
+                p.sD3 = p.B3;
+            }
             c->parts.push_back(p);
         }
         if (ok && nccl_id) {
@@ -972,8 +1019,6 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
     }
     ok = ok && alloc((void**)&c->io, sizeof(cd) * S * c->nvars);
-    ok = ok && alloc((void**)&c->phys, sizeof(double) * (size_t)c->P);
-    ok = ok && alloc((void**)&c->work, sizeof(cd) * S);
     int ext_total = 0;
     for (int d = 0; d < dims; ++d) ext_total += d == dims - 1 ? c->nh : n[d];
     ok = ok && alloc((void**)&c->etab, sizeof(double) * 2 * ext_total);
@@ -1018,10 +1063,10 @@ int skg_destroy(skg_ctx* c) {
             cudaFree(p.sA[f]);
             cudaFree(p.rA[f]);
         }
+        if (p.rA3 != p.A3) cudaFree(p.rA3);
+        if (p.sD3 != p.B3) cudaFree(p.sD3);
         cudaFree(p.A3);
         cudaFree(p.B3);
-        cudaFree(p.rA3);
-        cudaFree(p.sD3);
     }
     cudaFree(c->cmfull);
     cudaFree(c->d_kowner);
@@ -1179,6 +1224,7 @@ int skg_tendency(skg_ctx* c, const double* in, double* out) {
 
 int skg_fft_forward(skg_ctx* c, const double* u, double* uhat) {
     CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_fft_bufs(c)) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->phys, u, sizeof(double) * c->P, cudaMemcpyHostToDevice, c->stream));
     const cd* tw[3] = {c->tw[0], c->tw[1], c->tw[2]};
     CUDA_TRY(skg::fft_forward_dev(c->dims, c->n, c->phys, c->io, c->work, tw, c->stream, &c->launches));
@@ -1189,6 +1235,7 @@ int skg_fft_forward(skg_ctx* c, const double* u, double* uhat) {
 
 int skg_fft_inverse(skg_ctx* c, const double* uhat, double* u) {
     CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_fft_bufs(c)) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->io, uhat, sizeof(cd) * c->S, cudaMemcpyHostToDevice, c->stream));
     const cd* tw[3] = {c->tw[0], c->tw[1], c->tw[2]};
     CUDA_TRY(skg::fft_inverse_dev(c->dims, c->n, c->io, c->phys, c->work, tw, c->stream, &c->launches));
@@ -1258,6 +1305,7 @@ int skg_plan_inverse(int rank, const int* shape, const double* uhat, double* u, 
 int skg_get_grid(skg_ctx* c, int axis, double* k_axis, unsigned char* mask) {
     if (axis < 0 || axis >= c->dims) return fail(SKG_ESHAPE, "axis out of range");
     CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_fft_bufs(c)) return rc;
     double* dk = reinterpret_cast<double*>(c->work);  // >= nh doubles
     unsigned char* dm = mask ? reinterpret_cast<unsigned char*>(c->io) : nullptr;
     CUDA_TRY(skg::launch_grid_dump(c->dims, c->n, c->kc, c->kscale, axis, dk, dm, c->stream, &c->launches));

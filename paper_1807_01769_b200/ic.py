@@ -145,3 +145,29 @@ def cfl_dt(solver, n, state, cfl=0.5, dt_max=0.1):
         vel = max(float(np.abs(u).max()), 1e-30)
         dt = min(dt, cfl * (K_TWO_PI / n[a]) / vel)
     return dt
+
+
+def embed(v, n):
+    """Spectral embedding of a dealiased half-spectrum state v (vars, n0, ..,
+    n_last//2+1) of a coarser grid into grid n: the same modes (same signed
+    indices) with zeros elsewhere.  The physical field is the same
+    band-limited function sampled finer (1/N-forward convention), so the
+    BASELINE recipe at a large n is generated at a coarse grid holding all of
+    its spectral energy (E(k) ~ k^4 exp(-2 (k/k0)^2) is below 1e-200 of its
+    peak beyond |k| = 64) and embedded."""
+    small = v.shape[1:-1] + (2 * (v.shape[-1] - 1),)
+    d = len(n)
+    out = np.zeros((v.shape[0],) + tuple(n[:-1]) + (n[-1] // 2 + 1,), np.complex128)
+    idx = []
+    for a in range(d - 1):
+        i = np.arange(small[a])
+        si = np.where(i <= small[a] // 2, i, i - small[a])
+        keep = np.abs(si) < small[a] // 2          # the coarse Nyquist is masked anyway
+        idx.append((i[keep], np.where(si[keep] >= 0, si[keep], si[keep] + n[a])))
+    kz = small[-1] // 2                            # coarse Nyquist plane excluded
+    if d == 2:
+        out[:, idx[0][1][:, None], np.arange(kz)[None, :]] = v[:, idx[0][0][:, None], np.arange(kz)[None, :]]
+    else:
+        src = v[:, idx[0][0]][:, :, idx[1][0], :kz]
+        out[:, idx[0][1][:, None], idx[1][1][None, :], :kz] = src
+    return out

@@ -116,3 +116,30 @@ def test_slab_run_series():
     d.set_state(u0)
     a, b = d.run(5), one.run(5)
     assert np.allclose(a, b, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("n", [(32, 32, 32), (64, 32, 16), (16, 64, 128), (128, 128, 128)])
+def test_compact_layout_matches_full(n):
+    """ns3d compact single-GPU layout (skg_create_dist, world 1)."""
+    u0 = ic.ns3d_ic(n, seed=11)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    one = api.Simulation("ns3d", n, 1e-3, dt)
+    one.set_state(u0)
+    c = api.Simulation("ns3d", n, 1e-3, dt, compact=True)
+    c.set_state(u0)
+    a, b = c.run(3), one.run(3)
+    assert np.allclose(a, b, rtol=1e-12, atol=0)
+    s, r = c.get_state(), one.get_state()
+    for v in range(3):
+        assert O.rel_l2(s[v], r[v]) < 1e-14
+    mask = O.dealias_mask(n).astype(bool)
+    assert np.all(s[:, ~mask] == 0)
+
+
+def test_compact_layout_rejects_undealiased_state():
+    n = (16, 16, 16)
+    rng = np.random.default_rng(2)
+    v = np.stack([O.forward(rng.standard_normal(n)) for _ in range(3)])
+    c = api.Simulation("ns3d", n, 1e-3, 1e-3, compact=True)
+    with pytest.raises(api.UnsupportedError):
+        c.set_state(v)
