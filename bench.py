@@ -232,7 +232,8 @@ def run_our_arm(args):
         dist.broadcast_object_list(obj, src=0)
         sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
     else:
-        sim = api.Simulation(solver, n, nu, dt, device=local, compact=args.config in COARSE_IC)
+        compact = args.layout == "compact" or (args.layout == "auto" and args.config in COARSE_IC)
+        sim = api.Simulation(solver, n, nu, dt, device=local, compact=compact)
     # a dedicated (non-default) stream: the library launches on it and the
     # CUDA events below are recorded on the same stream
     stream = torch.cuda.Stream(device=local)
@@ -402,6 +403,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--instrumented-steps", type=int, default=20)
+    ap.add_argument("--layout", choices=["auto", "full", "compact"], default="auto",
+                    help="ns3d one-GPU layout (auto: compact where the full layout does not fit)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

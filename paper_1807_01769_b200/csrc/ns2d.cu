@@ -466,8 +466,12 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     auto issue = [&](int x) {
         if (x >= a.nrl) return;
         for (int i = t; i < a.ky_in; i += T) {
-            const int ro = a.kowner[i];
-            const int cs = a.cstart[ro], nc = a.cstart[ro + 1] - cs;
+            // owner of column i under cstart[q] = 2 floor(q PP / G), PP kept
+            // column pairs (skgpu.cu create_impl), computed instead of loaded
+            const int PP = (a.ky_in + 1) >> 1;
+            const int ro = (((i >> 1) + 1) * a.G - 1) / PP;
+            const int cs = 2 * (ro * PP / a.G);
+            const int nc = (ro == a.G - 1 ? a.ky_in : 2 * ((ro + 1) * PP / a.G)) - cs;
             const size_t q = (size_t)a.nrl * cs + ((size_t)(x / RG) * nc + (i - cs)) * RG + (x % RG);
             cp_async16(&st[i], P + q);
             cp_async16(&st[ld + i], Q + q);

@@ -61,6 +61,24 @@ __device__ __forceinline__ size_t sidx(const Ns3dArgs& a, int kx, int ys, int kz
     return ((size_t)kx * a.ystate + ys) * a.sz + kz;
 }
 
+// Owner rank, first line and line count of compact kept line kyi under the
+// partition kstart[q] = q K / G (K = 2 kcy + 1 kept lines; skgpu.cu
+// create_impl), computed instead of loaded: q = ((kyi + 1) G - 1) / K.
+__device__ __forceinline__ void line_owner(const Ns3dArgs& a, int kyi, int& q, int& ks, int& nk) {
+    const int K = 2 * a.kcy + 1;
+    q = ((kyi + 1) * a.G - 1) / K;
+    ks = q * K / a.G;
+    nk = (q + 1) * K / a.G - ks;
+}
+
+// Per-CTA table (shared memory) of the offset of line j (fixed x row) in the
+// x-pass buffer read by k2 / written by k2f, for kz stride kzs; -1 where the
+// line is masked.  Full layout: (x ny + j) kzs; slab layout: the owner's
+// block [xl][kyl][kz] (line_owner), computed once per CTA instead of per
+// element and field.
+template <int NY>
+__device__ __forceinline__ void line_offsets(const Ns3dArgs& a, int x, int kzs, int* off);
+
 // compact kept index of a kept ky (0..kcy, then ny-kcy..ny-1)
 __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
     return ky <= a.kcy ? ky : ky - (a.ny - (2 * a.kcy + 1));
@@ -85,11 +103,12 @@ __device__ __forceinline__ cd stage_input3(const Ns3dArgs& a, int stage, int c, 
 }
 
 // Lines per CTA for the strided passes: lanes walk the contiguous kz axis.
-template <int N>
+template <int N, int CT = 256>
 struct Strided {
     using F = BFFT<N>;
     static constexpr int T = F::T;
-    static constexpr int C = T >= 256 ? 1 : 256 / T;
+    static constexpr int C = T >= CT ? 1 : CT / T;
+    static constexpr int MINB = T * C > 256 ? 1 : 2;  // CTAs per SM
 };
 
 // ------------------------------------------------------------------ x-inverse
@@ -97,10 +116,10 @@ struct Strided {
 // streamed into shared memory with cp.async) and kept in thread-private
 // slots for its one or two FFTs.  PZ: dealiased state with kcx < 6T, so the
 // per-thread elements e in [6, 10) are zero and need no slot.
-template <int NX, bool PZ>
-__global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
+template <int NX, bool PZ, int CB = 256>
+__global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, int stage) {
     using F = BFFT<NX>;
-    constexpr int T = F::T, E = F::E, C = Strided<NX>::C;
+    constexpr int T = F::T, E = F::E, C = Strided<NX, CB>::C;
     constexpr int ZLO = PZ ? 6 : E, ZHI = PZ ? 10 : E;
     constexpr int CT = T * C;  // threads per CTA
     extern __shared__ cd smem[];
@@ -173,11 +192,31 @@ __global__ void __launch_bounds__(256, 2) k1_3d(Ns3dArgs a, int stage) {
     }
 }
 
-// ------------------------------------------------------------------ y-inverse
 template <int NY>
-__global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
+__device__ __forceinline__ void line_offsets(const Ns3dArgs& a, int x, int kzs, int* off) {
+    for (int j = threadIdx.x; j < NY; j += blockDim.x) {
+        const int sj = signed_index(j, NY);
+        int o = -1;
+        if (!a.pruned || abs(sj) <= a.kcy) {
+            if (!a.slab) {
+                o = (x * a.ny + j) * kzs;
+            } else {
+                const int kyi = ky_compact(a, j);
+                int q, ks, nk;
+                line_owner(a, kyi, q, ks, nk);
+                o = a.nrl * ks * kzs + (x * nk + (kyi - ks)) * kzs;
+            }
+        }
+        off[j] = o;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ y-inverse
+template <int NY, int CT = 256>
+__global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
     using F = BFFT<NY>;
-    constexpr int T = F::T, E = F::E, C = Strided<NY>::C;
+    constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_in + C - 1) / C;
@@ -196,6 +235,8 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
     const cd* A2 = Ab + 2 * afs;
     const cd* A3 = Ab + 3 * afs;
     const cd* A4 = Ab + 4 * afs;
+    int* loff = reinterpret_cast<int*>(smem + C * F::SMEM);
+    line_offsets<NY>(a, x, a.kz_in, loff);
 #pragma unroll 1
     for (int m = 0; m < 6; ++m) {
         cd v[E];
@@ -203,18 +244,10 @@ __global__ void __launch_bounds__(256, 2) k2_3d(Ns3dArgs a) {
         for (int e = 0; e < E; ++e) {
             const int j = t + T * e;
             const int sj = signed_index(j, NY);
-            const bool keep = active && (!a.pruned || abs(sj) <= a.kcy);
+            const int lo = loff[j];
             cd r = zero();
-            if (keep) {
-                size_t q;
-                if (!a.slab) {
-                    q = ((size_t)x * a.ny + j) * a.kz_in + kz;
-                } else {  // receive block of the line's owner, layout [xl][kyl][kz]
-                    const int kyi = ky_compact(a, j);
-                    const int ro = a.kowner[kyi];
-                    const int ks = a.kstart[ro], nk = a.kstart[ro + 1] - ks;
-                    q = (size_t)a.nrl * ks * a.kz_in + ((size_t)x * nk + (kyi - ks)) * a.kz_in + kz;
-                }
+            if (active && lo >= 0) {
+                const size_t q = (size_t)lo + kz;
                 const double kyv = a.ky_scale * (double)sj;
                 switch (m) {
                     case 0: r = A0[q]; break;  // vx
@@ -399,10 +432,10 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
 }
 
 // ------------------------------------------------------------------ y-forward
-template <int NY>
-__global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
+template <int NY, int CT = 256>
+__global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) {
     using F = BFFT<NY>;
-    constexpr int T = F::T, E = F::E, C = Strided<NY>::C;
+    constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_o + C - 1) / C;
@@ -413,6 +446,8 @@ __global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
+    int* loff = reinterpret_cast<int*>(smem + C * F::SMEM);
+    line_offsets<NY>(a, x, a.kz_o, loff);
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
         const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
@@ -426,16 +461,9 @@ __global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
                              : a.B + m * a.fstride;  // D fields live in B's memory
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                const int j = t + T * e;
-                if (abs(signed_index(j, NY)) > a.kcy) continue;  // masked: never read
-                if (!a.slab) {
-                    out[((size_t)x * a.ny + j) * a.kz_o + kz] = v[e];
-                } else {  // send block of the line's owner q, layout [xl][kyl_q][kz]
-                    const int kyi = ky_compact(a, j);
-                    const int q = a.kowner[kyi];
-                    const int ks = a.kstart[q], nk = a.kstart[q + 1] - ks;
-                    out[(size_t)a.nrl * ks * a.kz_o + ((size_t)x * nk + (kyi - ks)) * a.kz_o + kz] = v[e];
-                }
+                const int lo = loff[t + T * e];
+                if (lo >= 0 && abs(signed_index(t + T * e, NY)) <= a.kcy)  // masked: never read
+                    out[(size_t)lo + kz] = v[e];
             }
         }
     }
@@ -445,10 +473,10 @@ __global__ void __launch_bounds__(256, 2) k2f_3d(Ns3dArgs a) {
 // Components 0 and 1 are written back raw into their own D lines (in place,
 // L2-resident) and re-read by the same thread for the projection, so no
 // shared-memory slots are needed.
-template <int NX>
-__global__ void __launch_bounds__(256, 2) k4_3d(Ns3dArgs a, int stage) {
+template <int NX, int CT = 256>
+__global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, int stage) {
     using F = BFFT<NX>;
-    constexpr int T = F::T, E = F::E, C = Strided<NX>::C;
+    constexpr int T = F::T, E = F::E, C = Strided<NX, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_o + C - 1) / C;
@@ -610,9 +638,9 @@ void set_smem(K kernel, size_t bytes, size_t& done) {
     }
 }
 
-template <int NX>
-cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
-    constexpr int C = Strided<NX>::C;
+template <int NX, int CT>
+cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    constexpr int C = Strided<NX, CT>::C;
     using F = BFFT<NX>;
     if (inverse) {
         const int grid = a.nkyl * ((a.kz_in + C - 1) / C);
@@ -621,42 +649,60 @@ cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s
             if constexpr (NX >= 64) {
                 const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - 4) * F::T * C);
                 static size_t done = 0;
-                set_smem(k1_3d<NX, true>, smem, done);
-                k1_3d<NX, true><<<grid, F::T * C, smem, s>>>(a, stage);
+                set_smem(k1_3d<NX, true, CT>, smem, done);
+                k1_3d<NX, true, CT><<<grid, F::T * C, smem, s>>>(a, stage);
             }
         } else {
-            const size_t smem = sizeof(cd) * (F::SMEM * C + F::E * F::T * C);
-            static size_t done = 0;
-            set_smem(k1_3d<NX, false>, smem, done);
-            k1_3d<NX, false><<<grid, F::T * C, smem, s>>>(a, stage);
+            if constexpr (CT == 256) {
+                const size_t smem = sizeof(cd) * (F::SMEM * C + F::E * F::T * C);
+                static size_t done = 0;
+                set_smem(k1_3d<NX, false>, smem, done);
+                k1_3d<NX, false><<<grid, F::T * C, smem, s>>>(a, stage);
+            } else {
+                return launch_x3_v<NX, 256>(a, stage, inverse, s);
+            }
         }
     } else {
         const size_t smem = sizeof(cd) * F::SMEM * C;
         static size_t done = 0;
-        set_smem(k4_3d<NX>, smem, done);
+        set_smem(k4_3d<NX, CT>, smem, done);
         const int grid = a.nkyl * ((a.kz_o + C - 1) / C);
-        k4_3d<NX><<<grid, F::T * C, smem, s>>>(a, stage);
+        k4_3d<NX, CT><<<grid, F::T * C, smem, s>>>(a, stage);
     }
     return cudaGetLastError();
 }
 
-template <int NY>
-cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
-    constexpr int C = Strided<NY>::C;
+// opt 128: 512-thread CTAs for the x passes (2x wider kz chunks)
+template <int NX>
+cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    if (a.opt & 128) return launch_x3_v<NX, 512>(a, stage, inverse, s);
+    return launch_x3_v<NX, 256>(a, stage, inverse, s);
+}
+
+template <int NY, int CT>
+cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
+    constexpr int C = Strided<NY, CT>::C;
     using F = BFFT<NY>;
-    const size_t smem = sizeof(cd) * F::SMEM * C;
+    const size_t smem = sizeof(cd) * F::SMEM * C + sizeof(int) * NY;  // + line offsets
     if (inverse) {
         static size_t done = 0;
-        set_smem(k2_3d<NY>, smem, done);
+        set_smem(k2_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        k2_3d<NY><<<grid, F::T * C, smem, s>>>(a);
+        k2_3d<NY, CT><<<grid, F::T * C, smem, s>>>(a);
     } else {
         static size_t done = 0;
-        set_smem(k2f_3d<NY>, smem, done);
+        set_smem(k2f_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_o + C - 1) / C);
-        k2f_3d<NY><<<grid, F::T * C, smem, s>>>(a);
+        k2f_3d<NY, CT><<<grid, F::T * C, smem, s>>>(a);
     }
     return cudaGetLastError();
+}
+
+// opt 64: 512-thread CTAs for the y passes
+template <int NY>
+cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
+    if (a.opt & 64) return launch_y3_v<NY, 512>(a, inverse, s);
+    return launch_y3_v<NY, 256>(a, inverse, s);
 }
 
 template <int NZ, bool PF>

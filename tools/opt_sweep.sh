@@ -1,8 +1,9 @@
 #!/bin/bash
 # usage: opt_sweep.sh config opts...
 cfg=$1; shift
+extra=${EXTRA:-}
 for o in "$@"; do
-  SKG_OPT=$o timeout 300 python bench.py --config $cfg --steps 60 --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/sw_${cfg}_$o.log 2>&1
+  SKG_OPT=$o timeout 300 python bench.py --config $cfg --steps 60 --warmup 5 --no-cpu-baseline --e2e-steps 2 $extra > gpurun_out/sw_${cfg}_$o.log 2>&1
   python - "$o" gpurun_out/sw_${cfg}_$o.log <<'PY'
 import json,sys
 try:
