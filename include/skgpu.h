@@ -106,6 +106,21 @@ int skg_get_state_device(skg_ctx* ctx, double* d_spect_out);
  * tendency of the solver, check_finite after every step.  Blocking; returns
  * SKG_EDIVERGENCE with the state frozen after the first non-finite step
  * (see skg_last_divergence). */
+/*
+ * Adaptive time step (Simulation::compute_dt with fixed_dt = 0,
+ * simulation.cpp:463-476): dt = min(dt_max, cfl_coef * min_d dx_d / max|u_d|)
+ * per step, clamped to t_end (t_end < 0: no clamp), computed on the device
+ * from the max |u_d| of the step's initial state, reduced inside the
+ * stage-1 physical pass (no extra transforms).  While enabled, the dt
+ * argument of skg_step / skg_step_async / skg_run is ignored; a step whose dt
+ * would be <= 0 fails with SKG_ECONFIG ("past t_end") without running.
+ * cfl_coef <= 0 returns to the caller's fixed dt.  skg_last_dt = the dt of
+ * the last completed step; skg_set_time sets t (restart).
+ */
+int skg_set_cfl(skg_ctx* ctx, double cfl_coef, double dt_max, double t_end);
+double skg_last_dt(const skg_ctx* ctx);
+int skg_set_time(skg_ctx* ctx, double t);
+
 int skg_step(skg_ctx* ctx, double dt, long nsteps);
 /* Same, enqueued on the context stream without waiting; skg_sync() waits
  * and reports divergence. */

@@ -33,6 +33,7 @@ EXPORTS = [
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
+    "skg_set_cfl", "skg_last_dt", "skg_set_time",
 ]
 
 
@@ -111,6 +112,10 @@ def load_library():
     L.skg_set_timing.argtypes = [vp, C.c_int]
     L.skg_kernel_stats.argtypes = [vp, C.c_int, dp, C.POINTER(C.c_long), dp]
     L.skg_reset_stats.argtypes = [vp]
+    L.skg_set_cfl.argtypes = [vp, C.c_double, C.c_double, C.c_double]
+    L.skg_last_dt.argtypes = [vp]
+    L.skg_last_dt.restype = C.c_double
+    L.skg_set_time.argtypes = [vp, C.c_double]
     _lib = L
     return L
 
@@ -281,6 +286,21 @@ class Simulation:
     # ---------------------------------------------------------------- stepping
     def step_once(self, dt: float | None = None) -> None:
         self.step(1, dt)
+
+    def set_cfl(self, cfl_coef: float = 0.5, dt_max: float = 0.1, t_end: float | None = None) -> None:
+        """Adaptive dt as the reference's time_stepping with fixed_dt = 0
+        (compute_dt, simulation.cpp:463-476): per step
+        dt = min(dt_max, cfl_coef * min_d dx_d / max|u_d|), clamped to t_end;
+        computed on the device.  cfl_coef <= 0 returns to the fixed dt."""
+        self._call("skg_set_cfl", C.c_double(cfl_coef), C.c_double(dt_max),
+                   C.c_double(-1.0 if t_end is None else float(t_end)))
+
+    @property
+    def last_dt(self) -> float:
+        return load_library().skg_last_dt(self._h)
+
+    def set_time(self, t: float) -> None:
+        self._call("skg_set_time", C.c_double(t))
 
     def step(self, nsteps: int, dt: float | None = None) -> None:
         dt = self.dt if dt is None else float(dt)

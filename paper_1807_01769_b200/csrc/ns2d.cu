@@ -76,21 +76,21 @@ __device__ __forceinline__ cd stage_input(const Ns2dArgs& a, int stage, int ky, 
         if (stage == 2) {
             const double e1 = a.e1x[i] * a.e1y[ky];
             cd k = a.k1[idx];
-            return scale(add(u, scale(k, a.hdt)), e1);
+            return scale(add(u, scale(k, hdt_of(a))), e1);
         } else if (stage == 3) {
             const double e1 = a.e1x[i] * a.e1y[ky];
             cd k = a.k2[idx];
-            return add(scale(u, e1), scale(k, a.hdt));
+            return add(scale(u, e1), scale(k, hdt_of(a)));
         } else {
             const double e1 = a.e1x[i] * a.e1y[ky];
             const double e2 = a.e2x[i] * a.e2y[ky];
             cd k = a.k3[idx];
-            return add(scale(u, e2), scale(k, a.dt * e1));
+            return add(scale(u, e2), scale(k, dt_of(a) * e1));
         }
     } else {
-        if (stage == 2) return add(u, scale(a.k1[idx], a.hdt));
-        if (stage == 3) return add(u, scale(a.k2[idx], a.hdt));
-        return add(u, scale(a.k3[idx], a.dt));
+        if (stage == 2) return add(u, scale(a.k1[idx], hdt_of(a)));
+        if (stage == 3) return add(u, scale(a.k2[idx], hdt_of(a)));
+        return add(u, scale(a.k3[idx], dt_of(a)));
     }
 }
 
@@ -99,12 +99,12 @@ __device__ __forceinline__ cd stage_combine(const Ns2dArgs& a, int stage, int ky
     if (stage <= 1) return u;
     if (a.has_sigma) {
         const double e1 = a.e1x[i] * a.e1y[ky];
-        if (stage == 2) return scale(add(u, scale(k, a.hdt)), e1);
-        if (stage == 3) return add(scale(u, e1), scale(k, a.hdt));
+        if (stage == 2) return scale(add(u, scale(k, hdt_of(a))), e1);
+        if (stage == 3) return add(scale(u, e1), scale(k, hdt_of(a)));
         const double e2 = a.e2x[i] * a.e2y[ky];
-        return add(scale(u, e2), scale(k, a.dt * e1));
+        return add(scale(u, e2), scale(k, dt_of(a) * e1));
     }
-    return add(u, scale(k, stage == 4 ? a.dt : a.hdt));
+    return add(u, scale(k, stage == 4 ? dt_of(a) : hdt_of(a)));
 }
 
 // PZ: the state is dealiased and the kept |kx| <= kcx < 6T, so the elements
@@ -267,6 +267,8 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     };
     issue(0);
     cp_async_commit();
+    const bool cfl = a.dyn && a.ystage == 1;
+    double mx = 0.0, my = 0.0;
     double acc[E];
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
@@ -303,6 +305,13 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
         if (k < 3) issue(k + 1);
         cp_async_commit();
         F::template run<+1>(v, sm, t, wb);
+        if (cfl) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (q == 0) mx = fmax(mx, fabs(v[e].x));
+                else my = fmax(my, fabs(v[e].x));
+            }
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const double p = v[e].x * v[e].y;  // ux dx w | uy dy w
@@ -315,6 +324,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
             }
         }
     }
+    if (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
     // forward r2c of both rows packed: z = prod_a + i prod_b
     cd v[E];
 #pragma unroll
@@ -375,19 +385,19 @@ __global__ void __launch_bounds__(256, 2) k4_xfwd(Ns2dArgs a, int stage) {
                 const double e1 = a.e1x[i] * a.e1y[ky];
                 const double e2 = a.e2x[i] * a.e2y[ky];
                 if (a.rk2) {
-                    un = add(scale(u, e2), scale(kv, a.dt * e1));
+                    un = add(scale(u, e2), scale(kv, dt_of(a) * e1));
                 } else {
                     cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
                     cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
-                    un = add(scale(u, e2), scale(sum, a.sdt));
+                    un = add(scale(u, e2), scale(sum, sdt_of(a)));
                 }
             } else {
                 cd delta;
                 if (a.rk2) {
-                    delta = scale(kv, a.dt);
+                    delta = scale(kv, dt_of(a));
                 } else {
                     cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), sdt_of(a));
                 }
                 un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
             }
@@ -481,6 +491,8 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     issue(x);
     cp_async_commit();
     const double h = 0.5 * a.inv_n;
+    const bool cfl = a.dyn && a.ystage == 1;  // max |u_d| of the step's initial state
+    double mx = 0.0, my = 0.0;
     // every group runs the same number of iterations (barriers inside)
     const int iters = (a.nrl + stride - 1) / stride;
 #pragma unroll 1
@@ -512,6 +524,13 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
         issue(x + stride);
         cp_async_commit();
         F::template run<+1>(v, sm, t, wb);  // u + i v on the row
+        if (cfl) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                mx = fmax(mx, fabs(v[e].x));
+                my = fmax(my, fabs(v[e].y));
+            }
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const double u = v[e].x, w = v[e].y;
@@ -530,6 +549,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
             }
         }
     }
+    if (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
 }
 
 // x-forward of the two product spectra per kept ky column, combination
@@ -627,19 +647,19 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
                 const double e1 = a.e1x[i] * a.e1y[ky];
                 const double e2 = a.e2x[i] * a.e2y[ky];
                 if (a.rk2) {
-                    un = add(scale(u, e2), scale(kv, a.dt * e1));
+                    un = add(scale(u, e2), scale(kv, dt_of(a) * e1));
                 } else {
                     const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
                     const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
-                    un = add(scale(u, e2), scale(sum, a.sdt));
+                    un = add(scale(u, e2), scale(sum, sdt_of(a)));
                 }
             } else {
                 cd delta;
                 if (a.rk2) {
-                    delta = scale(kv, a.dt);
+                    delta = scale(kv, dt_of(a));
                 } else {
                     const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), sdt_of(a));
                 }
                 un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
             }
@@ -843,7 +863,9 @@ cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t 
         hook.end(0, B * (kept * (stage == 1 ? 1.0 : 2.0) + 2.0 * a.nx * a.ncols));
     } else if (pass == 1) {
         hook.begin(1);
-        err = dispatch_fast_y(a, s);
+        Ns2dArgs b = a;
+        b.ystage = stage;
+        err = dispatch_fast_y(b, s);
         hook.end(1, B * (4.0 * a.nrl * Kc));
     } else {
         hook.begin(2);
@@ -873,7 +895,9 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
     if ((err = dispatch_x(a, stage, true, s)) != cudaSuccess) return err;
     hook.end(0, B * (s_in * (stage == 1 ? 1.0 : 2.0) + 4.0 * inter));
     hook.begin(1);
-    if ((err = dispatch_y(a, s)) != cudaSuccess) return err;
+    Ns2dArgs b = a;
+    b.ystage = stage;
+    if ((err = dispatch_y(b, s)) != cudaSuccess) return err;
     hook.end(1, B * (4.0 * inter + rows));
     hook.begin(2);
     if ((err = dispatch_x(a, stage, false, s)) != cudaSuccess) return err;

@@ -42,12 +42,12 @@ __device__ __forceinline__ cd stage_combine3(const Ns3dArgs& a, int stage, int i
     if (stage <= 1) return u;
     if (a.has_sigma) {
         const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
-        if (stage == 2) return scale(add(u, scale(k, a.hdt)), e1);
-        if (stage == 3) return add(scale(u, e1), scale(k, a.hdt));
+        if (stage == 2) return scale(add(u, scale(k, hdt_of(a))), e1);
+        if (stage == 3) return add(scale(u, e1), scale(k, hdt_of(a)));
         const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
-        return add(scale(u, e2), scale(k, a.dt * e1));
+        return add(scale(u, e2), scale(k, dt_of(a) * e1));
     }
-    return add(u, scale(k, stage == 4 ? a.dt : a.hdt));
+    return add(u, scale(k, stage == 4 ? dt_of(a) : hdt_of(a)));
 }
 
 // ky of the kyi-th processed line of the x passes.
@@ -92,14 +92,14 @@ __device__ __forceinline__ cd stage_input3(const Ns3dArgs& a, int stage, int c, 
     if (stage <= 1) return u;
     if (a.has_sigma) {
         const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
-        if (stage == 2) return scale(add(u, scale(a.k1[idx], a.hdt)), e1);
-        if (stage == 3) return add(scale(u, e1), scale(a.k2[idx], a.hdt));
+        if (stage == 2) return scale(add(u, scale(a.k1[idx], hdt_of(a))), e1);
+        if (stage == 3) return add(scale(u, e1), scale(a.k2[idx], hdt_of(a)));
         const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
-        return add(scale(u, e2), scale(a.k3[idx], a.dt * e1));
+        return add(scale(u, e2), scale(a.k3[idx], dt_of(a) * e1));
     }
-    if (stage == 2) return add(u, scale(a.k1[idx], a.hdt));
-    if (stage == 3) return add(u, scale(a.k2[idx], a.hdt));
-    return add(u, scale(a.k3[idx], a.dt));
+    if (stage == 2) return add(u, scale(a.k1[idx], hdt_of(a)));
+    if (stage == 3) return add(u, scale(a.k2[idx], hdt_of(a)));
+    return add(u, scale(a.k3[idx], dt_of(a)));
 }
 
 // Lines per CTA for the strided passes: lanes walk the contiguous kz axis.
@@ -279,6 +279,84 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
     }
 }
 
+// Staged variant (dealiased states): the kept lines of the next output's
+// primary field stream into shared memory (cp.async, compact kept-line
+// index) while the current FFT runs; the secondary field of the three
+// vorticity outputs is read directly (recently read by this CTA: L2).
+// Output m: primary / secondary = A0 / -, A1 / -, A2 / -, A2 / A1, A4 / A0,
+// A3 / A0.
+template <int NY>
+__global__ void __launch_bounds__(256, 2) k2s_3d(Ns3dArgs a) {
+    using F = BFFT<NY>;
+    constexpr int T = F::T, E = F::E, C = Strided<NY>::C;
+    extern __shared__ cd smem[];
+    const int l = threadIdx.x % C, t = threadIdx.x / C;
+    const int nkzb = (a.kz_in + C - 1) / C;
+    const int x = blockIdx.x / nkzb;
+    const int kz0 = (blockIdx.x % nkzb) * C;
+    const int kz = kz0 + l;
+    const bool active = kz < a.kz_in;
+    if (a.flags->diverged) return;
+    const int K = 2 * a.kcy + 1;  // kept lines
+    cd* sm = smem + l * F::SMEM;
+    cd* stg = smem + C * F::SMEM;                       // [kyi][l]
+    int* loff = reinterpret_cast<int*>(stg + (size_t)K * C);
+    const int salt = l & 7;
+    const typename F::Bases wb = F::bases(t, a.twy);
+    const double kzv = a.kz_scale * (double)kz;
+    const cd* Ab = a.slab ? a.rA : a.A;
+    const size_t afs = a.slab ? a.rfs : a.fstride;
+    line_offsets<NY>(a, x, a.kz_in, loff);
+    const int nl = a.kz_in - kz0 < C ? a.kz_in - kz0 : C;  // active lanes
+    auto issue = [&](int f) {
+        const cd* src = Ab + (size_t)f * afs + kz0;
+        for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
+            const int kyi = i / C, ll = i % C;
+            if (ll >= nl) continue;
+            const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
+            cp_async16(&stg[i], src + loff[j] + ll);
+        }
+        cp_async_commit();
+    };
+    issue(0);
+#pragma unroll 1
+    for (int m = 0; m < 6; ++m) {
+        cp_async_wait_all();
+        __syncthreads();
+        const cd* sec = Ab + (size_t)(m == 3 ? 1 : 0) * afs;
+        cd v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int j = t + T * e;
+            const int sj = signed_index(j, NY);
+            cd r = zero();
+            if (active && abs(sj) <= a.kcy) {
+                const int kyi = sj >= 0 ? sj : sj + K;
+                const cd p = stg[kyi * C + l];
+                const double kyv = a.ky_scale * (double)sj;
+                if (m < 3) {
+                    r = p;
+                } else {
+                    const cd q = sec[(size_t)loff[j] + kz];
+                    if (m == 3) r = muli(sub(scale(p, kyv), scale(q, kzv)));  // wx = i (ky vz - kz vy)
+                    else if (m == 4) r = muli(sub(scale(q, kzv), p));         // wy = i (kz vx - kx vz)
+                    else r = muli(sub(p, scale(q, kyv)));                     // wz = i (kx vy - ky vx)
+                }
+            }
+            v[e] = r;
+        }
+        __syncthreads();  // stage consumed
+        if (m < 5) issue(m == 2 ? 2 : m == 3 ? 4 : m == 4 ? 3 : m + 1);  // primary of m + 1
+        F::template run<+1>(v, sm, t, wb, salt);
+        if (active) {
+            cd* out = a.B + m * a.fstride;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                out[((size_t)x * a.ny + (t + T * e)) * a.kz_in + kz] = v[e];
+        }
+    }
+}
+
 // ------------------------------------------------------------------ z pass
 // Per group: one row pair (r, r+1) of (x, y) rows along z.
 // 8 elements per thread (twice the warps per byte of shared memory).
@@ -353,6 +431,8 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         for (int f = 0; f < 6; ++f)
             l2_prefetch(B + f * fs + (size_t)r0 * a.kz_in, bytes, t, T);
     }
+    const bool cfl = a.dyn && a.ystage == 1;  // max |u_d| of the step's initial state
+    double mx = 0.0, my = 0.0, mz = 0.0;
     cd p[E], q[E];
     if (PF) fetch_pair<NZ>(a, FP[0], FQ[0], (size_t)r0 * a.kz_in, active, t, p, q);
 #pragma unroll 1
@@ -389,6 +469,11 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             const int y = t + T * e;
             const double ux = v[e].x, uy = v[e].y;
             const double uz = st[0 * NZ + y], ox = st[1 * NZ + y];
+            if (cfl) {
+                mx = fmax(mx, fabs(ux));
+                my = fmax(my, fabs(uy));
+                mz = fmax(mz, fabs(uz));
+            }
             const double oy = st[2 * NZ + y], oz = st[3 * NZ + y];
             const double cx = uy * oz - uz * oy;
             const double cy = uz * ox - ux * oz;
@@ -412,6 +497,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         }
         __syncthreads();
     }
+    if (cfl) umax_accumulate(a.dyn, 3, mx, my, mz);
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = mk(st[4 * NZ + t + T * e], st[0 * NZ + t + T * e]);
@@ -564,19 +650,19 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
                 const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
                 const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
                 if (a.rk2) {
-                    un = add(scale(u, e2), scale(kv, a.dt * e1));
+                    un = add(scale(u, e2), scale(kv, dt_of(a) * e1));
                 } else {
                     const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
                     const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
-                    un = add(scale(u, e2), scale(sum, a.sdt));
+                    un = add(scale(u, e2), scale(sum, sdt_of(a)));
                 }
             } else {
                 cd delta;
                 if (a.rk2) {
-                    delta = scale(kv, a.dt);
+                    delta = scale(kv, dt_of(a));
                 } else {
                     const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), a.sdt);
+                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), sdt_of(a));
                 }
                 un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
             }
@@ -684,7 +770,14 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NY, CT>::C;
     using F = BFFT<NY>;
     const size_t smem = sizeof(cd) * F::SMEM * C + sizeof(int) * NY;  // + line offsets
-    if (inverse) {
+    if (inverse && CT == 256 && a.pruned && !(a.opt & 256)) {
+        const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
+                              sizeof(int) * NY;
+        static size_t done = 0;
+        set_smem(k2s_3d<NY>, smem_s, done);
+        const int grid = a.nrl * ((a.kz_in + C - 1) / C);
+        k2s_3d<NY><<<grid, F::T * C, smem_s, s>>>(a);
+    } else if (inverse) {
         static size_t done = 0;
         set_smem(k2_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
@@ -780,11 +873,13 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
         hook.end(0, B * (3.0 * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + 5.0 * a.nx * lines_in));
         *launches += 1;
     } else if (pass == 1) {
+        Ns3dArgs b = a;  // the z pass of stage 1 feeds the CFL max
+        b.ystage = stage;
         hook.begin(3);
         if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
         hook.end(3, B * (5.0 * a.nrl * kyk * a.kz_in + 6.0 * plane_in));
         hook.begin(1);
-        if ((err = dispatch_z3(a, s)) != cudaSuccess) return err;
+        if ((err = dispatch_z3(b, s)) != cudaSuccess) return err;
         hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
         hook.begin(3);
         if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;

@@ -15,7 +15,47 @@ struct DevFlags {
     int div_var;    // variable index of the first non-finite value
     int div_step;   // step counter value (1-based within the launch batch)
     int steps;      // steps started since the counter was last reset
+    int bad_dt;     // adaptive dt: nonpositive dt (past t_end) at step div_step
 };
+
+// Adaptive (CFL) time step, device-resident so replayed graphs follow it
+// (Simulation::compute_dt + compute_cfl_dt, simulation.cpp:463-476,
+// time_stepping.cpp:15-26).  The stage-1 physical pass of every step reduces
+// max |u_d| of the step's initial state (Solver::max_velocity_per_axis,
+// solvers.cpp:176-194, 341-357) into umax; dt_update then sets dt and the
+// integrating-factor tables before stage 2.
+struct DynStep {
+    double dt, hdt, sdt;
+    double umax[3];      // non-negative: ordered like their bit patterns
+    double t;            // time at the start of the current step
+    double t_end;        // < 0: no clamp
+    double cfl, dt_max;
+    double dx[3];
+    double last_dt;
+};
+
+template <class A>
+__device__ __forceinline__ double dt_of(const A& a) { return a.dyn ? a.dyn->dt : a.dt; }
+template <class A>
+__device__ __forceinline__ double hdt_of(const A& a) { return a.dyn ? a.dyn->hdt : a.hdt; }
+template <class A>
+__device__ __forceinline__ double sdt_of(const A& a) { return a.dyn ? a.dyn->sdt : a.sdt; }
+
+// max(|a|, |b|, |c|) of one thread's points into dyn->umax (warp max, then one
+// atomic per warp and axis).
+__device__ __forceinline__ void umax_accumulate(DynStep* dyn, int naxes, double a, double b, double c) {
+    for (int o = 16; o > 0; o >>= 1) {
+        a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        c = fmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long* u = reinterpret_cast<unsigned long long*>(dyn->umax);
+        atomicMax(u + 0, (unsigned long long)__double_as_longlong(a));
+        atomicMax(u + 1, (unsigned long long)__double_as_longlong(b));
+        if (naxes > 2) atomicMax(u + 2, (unsigned long long)__double_as_longlong(c));
+    }
+}
 
 // Grid description shared by the 2D and 3D solvers.  Axis 0 is the slowest
 // (row-major), the last axis is the half-stored Hermitian one.
@@ -48,6 +88,8 @@ struct Ns2dArgs {
     double kx_scale, ky_scale;
     double inv_n;       // 1 / (nx ny)
     double dt, hdt, sdt;
+    DynStep* dyn;       // adaptive dt (nullptr: the fixed dt above)
+    int ystage;         // RK stage of the physical pass (stage 1 feeds the CFL max)
     const double* e1x;  // exp(0.5 dt (-nu kx^2)) per kx index (nx)
     const double* e1y;  // exp(0.5 dt (-nu ky^2)) per ky index (nh)
     const double* e2x;  // exp(dt (-nu kx^2))
@@ -126,6 +168,8 @@ struct Ns3dArgs {
     double kx_scale, ky_scale, kz_scale;
     double inv_n;
     double dt, hdt, sdt;
+    DynStep* dyn;       // adaptive dt (nullptr: the fixed dt above)
+    int ystage;         // RK stage of the physical pass (stage 1 feeds the CFL max)
     const double *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
     cd* u;               // 3 variables, each nx*ny*nh (reference layout)
     cd* k1;
@@ -199,6 +243,10 @@ cudaError_t launch_count_masked(const cd* f, int dims, const int* n, const int* 
 cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double* kscale,
                              int axis, double* d_k, unsigned char* d_mask, cudaStream_t s,
                              long* launches);
+// dt from umax (CFL), clamp to t_end, integrating-factor tables for it
+// (layout of skgpu.cu etab_ptr), umax reset; flags->bad_dt if dt <= 0.
+cudaError_t launch_dt_update(DynStep* dyn, DevFlags* flags, double* etab, int dims, const int* n,
+                             const double* kscale, double nu, cudaStream_t s, long* launches);
 cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* kscale, int nvars,
                           int solver2d, double* d_out, cudaStream_t s, long* launches,
                           double nu = 0.0, const int* steps = nullptr, bool zero_first = true);

@@ -163,6 +163,11 @@ struct skg_ctx {
     // stream change.
     cudaGraphExec_t gexec = nullptr;
     double* g_diag = nullptr;
+
+    // adaptive (CFL) dt: skg_set_cfl
+    bool adaptive = false;
+    double cfl = 0.5, dt_max = 0.1, t_end = -1.0, last_dt = 0.0;
+    skg::DynStep* d_dyn = nullptr;
     double g_dt = 0.0;
     bool g_pruned = false;
     cudaStream_t g_stream = nullptr;
@@ -293,6 +298,7 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     a.e1y = etab_ptr(c, 0, 1);
     a.e2x = etab_ptr(c, 1, 0);
     a.e2y = etab_ptr(c, 1, 1);
+    a.dyn = c->adaptive ? c->d_dyn : nullptr;
     a.u = c->u;
     a.k1 = c->k[0];
     a.k2 = c->k[1];
@@ -370,6 +376,7 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.e2x = etab_ptr(c, 1, 0);
     a.e2y = etab_ptr(c, 1, 1);
     a.e2z = etab_ptr(c, 1, 2);
+    a.dyn = c->adaptive ? c->d_dyn : nullptr;
     a.u = c->u;
     a.k1 = c->k[0];
     a.k2 = c->k[1];
@@ -428,9 +435,21 @@ int sync_and_check(skg_ctx* c, long nsteps, double dt) {
     harvest(c);
     skg::DevFlags f;
     CUDA_TRY(cudaMemcpy(&f, c->flags, sizeof(f), cudaMemcpyDeviceToHost));
+    skg::DynStep dyn{};
+    if (c->adaptive) {
+        CUDA_TRY(cudaMemcpy(&dyn, c->d_dyn, sizeof(dyn), cudaMemcpyDeviceToHost));
+        c->last_dt = dyn.last_dt;
+    }
+    if (f.bad_dt) {  // compute_dt gave dt <= 0 (past t_end): the step did not run
+        c->it += f.div_step - 1;
+        c->t = dyn.t;
+        return fail(SKG_ECONFIG, "step: nonpositive dt (past t_end?)");
+    }
     if (f.diverged) {
         const long done = f.div_step;
-        for (long i = 0; i < done; ++i) c->t += dt;
+        if (c->adaptive) c->t = dyn.t;
+        else
+            for (long i = 0; i < done; ++i) c->t += dt;
         c->it += done;
         c->div_it = c->it;
         c->div_var = f.div_var;
@@ -440,7 +459,12 @@ int sync_and_check(skg_ctx* c, long nsteps, double dt) {
         return fail(SKG_EDIVERGENCE, std::string("non-finite value in field '") + key +
                                          "' at iteration " + std::to_string(c->it));
     }
-    for (long i = 0; i < nsteps; ++i) c->t += dt;
+    if (c->adaptive) {
+        c->t = dyn.t;
+    } else {
+        for (long i = 0; i < nsteps; ++i) c->t += dt;
+        if (nsteps > 0) c->last_dt = dt;
+    }
     c->it += nsteps;
     return SKG_OK;
 }
@@ -601,16 +625,38 @@ int enqueue_dist_step(skg_ctx* c, double dt, long* counter) {
                 if (rc) return rc;
             }
         }
+        if (st == 1 && c->adaptive) {
+            if (c->comm) {  // global max |u_d| over the ranks' x rows
+                const ncclResult_t nr = ncclAllReduce(c->d_dyn->umax, c->d_dyn->umax, 3, ncclDouble,
+                                                      ncclMax, c->comm, c->stream);
+                if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+            }
+            CUDA_TRY(skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale,
+                                           c->nu, c->stream, counter));
+        }
     }
     return SKG_OK;
 }
 
 int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
-    if (!(dt > 0.0)) return fail(SKG_ECONFIG, "step: nonpositive dt");
+    if (c->adaptive) dt = -1.0;  // device-resident: compute_dt per step
+    else if (!(dt > 0.0)) return fail(SKG_ECONFIG, "step: nonpositive dt");
     if (nsteps < 0) return fail(SKG_ECONFIG, "step: negative step count");
     CUDA_TRY(cudaSetDevice(c->device));
-    int rc = refresh_exp(c, dt);
-    if (rc) return rc;
+    if (c->adaptive) {
+        skg::DynStep d{};
+        d.t = c->t;
+        d.t_end = c->t_end;
+        d.cfl = c->cfl;
+        d.dt_max = c->dt_max;
+        for (int k = 0; k < c->dims; ++k) d.dx[k] = c->L[k] / c->n[k];  // grid.cpp:50
+        d.last_dt = c->last_dt;
+        CUDA_TRY(cudaMemcpyAsync(c->d_dyn, &d, sizeof(d), cudaMemcpyHostToDevice, c->stream));
+        c->cached_dt = -1.0;  // the device owns the factor tables now
+    } else {
+        int rc = refresh_exp(c, dt);
+        if (rc) return rc;
+    }
     skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
     CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
@@ -630,14 +676,22 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             skg::Ns2dArgs a = args2d(c, dt);
             fused = skg::ns2d_fast_ok(a);
             if (!fused) a.diag = nullptr;
-            for (int st = 1; st <= nst && e == cudaSuccess; ++st)
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
                 e = skg::ns2d_launch_stage(a, st, c->stream, counter, hook);
+                if (st == 1 && c->adaptive && e == cudaSuccess)
+                    e = skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale,
+                                              c->nu, c->stream, counter);
+            }
         } else {
             skg::Ns3dArgs a = args3d(c, dt);
             fused = c->pruned;
             if (!fused) a.diag = nullptr;
-            for (int st = 1; st <= nst && e == cudaSuccess; ++st)
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
                 e = skg::ns3d_launch_stage(a, st, c->stream, counter, hook);
+                if (st == 1 && c->adaptive && e == cudaSuccess)
+                    e = skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale,
+                                              c->nu, c->stream, counter);
+            }
         }
         if (e == cudaSuccess && c->diag && !fused)  // unfused paths: one reduction per step
             e = skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
@@ -1025,6 +1079,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     ok = ok && alloc((void**)&c->flags, sizeof(skg::DevFlags));
     ok = ok && alloc((void**)&c->d_count, sizeof(unsigned long long));
     ok = ok && alloc((void**)&c->d_red, 3 * sizeof(double));
+    ok = ok && alloc((void**)&c->d_dyn, sizeof(skg::DynStep));
     if (!ok) return cleanup(SKG_ECUDA, "device allocation failed (grid too large for this GPU?)");
     for (int d = 0; d < dims; ++d) {
         c->tw[d] = twiddle_table(device, n[d]);
@@ -1052,6 +1107,7 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->flags);
     cudaFree(c->d_count);
     cudaFree(c->d_red);
+    cudaFree(c->d_dyn);
     harvest(c);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (Part& p : c->parts) {
@@ -1319,6 +1375,30 @@ int skg_get_grid(skg_ctx* c, int axis, double* k_axis, unsigned char* mask) {
 int skg_last_divergence(const skg_ctx* c, long* iteration, int* var) {
     *iteration = c->div_it;
     *var = c->div_var;
+    return SKG_OK;
+}
+
+int skg_set_cfl(skg_ctx* c, double cfl_coef, double dt_max, double t_end) {
+    if (cfl_coef <= 0.0) {
+        c->adaptive = false;
+        return SKG_OK;
+    }
+    if (!(dt_max > 0.0)) return fail(SKG_ECONFIG, "dt_max must be > 0");  // simulation.cpp:253-256
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    c->adaptive = true;
+    c->cfl = cfl_coef;
+    c->dt_max = dt_max;
+    c->t_end = t_end;
+    return SKG_OK;
+}
+
+double skg_last_dt(const skg_ctx* c) { return c->last_dt; }
+
+int skg_set_time(skg_ctx* c, double t) {
+    c->t = t;
     return SKG_OK;
 }
 

@@ -136,6 +136,57 @@ __global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long
     diag_accumulate(out, e, z, d);
 }
 
+struct DtGeo {
+    int dims;
+    int n[3];
+    int ext[3];
+    double ks[3];
+    double nu;
+};
+
+// Simulation::compute_dt (CFL branch, simulation.cpp:463-476) and
+// ExactLinStepper::refresh_exp (time_stepping.cpp:37-57) for the new dt.
+__global__ void dt_update(DynStep* dyn, DevFlags* flags, double* etab, DtGeo g) {
+    if (flags->diverged) return;
+    double dt = dyn->dt_max;
+    for (int d = 0; d < g.dims; ++d) {
+        const double vel = fmax(fabs(dyn->umax[d]), 1e-30);
+        dt = fmin(dt, dyn->cfl * dyn->dx[d] / vel);
+    }
+    if (dyn->t_end >= 0.0) {
+        const double remaining = dyn->t_end - dyn->t;
+        if (remaining < dt) dt = remaining;
+    }
+    __syncthreads();  // every thread has read umax and t
+    if (!(dt > 0.0)) {
+        if (threadIdx.x == 0) {
+            flags->bad_dt = 1;
+            flags->div_step = flags->steps;
+            flags->diverged = 1;  // stops the remaining kernels
+        }
+        return;
+    }
+    int per = 0;
+    for (int d = 0; d < g.dims; ++d) per += g.ext[d];
+    for (int q = threadIdx.x; q < 2 * per; q += blockDim.x) {
+        const int which = q / per;
+        int i = q % per, d = 0;
+        while (i >= g.ext[d]) i -= g.ext[d++];
+        const int si = d == g.dims - 1 ? i : signed_index(i, g.n[d]);
+        const double kv = g.ks[d] * si;
+        const double hdt = which == 0 ? 0.5 * dt : dt;
+        etab[q] = exp(hdt * (-g.nu * (kv * kv)));
+    }
+    if (threadIdx.x == 0) {
+        dyn->dt = dt;
+        dyn->hdt = 0.5 * dt;
+        dyn->sdt = dt / 6.0;
+        dyn->last_dt = dt;
+        dyn->t += dt;
+        dyn->umax[0] = dyn->umax[1] = dyn->umax[2] = 0.0;
+    }
+}
+
 MaskGeo make_geo(int dims, const int* n, const int* kc) {
     MaskGeo g{};
     g.dims = dims;
@@ -172,6 +223,21 @@ cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double
     long long S = 1;
     for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.nh : n[d]);
     grid_dump<<<592, 256, 0, s>>>(g, axis, kscale[axis], d_k, d_mask, S);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_update(DynStep* dyn, DevFlags* flags, double* etab, int dims, const int* n,
+                             const double* kscale, double nu, cudaStream_t s, long* launches) {
+    DtGeo g{};
+    g.dims = dims;
+    for (int d = 0; d < dims; ++d) {
+        g.n[d] = n[d];
+        g.ext[d] = d == dims - 1 ? n[d] / 2 + 1 : n[d];
+        g.ks[d] = kscale[d];
+    }
+    g.nu = nu;
+    dt_update<<<1, 256, 0, s>>>(dyn, flags, etab, g);
     ++*launches;
     return cudaGetLastError();
 }
