@@ -144,6 +144,10 @@ double skg_time(const skg_ctx* ctx);
  * arbitrary stage state (dealiased output, mean mode 0).  Host buffers,
  * nvars * S complex128 each. */
 int skg_tendency(skg_ctx* ctx, const double* in, double* out);
+/* Solver::max_velocity_per_axis (solvers.cpp:176-194, 341-357) of the
+ * spectral state `spect` (host, reference layout): max |u_d| over the grid,
+ * `dims` doubles, from the same fused physical pass as the tendency. */
+int skg_max_velocity(skg_ctx* ctx, const double* spect, double* umax);
 
 /* == FftPlan::forward (fft.cpp:92-98: r2c then *= 1/N) and FftPlan::inverse
  * (fft.cpp:100-106: unnormalised c2r, input untouched) on the context grid.

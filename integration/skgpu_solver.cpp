@@ -60,6 +60,26 @@ public:
     // Solver::tendency (simulation.hpp:34): dealiased nonlinear term of an
     // arbitrary stage state, computed on the GPU.
     void tendency(const StateVec& state, StateVec& out) override {
+        const std::size_t S = sim_.oper().spect_size;
+        pack(state);
+        res_.resize(nvars_ * S);
+        check(skg_tendency(ctx_, reinterpret_cast<const double*>(in_.data()),
+                           reinterpret_cast<double*>(res_.data())));
+        out.resize(nvars_);
+        for (int v = 0; v < nvars_; ++v) out[v].assign(res_.begin() + v * S, res_.begin() + (v + 1) * S);
+    }
+
+    // Solver::max_velocity_per_axis (solvers.cpp:176-194, 341-357) of the
+    // current state, for compute_dt with time_stepping.fixed_dt = 0.
+    std::vector<double> max_velocity_per_axis() override {
+        pack(sim_.state().spect());
+        std::vector<double> m(sim_.oper().dims, 0.0);
+        check(skg_max_velocity(ctx_, reinterpret_cast<const double*>(in_.data()), m.data()));
+        return m;
+    }
+
+protected:
+    void pack(const StateVec& state) {
         const auto& g = sim_.oper();
         if (!ctx_) {
             std::vector<double> L(g.L.begin(), g.L.end());
@@ -74,18 +94,8 @@ public:
             if (state[v].size() != S) throw ShapeError("gpu tendency: wrong state shape");
             std::memcpy(in_.data() + v * S, state[v].data(), S * sizeof(cplx));
         }
-        res_.resize(nvars_ * S);
-        check(skg_tendency(ctx_, reinterpret_cast<const double*>(in_.data()),
-                           reinterpret_cast<double*>(res_.data())));
-        out.resize(nvars_);
-        for (int v = 0; v < nvars_; ++v) out[v].assign(res_.begin() + v * S, res_.begin() + (v + 1) * S);
     }
 
-    std::vector<double> max_velocity_per_axis() override {
-        throw ConfigError("gpu solvers run with a fixed dt (time_stepping.fixed_dt > 0)");
-    }
-
-protected:
     const char* base_;
     int nvars_;
     skg_ctx* ctx_ = nullptr;
@@ -140,8 +150,8 @@ extern "C" {
 
 const char* skgi_last_error(void) { return g_err.c_str(); }
 
-// Runs the REFERENCE Simulation (step_once x nsteps, fixed dt, files and
-// forcing off) with solver `name` ("ns2d", "ns2d_gpu", "ns3d", "ns3d_gpu")
+// Runs the REFERENCE Simulation (step_once x nsteps, fixed dt or, with
+// dt = 0, the CFL dt of compute_dt; files and forcing off) with solver `name` ("ns2d", "ns2d_gpu", "ns3d", "ns3d_gpu")
 // from the spectral state `in`; writes the final state to `out`.
 int skgi_run(const char* name, int dims, const int* n, double nu, double dt, const double* in,
              long nsteps, double* out) {

@@ -33,7 +33,7 @@ EXPORTS = [
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
-    "skg_set_cfl", "skg_last_dt", "skg_set_time",
+    "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity",
 ]
 
 
@@ -116,6 +116,7 @@ def load_library():
     L.skg_last_dt.argtypes = [vp]
     L.skg_last_dt.restype = C.c_double
     L.skg_set_time.argtypes = [vp, C.c_double]
+    L.skg_max_velocity.argtypes = [vp, C.c_void_p, C.c_void_p]
     _lib = L
     return L
 
@@ -322,6 +323,13 @@ class Simulation:
         series = np.zeros((int(n_iters), 3), np.float64)
         self._call("skg_run", C.c_double(dt), C.c_long(int(n_iters)), _ptr(series))
         return series
+
+    def max_velocity(self, spect: np.ndarray) -> np.ndarray:
+        """Solver::max_velocity_per_axis of `spect` (solvers.cpp:176-194, 341-357)."""
+        s = np.ascontiguousarray(spect, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)
+        out = np.zeros(self.dims, np.float64)
+        self._call("skg_max_velocity", _ptr(s), _ptr(out))
+        return out
 
     def compute_tendency(self, spect: np.ndarray) -> np.ndarray:
         s = np.ascontiguousarray(spect, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)

@@ -1234,7 +1234,21 @@ int skg_run(skg_ctx* c, double dt, long nsteps, double* series) {
     return rc;
 }
 
+static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax);
+
 int skg_tendency(skg_ctx* c, const double* in, double* out) {
+    return tendency_impl(c, in, out, nullptr);
+}
+
+int skg_max_velocity(skg_ctx* c, const double* in, double* umax) {
+    if (!umax) return fail(SKG_ECONFIG, "skg_max_velocity: null output");
+    return tendency_impl(c, in, nullptr, umax);
+}
+
+// Solver::tendency of `in` (host, reference layout) into `out` (or not, when
+// null); with umax, also max |u_d| of `in` (Solver::max_velocity_per_axis)
+// from the same physical pass.
+static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax) {
     if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_tendency on a slab-decomposed context");
     CUDA_TRY(cudaSetDevice(c->device));
     if (c->pending_steps) {
@@ -1253,8 +1267,10 @@ int skg_tendency(skg_ctx* c, const double* in, double* out) {
         if (rc) return rc;
         skg::Ns2dArgs a = args2d(c, c->cached_dt);
         a.u = c->k[2];
+        a.dyn = umax ? c->d_dyn : nullptr;
         skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+        if (umax) CUDA_TRY(cudaMemsetAsync(c->d_dyn, 0, sizeof(skg::DynStep), c->stream));
         CUDA_TRY(skg::ns2d_launch_stage(a, 1, c->stream, &c->launches, hook_of(c)));
         rc = store_state_to_io(c, c->k[0]);
         if (rc) return rc;
@@ -1265,14 +1281,23 @@ int skg_tendency(skg_ctx* c, const double* in, double* out) {
         if (rc) return rc;
         skg::Ns3dArgs a = args3d(c, c->cached_dt);
         a.u = c->k[2];
+        a.dyn = umax ? c->d_dyn : nullptr;
         skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+        if (umax) CUDA_TRY(cudaMemsetAsync(c->d_dyn, 0, sizeof(skg::DynStep), c->stream));
         CUDA_TRY(skg::ns3d_launch_stage(a, 1, c->stream, &c->launches, hook_of(c)));
         rc = store_state_to_io(c, c->k[0]);
         if (rc) return rc;
     }
-    CUDA_TRY(cudaMemcpyAsync(out, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToHost,
-                             c->stream));
+    if (out)
+        CUDA_TRY(cudaMemcpyAsync(out, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    if (umax) {
+        skg::DynStep d;
+        CUDA_TRY(cudaMemcpyAsync(&d, c->d_dyn, sizeof(d), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        for (int k = 0; k < c->dims; ++k) umax[k] = d.umax[k];
+    }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->pruned = keep_pruned;
     return SKG_OK;

@@ -88,3 +88,22 @@ def test_cfl_t_end_clamp(solver, n):
     with pytest.raises(api.ConfigError):
         g.step(1)
     assert g.iteration == it
+
+
+@pytest.mark.parametrize("solver,n,kind", [("ns2d", (64, 64), "ic"), ("ns2d", (32, 32), "noise"),
+                                            ("ns3d", (16, 16, 16), "ic")])
+def test_max_velocity_matches_physical_fields(solver, n, kind):
+    """skg_max_velocity == max |u_d| of the c2r velocity components."""
+    nv = 1 if solver == "ns2d" else 3
+    u0 = ic.initial_state(solver, n, seed=2) if kind == "ic" else _noise(n, nv, 3)
+    g = api.Simulation(solver, n, 1e-3, 1e-3)
+    m = g.max_velocity(u0)
+    if solver == "ns2d":
+        kx, ky = O.k_axes(n)
+        ksq = O.k_sq(n)
+        psi = np.where(ksq == 0, 0, u0[0] / np.where(ksq == 0, 1, ksq))
+        comps = [1j * ky[None, :] * psi, -1j * kx[:, None] * psi]
+    else:
+        comps = list(u0)
+    ref = [np.abs(O.inverse(c, n)).max() for c in comps]
+    assert np.allclose(m, ref, rtol=1e-13, atol=0)

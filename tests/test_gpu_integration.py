@@ -48,3 +48,16 @@ def test_reference_simulation_on_gpu_tendency(solver, n, nu, steps):
     gpu = _run(L, solver + "_gpu", n, nu, dt, u0, steps)
     for v in range(u0.shape[0]):
         assert O.rel_l2(gpu[v], cpu[v]) < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("solver,n", [("ns2d", (64, 64)), ("ns3d", (16, 16, 16))])
+def test_reference_simulation_cfl_on_gpu(solver, n):
+    """time_stepping.fixed_dt = 0: the reference's compute_dt asks the GPU
+    solver's max_velocity_per_axis (skg_max_velocity) every step."""
+    L = _lib()
+    u0 = np.ascontiguousarray(ic.initial_state(solver, n, 8))
+    cpu = _run(L, solver, n, 1e-3, 0.0, u0, 4)
+    gpu = _run(L, solver + "_gpu", n, 1e-3, 0.0, u0, 4)
+    for v in range(u0.shape[0]):
+        assert O.rel_l2(gpu[v], cpu[v]) < 1e-10
