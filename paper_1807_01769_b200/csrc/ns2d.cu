@@ -112,21 +112,25 @@ __device__ __forceinline__ cd stage_combine(const Ns2dArgs& a, int stage, int ky
 // neither loaded nor stored, and the stage-state slots shrink from 16 to 12.
 // EM = 8 elements per thread: twice the threads per line, a quarter fewer
 // registers, one more shared-memory exchange; the zero band is then e in [3, 5).
-template <int N, int EM>
+// CTW: target CTA width (threads); narrow CTAs (one line each, CTW <= T)
+// spread small grids over all SMs.
+template <int N, int EM, int CTW = 256>
 struct XCfg {
     using F = BFFT<N, false, EM>;
     static constexpr int T = F::T;
-    static constexpr int LPC = T >= 256 ? 1 : 256 / T;
+    static constexpr int LPC = T >= CTW ? 1 : CTW / T;
     static constexpr int CT = T * LPC;
+    static constexpr int MINB = CT >= 256 ? 2 : 512 / CT;  // keeps <= 128 registers
     static constexpr int ZLO = EM == 16 ? 6 : 3, ZHI = EM == 16 ? 10 : 5;
 };
 
-template <int NX, bool PZ, int NM, int EM = 16>
-__global__ void __launch_bounds__(XCfg<NX, EM>::CT, (PZ || EM == 8) ? 2 : 1)
+template <int NX, bool PZ, int NM, int EM = 16, int CTW = 256>
+__global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
+                                  (PZ || EM == 8) ? XCfg<NX, EM, CTW>::MINB : XCfg<NX, EM, CTW>::MINB / 2)
     k1_xinv(Ns2dArgs a, int stage) {
     using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
-    constexpr int LPC = XCfg<NX, EM>::LPC;
+    constexpr int LPC = XCfg<NX, EM, CTW>::LPC;
     constexpr int ZLO = PZ ? XCfg<NX, EM>::ZLO : E, ZHI = PZ ? XCfg<NX, EM>::ZHI : E;
     constexpr int NS = E - (ZHI - ZLO);  // stage-state slots per thread
     extern __shared__ cd smem[];
@@ -151,22 +155,13 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, (PZ || EM == 8) ? 2 : 1)
     // same thread-private layout), so all loads are in flight at once.
     const cd* kprev = stage == 2 ? a.k1 : stage == 3 ? a.k2 : a.k3;
     cd* kv = sm;  // exchange buffer as k staging: kv[slot * T + t]
-    if ((a.opt & 8) && l == 0) {  // the columns one wave ahead
-        const int nk = (blockIdx.x + a.wave) * LPC;
-        const int ncol = NM == 2 ? a.ncols : a.ky_in;
-        if (nk < ncol) {
-            const size_t c = ncol - nk < LPC ? ncol - nk : LPC;
-            l2_prefetch(a.u + (size_t)nk * NX, sizeof(cd) * NX * c, t, T);
-            if (stage > 1) l2_prefetch(kprev + (size_t)nk * NX, sizeof(cd) * NX * c, t, T);
-        }
-    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         if (e >= ZLO && e < ZHI) continue;
         const int slot = e < ZLO ? e : e - (ZHI - ZLO);
         const int i = t + T * e;
         const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
-        if (keep && !(a.opt & 32)) {  // opt 32 diagnostic: no loads
+        if (keep) {
             const size_t idx = (size_t)kyl * NX + i;
             cp_async16(&sv[slot * T + t], a.u + idx);
             if (stage > 1) cp_async16(&kv[slot * T + t], kprev + idx);
@@ -218,7 +213,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, (PZ || EM == 8) ? 2 : 1)
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const int x = t + T * e;
-                    const int q = x / a.nrl, xl = x - q * a.nrl;
+                    const int q = x >> a.lg_nrl, xl = x & (a.nrl - 1);
                     out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG)] = v[e];
                 }
             } else {
@@ -476,13 +471,18 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     auto issue = [&](int x) {
         if (x >= a.nrl) return;
         for (int i = t; i < a.ky_in; i += T) {
-            // owner of column i under cstart[q] = 2 floor(q PP / G), PP kept
-            // column pairs (skgpu.cu create_impl), computed instead of loaded
-            const int PP = (a.ky_in + 1) >> 1;
-            const int ro = (((i >> 1) + 1) * a.G - 1) / PP;
-            const int cs = 2 * (ro * PP / a.G);
-            const int nc = (ro == a.G - 1 ? a.ky_in : 2 * ((ro + 1) * PP / a.G)) - cs;
-            const size_t q = (size_t)a.nrl * cs + ((size_t)(x / RG) * nc + (i - cs)) * RG + (x % RG);
+            size_t q;
+            if (a.G == 1) {
+                q = ((size_t)(x / RG) * a.ky_in + i) * RG + (x % RG);
+            } else {
+                // owner of column i under cstart[q] = 2 floor(q PP / G), PP kept
+                // column pairs (skgpu.cu create_impl), computed instead of loaded
+                const int PP = (a.ky_in + 1) >> 1;
+                const int ro = (((i >> 1) + 1) * a.G - 1) / PP;
+                const int cs = 2 * (ro * PP / a.G);
+                const int nc = (ro == a.G - 1 ? a.ky_in : 2 * ((ro + 1) * PP / a.G)) - cs;
+                q = (size_t)a.nrl * cs + ((size_t)(x / RG) * nc + (i - cs)) * RG + (x % RG);
+            }
             cp_async16(&st[i], P + q);
             cp_async16(&st[ld + i], Q + q);
         }
@@ -554,11 +554,12 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
 
 // x-forward of the two product spectra per kept ky column, combination
 // kx ky A + (kx^2 - ky^2) B, dealias + mean 0 + RK epilogue (as k4_xfwd).
-template <int NX, int EM = 16>
-__global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int stage) {
+template <int NX, int EM = 16, int CTW = 256>
+__global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB)
+    k4b_xfwd(Ns2dArgs a, int stage) {
     using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
-    constexpr int LPC = XCfg<NX, EM>::LPC;
+    constexpr int LPC = XCfg<NX, EM, CTW>::LPC;
     constexpr int ZLO = XCfg<NX, EM>::ZLO, ZHI = XCfg<NX, EM>::ZHI, NS = E - (ZHI - ZLO);
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
@@ -572,39 +573,14 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
     const double kyv = a.ky_scale * (double)ky;
     const size_t blk = (size_t)2 * ((a.ncols + 1) >> 1) * a.nrl;  // receive block per source
     auto ridx = [&](int x) {
-        const int ro = x / a.nrl, xl = x - ro * a.nrl;
+        const int ro = x >> a.lg_nrl, xl = x & (a.nrl - 1);
         return ro * blk + ((size_t)(kyl >> 1) * a.nrl + xl) * 2 + (kyl & 1);
     };
     const bool final = a.rk2 ? stage == 2 : stage == 4;
-    if (active && (a.opt & 1)) {  // field B of this column (all source blocks)
-        for (int ro = 0; ro < a.G; ++ro)
-            l2_prefetch(a.rA[1] + ro * blk + (size_t)(kyl >> 1) * a.nrl * 2, sizeof(cd) * 2 * a.nrl, t, T);
-    }
-    if (active && final && (a.opt & 2)) {  // RK epilogue operands
-        const size_t col = (size_t)kyl * NX;
-        l2_prefetch(a.u + col, sizeof(cd) * NX, t, T);
-        if (!a.rk2) {
-            l2_prefetch(a.k1 + col, sizeof(cd) * NX, t, T);
-            l2_prefetch(a.k2 + col, sizeof(cd) * NX, t, T);
-            l2_prefetch(a.k3 + col, sizeof(cd) * NX, t, T);
-        }
-    }
-    if ((a.opt & 4) && l == 0) {  // both fields of the column one wave ahead
-        const int nk = (blockIdx.x + a.wave) * LPC;
-        if (nk < a.ncols) {
-            const int c = a.ncols - nk < LPC ? a.ncols - nk : LPC;
-            const size_t np = (size_t)((nk + c - 1) >> 1) - (nk >> 1) + 1;
-            for (int ro = 0; ro < a.G; ++ro)
-                for (int f = 0; f < 2; ++f)
-                    l2_prefetch(a.rA[f] + ro * blk + (size_t)(nk >> 1) * a.nrl * 2,
-                                sizeof(cd) * 2 * a.nrl * np, t, T);
-        }
-    }
     cd v[E];
-    const bool noload = (a.opt & 16) != 0;  // diagnostic: FFT cost without the loads
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = noload ? mk(e, t) : active ? a.rA[0][ridx(t + T * e)] : zero();
+        v[e] = active ? a.rA[0][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -615,7 +591,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
     }
 #pragma unroll
     for (int e = 0; e < E; ++e)
-        v[e] = noload ? mk(t, e) : active ? a.rA[1][ridx(t + T * e)] : zero();
+        v[e] = active ? a.rA[1][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     bool bad = false;
@@ -685,9 +661,9 @@ __global__ void __launch_bounds__(XCfg<NX, EM>::CT, 2) k4b_xfwd(Ns2dArgs a, int 
     }
 }
 
-template <int NX, bool PZ, int NM, int EM = 16>
+template <int NX, bool PZ, int NM, int EM = 16, int CTW = 256>
 cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
-    using C = XCfg<NX, EM>;
+    using C = XCfg<NX, EM, CTW>;
     using F = typename C::F;
     constexpr int T = F::T, E = F::E;
     constexpr int LPC = C::LPC;
@@ -697,10 +673,10 @@ cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
     if (grid == 0) return cudaSuccess;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k1_xinv<NX, PZ, NM, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k1_xinv<NX, PZ, NM, EM, CTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    k1_xinv<NX, PZ, NM, EM><<<grid, T * LPC, smem, s>>>(a, stage);
+    k1_xinv<NX, PZ, NM, EM, CTW><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
 }
 
@@ -768,24 +744,35 @@ cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
 template <int NX>
 constexpr int fast_em() { return NX >= 4096 ? SKG_FAST_X_EM : 16; }
 
-template <int NX>
-cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+template <int NX, int CTW>
+cudaError_t launch_fast_x_w(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
     constexpr int EM = fast_em<NX>();
-    if (inverse) return launch_k1<NX, true, 2, EM>(a, stage, s);
-    using C = XCfg<NX, EM>;
+    if (inverse) return launch_k1<NX, true, 2, EM, CTW>(a, stage, s);
+    using C = XCfg<NX, EM, CTW>;
     using F = typename C::F;
     constexpr int T = F::T;
     constexpr int LPC = C::LPC;
     const size_t smem = sizeof(cd) * (F::SMEM + (F::E - (C::ZHI - C::ZLO)) * T) * LPC;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k4b_xfwd<NX, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k4b_xfwd<NX, EM, CTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    k4b_xfwd<NX, EM><<<grid, T * LPC, smem, s>>>(a, stage);
+    k4b_xfwd<NX, EM, CTW><<<grid, T * LPC, smem, s>>>(a, stage);
     return cudaGetLastError();
+}
+
+// Narrow CTAs (one column each) when 256-thread CTAs would leave SMs idle.
+template <int NX>
+cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+    constexpr int EM = fast_em<NX>();
+    constexpr int LPC = XCfg<NX, EM>::LPC;
+    if constexpr (LPC > 1) {
+        if ((a.ncols + LPC - 1) / LPC < a.wave) return launch_fast_x_w<NX, 1>(a, stage, inverse, s);
+    }
+    return launch_fast_x_w<NX, 256>(a, stage, inverse, s);
 }
 
 #define SKG_POW2_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)

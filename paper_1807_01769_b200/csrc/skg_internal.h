@@ -116,6 +116,7 @@ struct Ns2dArgs {
     // With G = 1 send and receive alias and the layouts reduce to the
     // single-GPU ones.
     int G, r, c0, ncols, nrl;
+    int lg_nrl;         // log2(nrl) (nx and G are powers of two)
     int lead;           // this partition advances the step counter
     const int* kowner;  // owning rank of each kept column (kcy + 1 entries)
     const int* cstart;  // first column of each rank (G + 1 entries)

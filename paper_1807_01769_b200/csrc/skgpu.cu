@@ -318,6 +318,8 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     a.c0 = 0;
     a.ncols = c->kc[1] + 1;
     a.nrl = c->n[0];
+    a.lg_nrl = 0;
+    while ((1 << a.lg_nrl) < a.nrl) ++a.lg_nrl;
     a.kowner = c->d_kowner;
     a.cstart = c->d_cstart;
     a.sI[0] = a.rI[0] = a.I[0];
@@ -338,6 +340,8 @@ skg::Ns2dArgs args2d_part(skg_ctx* c, double dt, const Part& p) {
     a.c0 = p.c0;
     a.ncols = p.ncols;
     a.nrl = c->nrl;
+    a.lg_nrl = 0;
+    while ((1 << a.lg_nrl) < a.nrl) ++a.lg_nrl;
     for (int f = 0; f < 2; ++f) {
         a.sI[f] = p.sI[f];
         a.rI[f] = p.rI[f];
