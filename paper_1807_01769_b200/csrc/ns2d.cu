@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
 // the input rows of FFT k+1 stream into a shared-memory stage (cp.async)
 // while FFT k runs.  Shared memory per group: split exchange (N doubles),
 // the finished row-a product (N doubles), stage (2 ld_i complex).
-template <int NY, int EM>
+template <int NY, int EM, bool CFL>
 __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, EM>::T : 256,
                                   EM == 8 ? 65536 / 64 / (BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, EM>::T : 256) : 2)
     k3_phys(Ns2dArgs a) {
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     };
     issue(0);
     cp_async_commit();
-    const bool cfl = a.dyn && a.ystage == 1;
+    constexpr bool cfl = CFL;  // max |u_d| of the step's initial state (adaptive dt)
     double mx = 0.0, my = 0.0;
     double acc[E];
 #pragma unroll 1
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
         if (k < 3) issue(k + 1);
         cp_async_commit();
         F::template run<+1>(v, sm, t, wb);
-        if (cfl) {
+        if constexpr (cfl) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 if (q == 0) mx = fmax(mx, fabs(v[e].x));
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
             }
         }
     }
-    if (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
+    if constexpr (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
     // forward r2c of both rows packed: z = prod_a + i prod_b
     cd v[E];
 #pragma unroll
@@ -448,7 +448,7 @@ __global__ void k4_decay(Ns2dArgs a) {
 
 // y pass, one row per group iteration, persistent over rows; the next row's
 // two input lines stream into shared memory (cp.async) during the FFTs.
-template <int NY>
+template <int NY, bool CFL>
 __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     using F = BFFT<NY>;
     constexpr int T = F::T, E = F::E;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     issue(x);
     cp_async_commit();
     const double h = 0.5 * a.inv_n;
-    const bool cfl = a.dyn && a.ystage == 1;  // max |u_d| of the step's initial state
+    constexpr bool cfl = CFL;  // max |u_d| of the step's initial state (adaptive dt)
     double mx = 0.0, my = 0.0;
     // every group runs the same number of iterations (barriers inside)
     const int iters = (a.nrl + stride - 1) / stride;
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
         issue(x + stride);
         cp_async_commit();
         F::template run<+1>(v, sm, t, wb);  // u + i v on the row
-        if (cfl) {
+        if constexpr (cfl) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 mx = fmax(mx, fabs(v[e].x));
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
             }
         }
     }
-    if (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
+    if constexpr (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
 }
 
 // x-forward of the two product spectra per kept ky column, combination
@@ -703,8 +703,8 @@ cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s)
     return cudaGetLastError();
 }
 
-template <int NY>
-cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
+template <int NY, bool CFL>
+cudaError_t launch_y_v(const Ns2dArgs& a, cudaStream_t s) {
     constexpr int EM = 16;
     using F = BFFT<NY, true, EM>;
     constexpr int T = F::T;
@@ -714,30 +714,37 @@ cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
     const int grid = (pairs + G - 1) / G;
     static size_t init = 0;
     if (init < smem) {
-        cudaFuncSetAttribute(k3_phys<NY, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k3_phys<NY, EM, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = smem;
     }
-    k3_phys<NY, EM><<<grid, T * G, smem, s>>>(a);
+    k3_phys<NY, EM, CFL><<<grid, T * G, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int NY>
-cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
+cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
+    return (a.dyn && a.ystage == 1) ? launch_y_v<NY, true>(a, s) : launch_y_v<NY, false>(a, s);
+}
+
+template <int NY, bool CFL>
+cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
     using F = BFFT<NY>;
     constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * (F::SMEM + 2 * a.ld_i) * G;
     static size_t init = 0;
     if (init < smem) {
-        cudaFuncSetAttribute(k3b_phys<NY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k3b_phys<NY, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = smem;
     }
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int groups = (a.nrl + G - 1) / G;
-    const int grid = groups < 2 * nsm ? groups : 2 * nsm;
-    k3b_phys<NY><<<grid, F::T * G, smem, s>>>(a);
+    const int grid = groups < a.wave ? groups : a.wave;
+    k3b_phys<NY, CFL><<<grid, F::T * G, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+template <int NY>
+cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
+    return (a.dyn && a.ystage == 1) ? launch_fast_y_v<NY, true>(a, s) : launch_fast_y_v<NY, false>(a, s);
 }
 
 // elements per thread of the fast path's x passes

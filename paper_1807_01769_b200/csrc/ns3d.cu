@@ -108,7 +108,7 @@ struct Strided {
     using F = BFFT<N>;
     static constexpr int T = F::T;
     static constexpr int C = T >= CT ? 1 : CT / T;
-    static constexpr int MINB = T * C > 256 ? 1 : 2;  // CTAs per SM
+    static constexpr int MINB = T * C >= 512 ? 1 : 512 / (T * C);  // keeps <= 128 registers
 };
 
 // ------------------------------------------------------------------ x-inverse
@@ -285,10 +285,10 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
 // vorticity outputs is read directly (recently read by this CTA: L2).
 // Output m: primary / secondary = A0 / -, A1 / -, A2 / -, A2 / A1, A4 / A0,
 // A3 / A0.
-template <int NY>
-__global__ void __launch_bounds__(256, 2) k2s_3d(Ns3dArgs a) {
+template <int NY, int CT = 256>
+__global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) {
     using F = BFFT<NY>;
-    constexpr int T = F::T, E = F::E, C = Strided<NY>::C;
+    constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_in + C - 1) / C;
@@ -406,16 +406,16 @@ __device__ __forceinline__ void pack_pair(int t, const cd* p, const cd* q, cd* v
     }
 }
 
-// PF: the raw inputs of the next packed FFT are loaded into registers while
-// the current one runs (6 inverse FFTs per row pair, one exposed load).
-template <int NZ, bool PF>
+// CFL: also reduce max |u_d| (adaptive dt, stage 1 only; a separate
+// instantiation so the common path carries no extra registers).
+template <int NZ, bool CFL>
 __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E, G = Z3<NZ>::G;
     extern __shared__ cd smem[];
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const long long r0 = 2ll * ((long long)blockIdx.x * G + g);
-    const bool active = r0 < (long long)a.nrl * a.ny && !(a.opt & 16);
+    const bool active = r0 < (long long)a.nrl * a.ny;
     if (a.flags->diverged) return;
     cd* sm = smem + g * Z3<NZ>::SLOT;
     double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
@@ -426,23 +426,21 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     // input field pairs of the three packed inverse FFTs of a row
     const cd* FP[3] = {B + 2 * fs, B + 4 * fs, B + 0 * fs};
     const cd* FQ[3] = {B + 3 * fs, B + 5 * fs, B + 1 * fs};
-    if (active && !(a.opt & 2)) {  // the row pair of all six fields into L2 up front
+    if (active) {  // the row pair of all six fields into L2 up front
         const size_t bytes = sizeof(cd) * 2 * a.kz_in;
         for (int f = 0; f < 6; ++f)
             l2_prefetch(B + f * fs + (size_t)r0 * a.kz_in, bytes, t, T);
     }
-    const bool cfl = a.dyn && a.ystage == 1;  // max |u_d| of the step's initial state
+    constexpr bool cfl = CFL;  // max |u_d| of the step's initial state
     double mx = 0.0, my = 0.0, mz = 0.0;
     cd p[E], q[E];
-    if (PF) fetch_pair<NZ>(a, FP[0], FQ[0], (size_t)r0 * a.kz_in, active, t, p, q);
 #pragma unroll 1
     for (int rr = 0; rr < 2; ++rr) {
         const size_t row = (size_t)(r0 + rr) * a.kz_in;
         cd v[E];
         // w + i wx
-        if (!PF) fetch_pair<NZ>(a, FP[0], FQ[0], row, active, t, p, q);
+        fetch_pair<NZ>(a, FP[0], FQ[0], row, active, t, p, q);
         pack_pair<NZ>(t, p, q, v);
-        if (PF) fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -450,9 +448,8 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[1 * NZ + t + T * e] = v[e].y;
         }
         // wy + i wz
-        if (!PF) fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
+        fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
         pack_pair<NZ>(t, p, q, v);
-        if (PF) fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -460,16 +457,15 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[3 * NZ + t + T * e] = v[e].y;
         }
         // u + i v, then the cross product (solvers.cpp:321-325)
-        if (!PF) fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
+        fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
         pack_pair<NZ>(t, p, q, v);
-        if (PF && rr == 0) fetch_pair<NZ>(a, FP[0], FQ[0], row + a.kz_in, active, t, p, q);
         F::template run<+1>(v, sm, t, wb);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int y = t + T * e;
             const double ux = v[e].x, uy = v[e].y;
             const double uz = st[0 * NZ + y], ox = st[1 * NZ + y];
-            if (cfl) {
+            if constexpr (cfl) {
                 mx = fmax(mx, fabs(ux));
                 my = fmax(my, fabs(uy));
                 mz = fmax(mz, fabs(uz));
@@ -497,7 +493,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         }
         __syncthreads();
     }
-    if (cfl) umax_accumulate(a.dyn, 3, mx, my, mz);
+    if constexpr (cfl) umax_accumulate(a.dyn, 3, mx, my, mz);
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = mk(st[4 * NZ + t + T * e], st[0 * NZ + t + T * e]);
@@ -758,10 +754,15 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
     return cudaGetLastError();
 }
 
-// opt 128: 512-thread CTAs for the x passes (2x wider kz chunks)
+// 128-thread CTAs (fewer kz lanes, finer kz blocks) when 256-thread CTAs
+// would leave SMs idle (small grids)
 template <int NX>
 cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
-    if (a.opt & 128) return launch_x3_v<NX, 512>(a, stage, inverse, s);
+    constexpr int C = Strided<NX, 256>::C;
+    if constexpr (C > 1) {
+        const int kz = inverse ? a.kz_in : a.kz_o;
+        if (a.nkyl * ((kz + C - 1) / C) < a.wave) return launch_x3_v<NX, 128>(a, stage, inverse, s);
+    }
     return launch_x3_v<NX, 256>(a, stage, inverse, s);
 }
 
@@ -770,13 +771,13 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NY, CT>::C;
     using F = BFFT<NY>;
     const size_t smem = sizeof(cd) * F::SMEM * C + sizeof(int) * NY;  // + line offsets
-    if (inverse && CT == 256 && a.pruned && !(a.opt & 256)) {
+    if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
                               sizeof(int) * NY;
         static size_t done = 0;
-        set_smem(k2s_3d<NY>, smem_s, done);
+        set_smem(k2s_3d<NY, CT>, smem_s, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        k2s_3d<NY><<<grid, F::T * C, smem_s, s>>>(a);
+        k2s_3d<NY, CT><<<grid, F::T * C, smem_s, s>>>(a);
     } else if (inverse) {
         static size_t done = 0;
         set_smem(k2_3d<NY, CT>, smem, done);
@@ -791,28 +792,32 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// opt 64: 512-thread CTAs for the y passes
 template <int NY>
 cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
-    if (a.opt & 64) return launch_y3_v<NY, 512>(a, inverse, s);
+    constexpr int C = Strided<NY, 256>::C;
+    if constexpr (C > 1) {
+        const int kz = inverse ? a.kz_in : a.kz_o;
+        if (a.nrl * ((kz + C - 1) / C) < a.wave) return launch_y3_v<NY, 128>(a, inverse, s);
+    }
     return launch_y3_v<NY, 256>(a, inverse, s);
-}
-
-template <int NZ, bool PF>
-cudaError_t launch_z3_v(const Ns3dArgs& a, cudaStream_t s) {
-    using Z = Z3<NZ>;
-    const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
-    static size_t done = 0;
-    set_smem(k3_3d<NZ, PF>, smem, done);
-    const long long pairs = (long long)a.nrl * a.ny / 2;
-    const int grid = (int)((pairs + Z::G - 1) / Z::G);
-    k3_3d<NZ, PF><<<grid, Z::T * Z::G, smem, s>>>(a);
-    return cudaGetLastError();
 }
 
 template <int NZ>
 cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
-    return (a.opt & 1) ? launch_z3_v<NZ, true>(a, s) : launch_z3_v<NZ, false>(a, s);
+    using Z = Z3<NZ>;
+    const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
+    static size_t done = 0;
+    static size_t done_c = 0;
+    const long long pairs = (long long)a.nrl * a.ny / 2;
+    const int grid = (int)((pairs + Z::G - 1) / Z::G);
+    if (a.dyn && a.ystage == 1) {
+        set_smem(k3_3d<NZ, true>, smem, done_c);
+        k3_3d<NZ, true><<<grid, Z::T * Z::G, smem, s>>>(a);
+    } else {
+        set_smem(k3_3d<NZ, false>, smem, done);
+        k3_3d<NZ, false><<<grid, Z::T * Z::G, smem, s>>>(a);
+    }
+    return cudaGetLastError();
 }
 
 #define SKG3_CASES(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)

@@ -160,6 +160,7 @@ bool ns2d_supported(int nx, int ny);
 // C aliases A and D aliases B (each is dead when the other is produced).
 struct Ns3dArgs {
     int opt;                // tuning bits (SKG_OPT)
+    int wave;               // resident 256-thread CTAs (2 per SM)
     int nx, ny, nz, nh;
     int kcx, kcy, kcz;
     int pruned, has_sigma, rk2;

@@ -354,6 +354,7 @@ skg::Ns2dArgs args2d_part(skg_ctx* c, double dt, const Part& p) {
 skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     skg::Ns3dArgs a{};
     a.opt = env_opt();
+    a.wave = 2 * c->nsm;
     a.nx = c->n[0];
     a.ny = c->n[1];
     a.nz = c->n[2];
