@@ -140,7 +140,10 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
     const int ky = (NM == 2 ? a.c0 : 0) + kyl;
     const bool active = kyl < (NM == 2 ? a.ncols : a.ky_in);
     if (a.flags->diverged) return;
-    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
+    // step counter: here on the general path, in the stage-1 y pass on the
+    // fast path (whose x-inverse usually runs fused into the previous step)
+    if (NM == 4 && stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead)
+        atomicAdd(&a.flags->steps, 1);
     cd* sm = smem + l * (F::SMEM + NS * T);
     cd* sv = sm + F::SMEM;  // thread-private slots sv[slot * T + t]
     const double kyv = a.ky_scale * (double)ky;
@@ -458,6 +461,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     const int slot = F::SMEM + 2 * ld;
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     if (a.flags->diverged) return;
+    if (a.ystage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     cd* sm = smem + g * slot;
     cd* st = sm + F::SMEM;
     const typename F::Bases wb = F::bases(t, a.twy);
@@ -554,9 +558,14 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
 
 // x-forward of the two product spectra per kept ky column, combination
 // kx ky A + (kx^2 - ky^2) B, dealias + mean 0 + RK epilogue (as k4_xfwd).
-template <int NX, int EM = 16, int CTW = 256>
+// FUSE (next != 0): the same CTA then runs the NEXT stage's x-inverse of its
+// column (k1_xinv's body): the next stage state is formed in registers from
+// the tendency just computed (stage_combine, or the new u after the final
+// update = stage 1 of the next step), so k_j is not re-read, u is read once,
+// and one launch per stage disappears.
+template <int NX, int EM = 16, int CTW = 256, bool FUSE = false>
 __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB)
-    k4b_xfwd(Ns2dArgs a, int stage) {
+    k4b_xfwd(Ns2dArgs a, int stage, int next) {
     using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
     constexpr int LPC = XCfg<NX, EM, CTW>::LPC;
@@ -603,6 +612,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
         const cd u0 = a.u[(size_t)kyl * NX];  // mean mode: untouched, enstrophy only
         sZ += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
     }
+    const bool fuse = FUSE && next;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         if (!active) break;
@@ -610,12 +620,17 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
         const int slot = e < ZLO ? e : e - (ZHI - ZLO);
         const int i = t + T * e;
         const int si = signed_index(i, NX);
-        if (abs(si) > a.kcx || (i == 0 && ky == 0)) continue;
+        if (abs(si) > a.kcx || (i == 0 && ky == 0)) {
+            if (fuse) sv[slot * T + t] = zero();  // psi of the next stage: 0 here
+            continue;
+        }
         const double kxv = a.kx_scale * (double)si;
         const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
         const size_t idx = (size_t)kyl * NX + i;
+        cd wn = zero();  // next stage state (fused)
         if (!final) {
             kout[idx] = kv;
+            if (fuse) wn = stage_combine(a, stage + 1, ky, i, a.u[idx], kv);
         } else {
             const cd u = a.u[idx];
             cd un;
@@ -640,6 +655,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
                 un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
             }
             a.u[idx] = un;
+            wn = un;  // stage 1 of the next step
             bad |= !finite2(un);
             if (a.diag) {
                 const double ksq = kxv * kxv + kyv * kyv;
@@ -652,12 +668,44 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
                 }
             }
         }
+        if (fuse) {  // psi = w / |k|^2 of the next stage (k1_xinv prologue)
+            const double ksq = kxv * kxv + kyv * kyv;
+            const double r = __drcp_rn(ksq);  // ksq > 0: the mean mode was skipped
+            sv[slot * T + t] = mk(wn.x * r, wn.y * r);
+        }
     }
     if (final && a.diag) diag_accumulate(a.diag + 3 * (a.flags->steps - 1), sE, sZ, sD);
     if (bad) {
         atomicMin(&a.flags->div_var, 0);
         atomicExch(&a.flags->div_step, a.flags->steps);
         atomicExch(&a.flags->diverged, 1);
+    }
+    if constexpr (FUSE) {
+        if (!next) return;
+        // next stage's x-inverse of this column: X[psi], X[kx psi] (k1_xinv, NM = 2)
+#pragma unroll 1
+        for (int m = 0; m < 2; ++m) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (e >= ZLO && e < ZHI) {
+                    v[e] = zero();
+                    continue;
+                }
+                const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+                const cd psi = sv[slot * T + t];
+                v[e] = m == 0 ? psi : scale(psi, a.kx_scale * (double)signed_index(t + T * e, NX));
+            }
+            F::template run<+1>(v, sm, t, wb);
+            if (active) {
+                cd* out = a.sI[m];
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int x = t + T * e;
+                    const int q = x >> a.lg_nrl, xl = x & (a.nrl - 1);
+                    out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG)] = v[e];
+                }
+            }
+        }
     }
 }
 
@@ -751,10 +799,11 @@ cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
 template <int NX>
 constexpr int fast_em() { return NX >= 4096 ? SKG_FAST_X_EM : 16; }
 
-template <int NX, int CTW>
-cudaError_t launch_fast_x_w(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+// mode 0: x-inverse (k1_xinv); 1: x-forward + RK; 2: x-forward + RK fused
+// with the next stage's x-inverse.
+template <int NX, int CTW, bool FUSE>
+cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     constexpr int EM = fast_em<NX>();
-    if (inverse) return launch_k1<NX, true, 2, EM, CTW>(a, stage, s);
     using C = XCfg<NX, EM, CTW>;
     using F = typename C::F;
     constexpr int T = F::T;
@@ -762,24 +811,33 @@ cudaError_t launch_fast_x_w(const Ns2dArgs& a, int stage, bool inverse, cudaStre
     const size_t smem = sizeof(cd) * (F::SMEM + (F::E - (C::ZHI - C::ZLO)) * T) * LPC;
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k4b_xfwd<NX, EM, CTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k4b_xfwd<NX, EM, CTW, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         init = true;
     }
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    k4b_xfwd<NX, EM, CTW><<<grid, T * LPC, smem, s>>>(a, stage);
+    k4b_xfwd<NX, EM, CTW, FUSE><<<grid, T * LPC, smem, s>>>(a, stage, FUSE ? 1 : 0);
     return cudaGetLastError();
+}
+
+template <int NX, int CTW>
+cudaError_t launch_fast_x_w(const Ns2dArgs& a, int stage, int mode, cudaStream_t s) {
+    constexpr int EM = fast_em<NX>();
+    if (mode == 0) return launch_k1<NX, true, 2, EM, CTW>(a, stage, s);
+    if (mode == 2) return launch_k4b<NX, CTW, true>(a, stage, s);
+    return launch_k4b<NX, CTW, false>(a, stage, s);
 }
 
 // Narrow CTAs (one column each) when 256-thread CTAs would leave SMs idle.
 template <int NX>
-cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, int mode, cudaStream_t s) {
     constexpr int EM = fast_em<NX>();
     constexpr int LPC = XCfg<NX, EM>::LPC;
     if constexpr (LPC > 1) {
-        if ((a.ncols + LPC - 1) / LPC < a.wave) return launch_fast_x_w<NX, 1>(a, stage, inverse, s);
+        if ((a.ncols + LPC - 1) / LPC < a.wave) return launch_fast_x_w<NX, 1>(a, stage, mode, s);
     }
-    return launch_fast_x_w<NX, 256>(a, stage, inverse, s);
+    return launch_fast_x_w<NX, 256>(a, stage, mode, s);
 }
 
 #define SKG_POW2_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
@@ -805,10 +863,10 @@ cudaError_t dispatch_y(const Ns2dArgs& a, cudaStream_t s) {
     }
 }
 
-cudaError_t dispatch_fast_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
+cudaError_t dispatch_fast_x(const Ns2dArgs& a, int stage, int mode, cudaStream_t s) {
     switch (a.nx) {
 #define CASE(N) \
-    case N: return launch_fast_x<N>(a, stage, inverse, s);
+    case N: return launch_fast_x<N>(a, stage, mode, s);
         SKG_FAST_CASES(CASE)
 #undef CASE
         default: return cudaErrorInvalidValue;
@@ -845,7 +903,7 @@ bool ns2d_supported(int nx, int ny) {
 bool ns2d_fast_ok(const Ns2dArgs& a) { return fast_ok(a); }
 
 cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
-                           const LaunchHook& hook) {
+                           const LaunchHook& hook, int next) {
     cudaError_t err;
     const double B = sizeof(cd);
     const bool final = a.rk2 ? stage == 2 : stage == 4;
@@ -853,7 +911,7 @@ cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t 
     const double Kc = a.kcy + 1.0;
     if (pass == 0) {
         hook.begin(0);
-        err = dispatch_fast_x(a, stage, true, s);
+        err = dispatch_fast_x(a, stage, 0, s);
         hook.end(0, B * (kept * (stage == 1 ? 1.0 : 2.0) + 2.0 * a.nx * a.ncols));
     } else if (pass == 1) {
         hook.begin(1);
@@ -861,10 +919,14 @@ cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t 
         b.ystage = stage;
         err = dispatch_fast_y(b, s);
         hook.end(1, B * (4.0 * a.nrl * Kc));
-    } else {
+    } else if (pass == 2 || !next) {
         hook.begin(2);
-        err = dispatch_fast_x(a, stage, false, s);
+        err = dispatch_fast_x(a, stage, 1, s);
         hook.end(2, B * (2.0 * a.nx * a.ncols + (final ? (a.rk2 ? 3.0 : 5.0) : 1.0) * kept));
+    } else {  // pass 3: x-forward + RK fused with the next stage's x-inverse
+        hook.begin(2);
+        err = dispatch_fast_x(a, stage, 2, s);
+        hook.end(2, B * (4.0 * a.nx * a.ncols + (final ? (a.rk2 ? 3.0 : 5.0) : 2.0) * kept));
     }
     ++*launches;
     return err;

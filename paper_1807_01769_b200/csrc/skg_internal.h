@@ -146,8 +146,11 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
 // The three passes of the fast path separately (slab decomposition):
 // pass 0 x-inverse, 1 y pass, 2 x-forward + RK.
 bool ns2d_fast_ok(const Ns2dArgs& a);
+// Dealiased-path passes: 0 x-inverse, 1 y pass, 2 x-forward + RK,
+// 3 x-forward + RK fused with the x-inverse of the next stage (next != 0;
+// after the final stage: stage 1 of the next step).
 cudaError_t ns2d_fast_pass(const Ns2dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
-                           const LaunchHook& hook);
+                           const LaunchHook& hook, int next = 0);
 bool ns2d_supported(int nx, int ny);
 
 // ---------------------------------------------------------------- ns3d

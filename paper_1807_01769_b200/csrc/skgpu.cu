@@ -169,6 +169,7 @@ struct skg_ctx {
     double cfl = 0.5, dt_max = 0.1, t_end = -1.0, last_dt = 0.0;
     skg::DynStep* d_dyn = nullptr;
     double g_dt = 0.0;
+    long g_launches = 0;
     bool g_pruned = false;
     cudaStream_t g_stream = nullptr;
 };
@@ -610,35 +611,54 @@ int exchange3(skg_ctx* c, int which) {
     return SKG_OK;
 }
 
-int enqueue_dist_step(skg_ctx* c, double dt, long* counter) {
+int dist_dt_update(skg_ctx* c, long* counter) {
+    if (c->comm) {  // global max |u_d| over the ranks' x rows
+        const ncclResult_t nr = ncclAllReduce(c->d_dyn->umax, c->d_dyn->umax, 3, ncclDouble, ncclMax,
+                                              c->comm, c->stream);
+        if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+    }
+    CUDA_TRY(skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale, c->nu,
+                                   c->stream, counter));
+    return SKG_OK;
+}
+
+// One step of a slab-decomposed context.  ns2d: the x-forward of every stage
+// runs fused with the next stage's x-inverse (first: the step opens the
+// batch and runs its own stage-1 x-inverse; last: no next stage).
+int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool last) {
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
-    for (int st = 1; st <= nst; ++st) {
-        for (int pass = 0; pass < 3; ++pass) {
-            for (const Part& p : c->parts) {
-                if (c->solver == 3) {
+    int rc;
+    if (c->solver == 3) {
+        for (int st = 1; st <= nst; ++st) {
+            for (int pass = 0; pass < 3; ++pass) {
+                for (const Part& p : c->parts) {
                     skg::Ns3dArgs a = args3d_part(c, dt, p);
                     CUDA_TRY(skg::ns3d_pass(a, pass, st, c->stream, counter, hook));
-                    continue;
                 }
-                skg::Ns2dArgs a = args2d_part(c, dt, p);
-                a.lead = p.r == 0 ? 1 : 0;
-                CUDA_TRY(skg::ns2d_fast_pass(a, pass, st, c->stream, counter, hook));
+                if (pass < 2 && (rc = exchange(c, pass))) return rc;
             }
-            if (pass < 2) {
-                int rc = exchange(c, pass);
-                if (rc) return rc;
-            }
+            if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;
         }
-        if (st == 1 && c->adaptive) {
-            if (c->comm) {  // global max |u_d| over the ranks' x rows
-                const ncclResult_t nr = ncclAllReduce(c->d_dyn->umax, c->d_dyn->umax, 3, ncclDouble,
-                                                      ncclMax, c->comm, c->stream);
-                if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
-            }
-            CUDA_TRY(skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale,
-                                           c->nu, c->stream, counter));
+        return SKG_OK;
+    }
+    auto run_pass = [&](int pass, int st, int next) -> int {
+        for (const Part& p : c->parts) {
+            skg::Ns2dArgs a = args2d_part(c, dt, p);
+            a.lead = p.r == 0 ? 1 : 0;
+            CUDA_TRY(skg::ns2d_fast_pass(a, pass, st, c->stream, counter, hook, next));
         }
+        return SKG_OK;
+    };
+    if (first) {
+        if ((rc = run_pass(0, 1, 0)) || (rc = exchange(c, 0))) return rc;
+    }
+    for (int st = 1; st <= nst; ++st) {
+        if ((rc = run_pass(1, st, 0)) || (rc = exchange(c, 1))) return rc;
+        if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;
+        const int next = st < nst || !last;
+        if ((rc = run_pass(3, st, next))) return rc;
+        if (next && (rc = exchange(c, 0))) return rc;
     }
     return SKG_OK;
 }
@@ -666,26 +686,41 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
-    long launches_per_step = 0;
     if (c->dist) {
         for (long s = 0; s < nsteps; ++s) {
-            int rc2 = enqueue_dist_step(c, dt, &c->launches);
+            int rc2 = enqueue_dist_step(c, dt, &c->launches, s == 0, s == nsteps - 1);
             if (rc2) return rc2;
         }
         return SKG_OK;
     }
-    auto one_step = [&](long* counter) -> cudaError_t {
+    // first: the step opens the batch; last: it closes it.  On the ns2d fast
+    // path the x-forward of each stage is fused with the next stage's
+    // x-inverse (across the step boundary too), so only the batch's first
+    // step runs a standalone x-inverse and the last one no trailing one.
+    auto one_step = [&](long* counter, bool first, bool last) -> cudaError_t {
         cudaError_t e = cudaSuccess;
         bool fused = false;
+        auto dt_update = [&]() {
+            return skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale, c->nu,
+                                         c->stream, counter);
+        };
         if (c->solver == 2) {
             skg::Ns2dArgs a = args2d(c, dt);
             fused = skg::ns2d_fast_ok(a);
             if (!fused) a.diag = nullptr;
-            for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
-                e = skg::ns2d_launch_stage(a, st, c->stream, counter, hook);
-                if (st == 1 && c->adaptive && e == cudaSuccess)
-                    e = skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale,
-                                              c->nu, c->stream, counter);
+            if (fused) {
+                if (first) e = skg::ns2d_fast_pass(a, 0, 1, c->stream, counter, hook);
+                for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                    e = skg::ns2d_fast_pass(a, 1, st, c->stream, counter, hook);
+                    if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+                    if (e == cudaSuccess)
+                        e = skg::ns2d_fast_pass(a, 3, st, c->stream, counter, hook, st < nst || !last);
+                }
+            } else {
+                for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                    e = skg::ns2d_launch_stage(a, st, c->stream, counter, hook);
+                    if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+                }
             }
         } else {
             skg::Ns3dArgs a = args3d(c, dt);
@@ -693,9 +728,7 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             if (!fused) a.diag = nullptr;
             for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
                 e = skg::ns3d_launch_stage(a, st, c->stream, counter, hook);
-                if (st == 1 && c->adaptive && e == cudaSuccess)
-                    e = skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale,
-                                              c->nu, c->stream, counter);
+                if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
             }
         }
         if (e == cudaSuccess && c->diag && !fused)  // unfused paths: one reduction per step
@@ -705,12 +738,11 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     };
     long s = 0;
     if (nsteps > 0) {  // first step eagerly (also sets kernel attributes)
-        const long before = c->launches;
-        CUDA_TRY(one_step(&c->launches));
-        launches_per_step = c->launches - before;
+        CUDA_TRY(one_step(&c->launches, true, nsteps == 1));
         s = 1;
     }
-    if (nsteps - s >= 2 && !c->timing && c->stream != nullptr) {
+    // middle steps: replay of a captured step; the last step eagerly
+    if (nsteps - s >= 3 && !c->timing && c->stream != nullptr) {
         if (c->gexec && (c->g_dt != dt || c->g_pruned != c->pruned || c->g_stream != c->stream ||
                          c->g_diag != c->diag)) {
             cudaGraphExecDestroy(c->gexec);
@@ -720,23 +752,24 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             cudaGraph_t graph;
             long dummy = 0;
             CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-            cudaError_t e = one_step(&dummy);
+            cudaError_t e = one_step(&dummy, false, false);
             cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
             CUDA_TRY(e);
             CUDA_TRY(e2);
             CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
             cudaGraphDestroy(graph);
+            c->g_launches = dummy;
             c->g_dt = dt;
             c->g_diag = c->diag;
             c->g_pruned = c->pruned;
             c->g_stream = c->stream;
         }
-        for (; s < nsteps; ++s) {
+        for (; s < nsteps - 1; ++s) {
             CUDA_TRY(cudaGraphLaunch(c->gexec, c->stream));
-            c->launches += launches_per_step;
+            c->launches += c->g_launches;
         }
     }
-    for (; s < nsteps; ++s) CUDA_TRY(one_step(&c->launches));
+    for (; s < nsteps; ++s) CUDA_TRY(one_step(&c->launches, false, s == nsteps - 1));
     return SKG_OK;
 }
 
