@@ -58,8 +58,11 @@ def launches(path: Path, out: Path):
 
 
 def report(rep: Path, out: Path):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.suffix == ".csv":  # `ncu -i … --page raw --csv` captured on the GPU box
+        txt = rep.read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
@@ -90,7 +93,7 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--config", required=True)
     ap.add_argument("--launches")
-    ap.add_argument("--report")
+    ap.add_argument("--report", help=".ncu-rep, or its raw page as CSV")
     ap.add_argument("--dominant", help="kernel name prefix of the roofline kernel")
     a = ap.parse_args()
     PROF.mkdir(exist_ok=True)
