@@ -158,9 +158,14 @@ def cpu_reference_rate(solver, n, nu, dt, u0, steps, warmup, threads):
     ref.set_workers(threads)
     r = ref.RefSimulation(solver, n, nu, dt)
     r.set_state(u0)
-    if warmup:
-        r.step(warmup)
-    times = [r.step(1) for _ in range(steps)]
+    t_warm = r.step(warmup) if warmup else 0.0
+    # bounded sample (~10-30 s of CPU work): fewer timed steps when one step
+    # is long (ns3d 512^3: ~30 s per step)
+    times = []
+    while len(times) < steps and sum(times) + (times[-1] if times else t_warm) <= 30.0:
+        times.append(r.step(1))
+    if not times:
+        times.append(t_warm)  # the warm-up step itself is the sample
     r.close()
     return times
 
@@ -342,7 +347,7 @@ def run_our_arm(args):
             times = cpu_reference_rate(solver, n, nu, dt, u0, args.cpu_steps, 1, threads)
             sec = sum(times) / len(times)
             cpu = {"value": P / sec / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"{args.cpu_steps} step_once of {args.config} after 1 warm-up "
+                   "sample": f"{len(times)} step_once of {args.config} after 1 warm-up "
                              f"({sec:.2f} s/step); reference proj/src compiled unmodified, "
                              f"FFT = oracle/fft_shim.c (FFTW absent), {threads} threads"}
         except Exception as exc:  # the oracle .so may be missing on a foreign box

@@ -182,8 +182,8 @@ long skg_launch_count(const skg_ctx* ctx);
 /* Per-kernel-class device timing for the roofline report: when enabled,
  * CUDA events bracket every hot-path launch on the context stream.
  * Classes: 0 x-inverse pass, 1 physical-space pass, 2 x-forward pass + RK,
- * 3 other (3D y passes, decay, utilities), 4 all-to-all exchange (bytes =
- * bytes sent to other ranks).  skg_kernel_stats returns the
+ * 3 y-inverse pass (3D) and other (decay), 4 all-to-all exchange (bytes =
+ * bytes sent to other ranks), 5 y-forward pass (3D).  skg_kernel_stats returns the
  * accumulated device milliseconds, launch count and ALGORITHMIC bytes (the
  * HBM bytes the kernel must move: fields crossing the pass boundary, read or
  * written once) of one class since the last reset. */

@@ -381,7 +381,7 @@ class Simulation:
     def launch_count(self) -> int:
         return load_library().skg_launch_count(self._h)
 
-    KERNEL_CLASSES = ("x_inverse", "physical", "x_forward_rk", "other", "exchange")
+    KERNEL_CLASSES = ("x_inverse", "physical", "x_forward_rk", "y_inverse", "exchange", "y_forward")
 
     def set_timing(self, on: bool) -> None:
         self._call("skg_set_timing", C.c_int(1 if on else 0))

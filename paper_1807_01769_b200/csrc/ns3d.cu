@@ -886,9 +886,9 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
         hook.begin(1);
         if ((err = dispatch_z3(b, s)) != cudaSuccess) return err;
         hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
-        hook.begin(3);
+        hook.begin(5);
         if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;
-        hook.end(3, B * (3.0 * plane_o + 3.0 * a.nrl * kyk * a.kz_o));
+        hook.end(5, B * (3.0 * plane_o + 3.0 * a.nrl * kyk * a.kz_o));
         *launches += 3;
     } else {
         hook.begin(2);

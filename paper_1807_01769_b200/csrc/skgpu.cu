@@ -154,9 +154,9 @@ struct skg_ctx {
     std::vector<cudaEvent_t> pool;
     std::vector<Pending> pend;
     cudaEvent_t cur = nullptr;
-    double st_ms[5] = {0, 0, 0, 0, 0};
-    long st_n[5] = {0, 0, 0, 0, 0};
-    double st_bytes[5] = {0, 0, 0, 0, 0};
+    double st_ms[6] = {0, 0, 0, 0, 0, 0};
+    long st_n[6] = {0, 0, 0, 0, 0, 0};
+    double st_bytes[6] = {0, 0, 0, 0, 0, 0};
 
     // CUDA graph of one RK step (all stage kernels), replayed per step when
     // timing is off; recaptured when dt, the fast-path decision or the
@@ -1474,7 +1474,7 @@ int skg_reset_stats(skg_ctx* c) {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     harvest(c);
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < 6; ++i) {
         c->st_ms[i] = 0;
         c->st_n[i] = 0;
         c->st_bytes[i] = 0;
@@ -1483,7 +1483,7 @@ int skg_reset_stats(skg_ctx* c) {
 }
 
 int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, double* bytes) {
-    if (cls < 0 || cls > 4) return fail(SKG_ESHAPE, "kernel class out of range");
+    if (cls < 0 || cls > 5) return fail(SKG_ESHAPE, "kernel class out of range");
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     harvest(c);
