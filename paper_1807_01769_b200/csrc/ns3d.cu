@@ -555,7 +555,9 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
 // Components 0 and 1 are written back raw into their own D lines (in place,
 // L2-resident) and re-read by the same thread for the projection, so no
 // shared-memory slots are needed.
-template <int NX, int CT = 256>
+// FIN: final-stage instantiation (RK update, diagnostics); the other stages
+// run a leaner one that only stores k_j.
+template <int NX, int CT = 256, bool FIN = false>
 __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, int stage) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E, C = Strided<NX, CT>::C;
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
             for (int e = 0; e < E; ++e) line[(size_t)(t + T * e) * xstr] = v[e];
         }
     }
-    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    constexpr bool final = FIN;
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     const double kyv = a.ky_scale * (double)sky;
     const double kzv = a.kz_scale * (double)kz;
@@ -747,9 +749,15 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
     } else {
         const size_t smem = sizeof(cd) * F::SMEM * C;
         static size_t done = 0;
-        set_smem(k4_3d<NX, CT>, smem, done);
         const int grid = a.nkyl * ((a.kz_o + C - 1) / C);
-        k4_3d<NX, CT><<<grid, F::T * C, smem, s>>>(a, stage);
+        if (a.rk2 ? stage == 2 : stage == 4) {
+            static size_t done_f = 0;
+            set_smem(k4_3d<NX, CT, true>, smem, done_f);
+            k4_3d<NX, CT, true><<<grid, F::T * C, smem, s>>>(a, stage);
+        } else {
+            set_smem(k4_3d<NX, CT, false>, smem, done);
+            k4_3d<NX, CT, false><<<grid, F::T * C, smem, s>>>(a, stage);
+        }
     }
     return cudaGetLastError();
 }
