@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
     const int kyl = blockIdx.x * LPC + l;
     const int ky = (NM == 2 ? a.c0 : 0) + kyl;
     const bool active = kyl < (NM == 2 ? a.ncols : a.ky_in);
+    pdl_wait();
     if (a.flags->diverged) return;
     // step counter: here on the general path, in the stage-1 y pass on the
     // fast path (whose x-inverse usually runs fused into the previous step)
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const int xa = 2 * (blockIdx.x * G + g);
     const bool active = xa < a.nx;
+    pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + g * slot;
     double* prow = reinterpret_cast<double*>(sm + F::SMEM);
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(256, 2) k4_xfwd(Ns2dArgs a, int stage) {
     const int l = threadIdx.x / T, t = threadIdx.x % T;
     const int ky = blockIdx.x * LPC + l;
     const bool active = ky < a.ld_o;
+    pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + l * F::SMEM;
     cd v[E];
@@ -413,6 +416,7 @@ __global__ void __launch_bounds__(256, 2) k4_xfwd(Ns2dArgs a, int stage) {
 // Unpruned final update of the ky columns above the cut: tendency is zero
 // there, so u <- E2 u (time_stepping.cpp:186-192 with k = 0).
 __global__ void k4_decay(Ns2dArgs a) {
+    pdl_wait();
     if (a.flags->diverged) return;
     const size_t cols = (size_t)(a.nh - (a.kcy + 1));
     const size_t total = cols * a.nx;
@@ -460,6 +464,7 @@ __global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
     const int ld = a.ld_i;
     const int slot = F::SMEM + 2 * ld;
     const int g = threadIdx.x / T, t = threadIdx.x % T;
+    pdl_wait();
     if (a.flags->diverged) return;
     if (a.ystage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     cd* sm = smem + g * slot;
@@ -575,6 +580,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
     const int kyl = blockIdx.x * LPC + l;  // local column
     const int ky = a.c0 + kyl;
     const bool active = kyl < a.ncols;
+    pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + l * (F::SMEM + NS * T);
     cd* sv = sm + F::SMEM;
@@ -724,7 +730,7 @@ cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
         cudaFuncSetAttribute(k1_xinv<NX, PZ, NM, EM, CTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    k1_xinv<NX, PZ, NM, EM, CTW><<<grid, T * LPC, smem, s>>>(a, stage);
+    if (cudaError_t e_ = launch_pdl(k1_xinv<NX, PZ, NM, EM, CTW>, dim3(grid), dim3(T * LPC), smem, s, a, stage); e_ != cudaSuccess) return e_;
     return cudaGetLastError();
 }
 
@@ -747,7 +753,7 @@ cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s)
         cudaFuncSetAttribute(k4_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    k4_xfwd<NX><<<grid, T * LPC, smem, s>>>(a, stage);
+    if (cudaError_t e_ = launch_pdl(k4_xfwd<NX>, dim3(grid), dim3(T * LPC), smem, s, a, stage); e_ != cudaSuccess) return e_;
     return cudaGetLastError();
 }
 
@@ -765,7 +771,7 @@ cudaError_t launch_y_v(const Ns2dArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(k3_phys<NY, EM, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = smem;
     }
-    k3_phys<NY, EM, CFL><<<grid, T * G, smem, s>>>(a);
+    if (cudaError_t e_ = launch_pdl(k3_phys<NY, EM, CFL>, dim3(grid), dim3(T * G), smem, s, a); e_ != cudaSuccess) return e_;
     return cudaGetLastError();
 }
 
@@ -786,7 +792,7 @@ cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
     }
     const int groups = (a.nrl + G - 1) / G;
     const int grid = groups < a.wave ? groups : a.wave;
-    k3b_phys<NY, CFL><<<grid, F::T * G, smem, s>>>(a);
+    if (cudaError_t e_ = launch_pdl(k3b_phys<NY, CFL>, dim3(grid), dim3(F::T * G), smem, s, a); e_ != cudaSuccess) return e_;
     return cudaGetLastError();
 }
 
@@ -817,7 +823,7 @@ cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     }
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    k4b_xfwd<NX, EM, CTW, FUSE><<<grid, T * LPC, smem, s>>>(a, stage, FUSE ? 1 : 0);
+    if (cudaError_t e_ = launch_pdl(k4b_xfwd<NX, EM, CTW, FUSE>, dim3(grid), dim3(T * LPC), smem, s, a, stage, FUSE ? 1 : 0); e_ != cudaSuccess) return e_;
     return cudaGetLastError();
 }
 
@@ -961,7 +967,7 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
     *launches += 3;
     if (final && !a.pruned && a.nh > a.kcy + 1) {
         hook.begin(3);
-        k4_decay<<<296, 256, 0, s>>>(a);
+        if (cudaError_t e_ = launch_pdl(k4_decay, dim3(296), dim3(256), 0, s, a); e_ != cudaSuccess) return e_;
         hook.end(3, B * 2.0 * a.nx * (a.nh - a.kcy - 1));
         *launches += 1;
         if ((err = cudaGetLastError()) != cudaSuccess) return err;

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
     const int kyi = a.kys + blockIdx.x / nkzb;
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_in;
+    pdl_wait();
     if (a.flags->diverged) return;
     if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     const int ky = ky_of(a, kyi);
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
     const int x = blockIdx.x / nkzb;
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_in;
+    pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
@@ -296,6 +298,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
     const int kz0 = (blockIdx.x % nkzb) * C;
     const int kz = kz0 + l;
     const bool active = kz < a.kz_in;
+    pdl_wait();
     if (a.flags->diverged) return;
     const int K = 2 * a.kcy + 1;  // kept lines
     cd* sm = smem + l * F::SMEM;
@@ -416,6 +419,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const long long r0 = 2ll * ((long long)blockIdx.x * G + g);
     const bool active = r0 < (long long)a.nrl * a.ny;
+    pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + g * Z3<NZ>::SLOT;
     double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
@@ -524,6 +528,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
     const int x = blockIdx.x / nkzb;
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_o;
+    pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
@@ -567,6 +572,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     const int kyi = a.kys + blockIdx.x / nkzb;
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_o;
+    pdl_wait();
     if (a.flags->diverged) return;
     const int ky = ky_of(a, kyi);
     const int ys = a.slab ? kyi - a.kys : ky;
@@ -685,6 +691,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
 
 // Unpruned final update of the kz planes above the cut (tendency zero there).
 __global__ void k4_3d_decay(Ns3dArgs a) {
+    pdl_wait();
     if (a.flags->diverged) return;
     const int nk = a.nh - a.kz_o;
     const size_t total = (size_t)a.nx * a.ny * nk;
@@ -734,14 +741,14 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
                 const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - 4) * F::T * C);
                 static size_t done = 0;
                 set_smem(k1_3d<NX, true, CT>, smem, done);
-                k1_3d<NX, true, CT><<<grid, F::T * C, smem, s>>>(a, stage);
+                if (cudaError_t e_ = launch_pdl(k1_3d<NX, true, CT>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
             }
         } else {
             if constexpr (CT == 256) {
                 const size_t smem = sizeof(cd) * (F::SMEM * C + F::E * F::T * C);
                 static size_t done = 0;
                 set_smem(k1_3d<NX, false>, smem, done);
-                k1_3d<NX, false><<<grid, F::T * C, smem, s>>>(a, stage);
+                if (cudaError_t e_ = launch_pdl(k1_3d<NX, false>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
             } else {
                 return launch_x3_v<NX, 256>(a, stage, inverse, s);
             }
@@ -753,10 +760,10 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
         if (a.rk2 ? stage == 2 : stage == 4) {
             static size_t done_f = 0;
             set_smem(k4_3d<NX, CT, true>, smem, done_f);
-            k4_3d<NX, CT, true><<<grid, F::T * C, smem, s>>>(a, stage);
+            if (cudaError_t e_ = launch_pdl(k4_3d<NX, CT, true>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
         } else {
             set_smem(k4_3d<NX, CT, false>, smem, done);
-            k4_3d<NX, CT, false><<<grid, F::T * C, smem, s>>>(a, stage);
+            if (cudaError_t e_ = launch_pdl(k4_3d<NX, CT, false>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
         }
     }
     return cudaGetLastError();
@@ -785,17 +792,17 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
         static size_t done = 0;
         set_smem(k2s_3d<NY, CT>, smem_s, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        k2s_3d<NY, CT><<<grid, F::T * C, smem_s, s>>>(a);
+        if (cudaError_t e_ = launch_pdl(k2s_3d<NY, CT>, dim3(grid), dim3(F::T * C), smem_s, s, a); e_ != cudaSuccess) return e_;
     } else if (inverse) {
         static size_t done = 0;
         set_smem(k2_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        k2_3d<NY, CT><<<grid, F::T * C, smem, s>>>(a);
+        if (cudaError_t e_ = launch_pdl(k2_3d<NY, CT>, dim3(grid), dim3(F::T * C), smem, s, a); e_ != cudaSuccess) return e_;
     } else {
         static size_t done = 0;
         set_smem(k2f_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_o + C - 1) / C);
-        k2f_3d<NY, CT><<<grid, F::T * C, smem, s>>>(a);
+        if (cudaError_t e_ = launch_pdl(k2f_3d<NY, CT>, dim3(grid), dim3(F::T * C), smem, s, a); e_ != cudaSuccess) return e_;
     }
     return cudaGetLastError();
 }
@@ -820,10 +827,10 @@ cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
     if (a.dyn && a.ystage == 1) {
         set_smem(k3_3d<NZ, true>, smem, done_c);
-        k3_3d<NZ, true><<<grid, Z::T * Z::G, smem, s>>>(a);
+        if (cudaError_t e_ = launch_pdl(k3_3d<NZ, true>, dim3(grid), dim3(Z::T * Z::G), smem, s, a); e_ != cudaSuccess) return e_;
     } else {
         set_smem(k3_3d<NZ, false>, smem, done);
-        k3_3d<NZ, false><<<grid, Z::T * Z::G, smem, s>>>(a);
+        if (cudaError_t e_ = launch_pdl(k3_3d<NZ, false>, dim3(grid), dim3(Z::T * Z::G), smem, s, a); e_ != cudaSuccess) return e_;
     }
     return cudaGetLastError();
 }
@@ -906,7 +913,7 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
         *launches += 1;
         if (final && !a.pruned && a.nh > a.kz_o) {
             hook.begin(3);
-            k4_3d_decay<<<592, 256, 0, s>>>(a);
+            if (cudaError_t e_ = launch_pdl(k4_3d_decay, dim3(592), dim3(256), 0, s, a); e_ != cudaSuccess) return e_;
             hook.end(3, B * 6.0 * a.nx * a.ny * (a.nh - a.kz_o));
             *launches += 1;
             if ((err = cudaGetLastError()) != cudaSuccess) return err;

@@ -99,6 +99,7 @@ struct EnGeo {
 // Solver::mode_energy of simulation.cpp:163-170).
 __global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long long S,
                               double* out, const int* steps) {
+    pdl_wait();
     if (steps) out += 3 * (*steps - 1);  // per-step series slot
     double e = 0.0, z = 0.0, d = 0.0;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < S;
@@ -147,6 +148,7 @@ struct DtGeo {
 // Simulation::compute_dt (CFL branch, simulation.cpp:463-476) and
 // ExactLinStepper::refresh_exp (time_stepping.cpp:37-57) for the new dt.
 __global__ void dt_update(DynStep* dyn, DevFlags* flags, double* etab, DtGeo g) {
+    pdl_wait();
     if (flags->diverged) return;
     double dt = dyn->dt_max;
     for (int d = 0; d < g.dims; ++d) {
@@ -237,7 +239,7 @@ cudaError_t launch_dt_update(DynStep* dyn, DevFlags* flags, double* etab, int di
         g.ks[d] = kscale[d];
     }
     g.nu = nu;
-    dt_update<<<1, 256, 0, s>>>(dyn, flags, etab, g);
+    if (cudaError_t e_ = launch_pdl(dt_update, dim3(1), dim3(256), 0, s, dyn, flags, etab, g); e_ != cudaSuccess) return e_;
     ++*launches;
     return cudaGetLastError();
 }
@@ -254,7 +256,7 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
     long long S = 1;
     for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.m.nh : n[d]);
     if (zero_first) cudaMemsetAsync(d_out, 0, 3 * sizeof(double), s);
-    energy_kernel<<<592, 256, 0, s>>>(f, g, nvars, S, d_out, steps);
+    if (cudaError_t e_ = launch_pdl(energy_kernel, dim3(592), dim3(256), 0, s, f, g, nvars, S, d_out, steps); e_ != cudaSuccess) return e_;
     ++*launches;
     return cudaGetLastError();
 }
