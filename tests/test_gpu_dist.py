@@ -143,3 +143,29 @@ def test_compact_layout_rejects_undealiased_state():
     c = api.Simulation("ns3d", n, 1e-3, 1e-3, compact=True)
     with pytest.raises(api.UnsupportedError):
         c.set_state(v)
+
+
+def test_nccl_single_rank_communicator():
+    """The NCCL plumbing on one GPU: a 1-rank communicator (ncclCommInitRank,
+    the all-reduce of the state gather and of the CFL maxima) on the compact
+    ns3d layout; ranks that wait on each other are never co-located."""
+    n = (32, 32, 32)
+    u0 = ic.ns3d_ic(n, seed=12)
+    one = api.Simulation("ns3d", n, 1e-3, 1e-3)
+    one.set_state(u0)
+    one.step(3)
+    d = api.Simulation("ns3d", n, 1e-3, 1e-3, world=1, rank=0, nccl_id=api.nccl_unique_id(),
+                       compact=True)
+    d.set_state(u0)
+    d.step(3)
+    a, b = d.get_state(), one.get_state()
+    for v in range(3):
+        assert O.rel_l2(a[v], b[v]) < 1e-14
+    d.set_cfl(0.5, 0.1)
+    one.set_cfl(0.5, 0.1)
+    d.step(2)
+    one.step(2)
+    assert d.t == one.t
+    s, r = d.get_state(), one.get_state()
+    for v in range(3):
+        assert O.rel_l2(s[v], r[v]) < 1e-14
