@@ -52,6 +52,13 @@ __device__ __forceinline__ size_t cpidx(int x, int ky, int nx) {
 // pass stores RG consecutive x of one column as one 16*RG-byte chunk.
 constexpr int RG = 4;
 
+// x-inverse output (x, local column kyl) in the send block of the row's owner
+// q: rows(q) x own columns, row-quad interleaved ((xl/4) ncols + kyl) 4 + xl%4.
+__device__ __forceinline__ size_t sidx_send(const Ns2dArgs& a, int x, int kyl) {
+    const int q = x >> a.lg_nrl, xl = x & (a.nrl - 1);
+    return (size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG);
+}
+
 __device__ __forceinline__ cd* pick(const Ns2dArgs& a, int m) {
     return m == 0 ? a.I[0] : m == 1 ? a.I[1] : m == 2 ? a.I[2] : a.I[3];
 }
@@ -217,8 +224,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const int x = t + T * e;
-                    const int q = x >> a.lg_nrl, xl = x & (a.nrl - 1);
-                    out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG)] = v[e];
+                    out[sidx_send(a, x, kyl)] = v[e];
                 }
             } else {
                 cd* out = pick(a, m);
@@ -707,8 +713,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const int x = t + T * e;
-                    const int q = x >> a.lg_nrl, xl = x & (a.nrl - 1);
-                    out[(size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG)] = v[e];
+                    out[sidx_send(a, x, kyl)] = v[e];
                 }
             }
         }
@@ -730,7 +735,7 @@ cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
         cudaFuncSetAttribute(k1_xinv<NX, PZ, NM, EM, CTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    if (cudaError_t e_ = launch_pdl(k1_xinv<NX, PZ, NM, EM, CTW>, dim3(grid), dim3(T * LPC), smem, s, a, stage); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(k1_xinv<NX, PZ, NM, EM, CTW>, grid, T * LPC, smem, s, a, stage));
     return cudaGetLastError();
 }
 
@@ -753,7 +758,7 @@ cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s)
         cudaFuncSetAttribute(k4_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = true;
     }
-    if (cudaError_t e_ = launch_pdl(k4_xfwd<NX>, dim3(grid), dim3(T * LPC), smem, s, a, stage); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(k4_xfwd<NX>, grid, T * LPC, smem, s, a, stage));
     return cudaGetLastError();
 }
 
@@ -771,7 +776,7 @@ cudaError_t launch_y_v(const Ns2dArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(k3_phys<NY, EM, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = smem;
     }
-    if (cudaError_t e_ = launch_pdl(k3_phys<NY, EM, CFL>, dim3(grid), dim3(T * G), smem, s, a); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(k3_phys<NY, EM, CFL>, grid, T * G, smem, s, a));
     return cudaGetLastError();
 }
 
@@ -792,7 +797,7 @@ cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
     }
     const int groups = (a.nrl + G - 1) / G;
     const int grid = groups < a.wave ? groups : a.wave;
-    if (cudaError_t e_ = launch_pdl(k3b_phys<NY, CFL>, dim3(grid), dim3(F::T * G), smem, s, a); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(k3b_phys<NY, CFL>, grid, F::T * G, smem, s, a));
     return cudaGetLastError();
 }
 
@@ -823,7 +828,8 @@ cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     }
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    if (cudaError_t e_ = launch_pdl(k4b_xfwd<NX, EM, CTW, FUSE>, dim3(grid), dim3(T * LPC), smem, s, a, stage, FUSE ? 1 : 0); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(k4b_xfwd<NX, EM, CTW, FUSE>, grid, T * LPC, smem, s,
+                          a, stage, FUSE ? 1 : 0));
     return cudaGetLastError();
 }
 
@@ -967,7 +973,7 @@ cudaError_t ns2d_launch_stage(const Ns2dArgs& a, int stage, cudaStream_t s, long
     *launches += 3;
     if (final && !a.pruned && a.nh > a.kcy + 1) {
         hook.begin(3);
-        if (cudaError_t e_ = launch_pdl(k4_decay, dim3(296), dim3(256), 0, s, a); e_ != cudaSuccess) return e_;
+        SKG_TRY(launch_pdl(k4_decay, 296, 256, 0, s, a));
         hook.end(3, B * 2.0 * a.nx * (a.nh - a.kcy - 1));
         *launches += 1;
         if ((err = cudaGetLastError()) != cudaSuccess) return err;

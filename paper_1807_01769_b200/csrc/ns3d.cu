@@ -741,14 +741,14 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
                 const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - 4) * F::T * C);
                 static size_t done = 0;
                 set_smem(k1_3d<NX, true, CT>, smem, done);
-                if (cudaError_t e_ = launch_pdl(k1_3d<NX, true, CT>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
+                SKG_TRY(launch_pdl(k1_3d<NX, true, CT>, grid, F::T * C, smem, s, a, stage));
             }
         } else {
             if constexpr (CT == 256) {
                 const size_t smem = sizeof(cd) * (F::SMEM * C + F::E * F::T * C);
                 static size_t done = 0;
                 set_smem(k1_3d<NX, false>, smem, done);
-                if (cudaError_t e_ = launch_pdl(k1_3d<NX, false>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
+                SKG_TRY(launch_pdl(k1_3d<NX, false>, grid, F::T * C, smem, s, a, stage));
             } else {
                 return launch_x3_v<NX, 256>(a, stage, inverse, s);
             }
@@ -760,10 +760,10 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
         if (a.rk2 ? stage == 2 : stage == 4) {
             static size_t done_f = 0;
             set_smem(k4_3d<NX, CT, true>, smem, done_f);
-            if (cudaError_t e_ = launch_pdl(k4_3d<NX, CT, true>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
+            SKG_TRY(launch_pdl(k4_3d<NX, CT, true>, grid, F::T * C, smem, s, a, stage));
         } else {
             set_smem(k4_3d<NX, CT, false>, smem, done);
-            if (cudaError_t e_ = launch_pdl(k4_3d<NX, CT, false>, dim3(grid), dim3(F::T * C), smem, s, a, stage); e_ != cudaSuccess) return e_;
+            SKG_TRY(launch_pdl(k4_3d<NX, CT, false>, grid, F::T * C, smem, s, a, stage));
         }
     }
     return cudaGetLastError();
@@ -792,17 +792,17 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
         static size_t done = 0;
         set_smem(k2s_3d<NY, CT>, smem_s, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        if (cudaError_t e_ = launch_pdl(k2s_3d<NY, CT>, dim3(grid), dim3(F::T * C), smem_s, s, a); e_ != cudaSuccess) return e_;
+        SKG_TRY(launch_pdl(k2s_3d<NY, CT>, grid, F::T * C, smem_s, s, a));
     } else if (inverse) {
         static size_t done = 0;
         set_smem(k2_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        if (cudaError_t e_ = launch_pdl(k2_3d<NY, CT>, dim3(grid), dim3(F::T * C), smem, s, a); e_ != cudaSuccess) return e_;
+        SKG_TRY(launch_pdl(k2_3d<NY, CT>, grid, F::T * C, smem, s, a));
     } else {
         static size_t done = 0;
         set_smem(k2f_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_o + C - 1) / C);
-        if (cudaError_t e_ = launch_pdl(k2f_3d<NY, CT>, dim3(grid), dim3(F::T * C), smem, s, a); e_ != cudaSuccess) return e_;
+        SKG_TRY(launch_pdl(k2f_3d<NY, CT>, grid, F::T * C, smem, s, a));
     }
     return cudaGetLastError();
 }
@@ -827,10 +827,10 @@ cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
     if (a.dyn && a.ystage == 1) {
         set_smem(k3_3d<NZ, true>, smem, done_c);
-        if (cudaError_t e_ = launch_pdl(k3_3d<NZ, true>, dim3(grid), dim3(Z::T * Z::G), smem, s, a); e_ != cudaSuccess) return e_;
+        SKG_TRY(launch_pdl(k3_3d<NZ, true>, grid, Z::T * Z::G, smem, s, a));
     } else {
         set_smem(k3_3d<NZ, false>, smem, done);
-        if (cudaError_t e_ = launch_pdl(k3_3d<NZ, false>, dim3(grid), dim3(Z::T * Z::G), smem, s, a); e_ != cudaSuccess) return e_;
+        SKG_TRY(launch_pdl(k3_3d<NZ, false>, grid, Z::T * Z::G, smem, s, a));
     }
     return cudaGetLastError();
 }
@@ -913,7 +913,7 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
         *launches += 1;
         if (final && !a.pruned && a.nh > a.kz_o) {
             hook.begin(3);
-            if (cudaError_t e_ = launch_pdl(k4_3d_decay, dim3(592), dim3(256), 0, s, a); e_ != cudaSuccess) return e_;
+            SKG_TRY(launch_pdl(k4_3d_decay, 592, 256, 0, s, a));
             hook.end(3, B * 6.0 * a.nx * a.ny * (a.nh - a.kz_o));
             *launches += 1;
             if ((err = cudaGetLastError()) != cudaSuccess) return err;

@@ -257,6 +257,13 @@ cudaError_t launch_count_masked(const cd* f, int dims, const int* n, const int* 
 cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double* kscale,
                              int axis, double* d_k, unsigned char* d_mask, cudaStream_t s,
                              long* launches);
+// Return the error of a CUDA call from a cudaError_t function.
+#define SKG_TRY(...)                                \
+    do {                                            \
+        const cudaError_t skg_e_ = (__VA_ARGS__);   \
+        if (skg_e_ != cudaSuccess) return skg_e_;   \
+    } while (0)
+
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KP, typename... A>
 inline cudaError_t launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -239,7 +239,7 @@ cudaError_t launch_dt_update(DynStep* dyn, DevFlags* flags, double* etab, int di
         g.ks[d] = kscale[d];
     }
     g.nu = nu;
-    if (cudaError_t e_ = launch_pdl(dt_update, dim3(1), dim3(256), 0, s, dyn, flags, etab, g); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(dt_update, 1, 256, 0, s, dyn, flags, etab, g));
     ++*launches;
     return cudaGetLastError();
 }
@@ -256,7 +256,7 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
     long long S = 1;
     for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.m.nh : n[d]);
     if (zero_first) cudaMemsetAsync(d_out, 0, 3 * sizeof(double), s);
-    if (cudaError_t e_ = launch_pdl(energy_kernel, dim3(592), dim3(256), 0, s, f, g, nvars, S, d_out, steps); e_ != cudaSuccess) return e_;
+    SKG_TRY(launch_pdl(energy_kernel, 592, 256, 0, s, f, g, nvars, S, d_out, steps));
     ++*launches;
     return cudaGetLastError();
 }
