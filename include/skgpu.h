@@ -59,6 +59,9 @@ const char* skg_last_error(void);
  *   scheme: SKG_RK4 or SKG_RK2 (ExactLinStepper, time_stepping.cpp:72-194).
  *   device: CUDA ordinal.
  * The state starts at zero, like init_fields.type = "constant" with value 0.
+ * Extents: any even n >= 4, as the reference (grid.cpp:34-44).  Powers of
+ * two (ns2d 4..8192, ns3d 8..1024) run the fused kernels; other extents run
+ * the generic step (one pass per reference operator, csrc/generic.cu).
  */
 int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                double dealias_coef, double nu, int scheme, int device);

@@ -264,6 +264,34 @@ cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double
         if (skg_e_ != cudaSuccess) return skg_e_;   \
     } while (0)
 
+// Generic (unfused) step for extents outside the fused kernels' range
+// (generic.cu): reference layout, one pass per reference operator.
+struct GenArgs {
+    int dims, n[3], nh, kc[3];
+    double ks[3];
+    long long S, P;
+    int nvars, has_sigma, rk2;
+    double dt, hdt, sdt;
+    DynStep* dyn;
+    const double* e1[3];
+    const double* e2[3];
+    cd *u, *k1, *k2, *k3;
+    DevFlags* flags;
+};
+struct GenScratch {
+    cd* w;        // stage state (nvars S)
+    cd* spec;     // spectral inputs of the inverse transforms (4 S in 2D, 3 S in 3D)
+    cd* nl;       // forward-transformed products (nvars S)
+    double* phys; // physical fields (4 P in 2D, 6 P in 3D)
+    cd* work;     // transform scratch (S)
+    const cd* tw[3];
+};
+cudaError_t generic_stage(const GenArgs& a, int stage, GenScratch& g, cudaStream_t s, long* launches);
+// Tendency of w into g.nl (kout == nullptr) with the stage-1 CFL reduction
+// when a.dyn is set.
+cudaError_t generic_tendency(const GenArgs& a, const cd* w, int stage, cd* kout, GenScratch& g,
+                             cudaStream_t s, long* launches);
+
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KP, typename... A>
 inline cudaError_t launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -164,6 +164,10 @@ struct skg_ctx {
     cudaGraphExec_t gexec = nullptr;
     double* g_diag = nullptr;
 
+    // generic path (extents outside the fused kernels' range, generic.cu)
+    bool generic = false;
+    skg::GenScratch gs{};
+
     // adaptive (CFL) dt: skg_set_cfl
     bool adaptive = false;
     double cfl = 0.5, dt_max = 0.1, t_end = -1.0, last_dt = 0.0;
@@ -436,6 +440,39 @@ skg::Ns3dArgs args3d_part(skg_ctx* c, double dt, const Part& p) {
     return a;
 }
 
+// launch_energy's metric/layout code: ns2d CM layout 1, ns2d reference layout 2, ns3d 0
+int energy_mode(const skg_ctx* c) { return c->solver == 2 ? (c->generic ? 2 : 1) : 0; }
+
+skg::GenArgs args_gen(skg_ctx* c, double dt) {
+    skg::GenArgs a{};
+    a.dims = c->dims;
+    for (int d = 0; d < 3; ++d) {
+        a.n[d] = c->n[d];
+        a.kc[d] = c->kc[d];
+        a.ks[d] = c->kscale[d];
+    }
+    a.nh = c->nh;
+    a.S = c->S;
+    a.P = c->P;
+    a.nvars = c->nvars;
+    a.has_sigma = c->nu != 0.0;
+    a.rk2 = c->scheme == SKG_RK2;
+    a.dt = dt;
+    a.hdt = 0.5 * dt;
+    a.sdt = dt / 6.0;
+    a.dyn = c->adaptive ? c->d_dyn : nullptr;
+    for (int d = 0; d < c->dims; ++d) {
+        a.e1[d] = etab_ptr(c, 0, d);
+        a.e2[d] = etab_ptr(c, 1, d);
+    }
+    a.u = c->u;
+    a.k1 = c->k[0];
+    a.k2 = c->k[1];
+    a.k3 = c->k[2];
+    a.flags = c->flags;
+    return a;
+}
+
 int sync_and_check(skg_ctx* c, long nsteps, double dt) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     harvest(c);
@@ -704,7 +741,13 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             return skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale, c->nu,
                                          c->stream, counter);
         };
-        if (c->solver == 2) {
+        if (c->generic) {
+            skg::GenArgs a = args_gen(c, dt);
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                e = skg::generic_stage(a, st, c->gs, c->stream, counter);
+                if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+            }
+        } else if (c->solver == 2) {
             skg::Ns2dArgs a = args2d(c, dt);
             fused = skg::ns2d_fast_ok(a);
             if (!fused) a.diag = nullptr;
@@ -732,7 +775,7 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             }
         }
         if (e == cudaSuccess && c->diag && !fused)  // unfused paths: one reduction per step
-            e = skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
+            e = skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, energy_mode(c),
                                    c->diag, c->stream, counter, c->nu, &c->flags->steps, false);
         return e;
     };
@@ -833,7 +876,7 @@ int load_state_from_io(skg_ctx* c) {
                                          sizeof(cd) * p.ncols * c->n[0], cudaMemcpyDeviceToDevice, c->stream));
         return SKG_OK;
     }
-    if (c->solver == 2) {
+    if (c->solver == 2 && !c->generic) {
         CUDA_TRY(skg::launch_transpose_c(c->io, c->u, c->n[0], c->nh, 0, c->stream, &c->launches));
     } else {
         CUDA_TRY(cudaMemcpyAsync(c->u, c->io, sizeof(cd) * c->S * c->nvars,
@@ -870,7 +913,7 @@ int store_state_to_io(skg_ctx* c, const cd* src) {
         CUDA_TRY(skg::launch_transpose_c(c->cmfull, c->io, c->nh, c->n[0], 0, c->stream, &c->launches));
         return SKG_OK;
     }
-    if (c->solver == 2) {
+    if (c->solver == 2 && !c->generic) {
         CUDA_TRY(skg::launch_transpose_c(src, c->io, c->nh, c->n[0], 0, c->stream, &c->launches));
     } else {
         CUDA_TRY(cudaMemcpyAsync(c->io, src, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToDevice,
@@ -957,10 +1000,11 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         return fail(SKG_ECONFIG, "dealias_coef must be in (0, 1]");
     if (!(nu >= 0.0)) return fail(SKG_ECONFIG, "viscosity must be >= 0");
     if (scheme != SKG_RK4 && scheme != SKG_RK2) return fail(SKG_ECONFIG, "unknown time scheme");
-    if (sid == 2 && !skg::ns2d_supported(n[0], n[1]))
-        return fail(SKG_EUNSUPPORTED, "ns2d kernels need power-of-two extents in [4, 8192]");
-    if (sid == 3 && !skg::ns3d_supported(n[0], n[1], n[2]))
-        return fail(SKG_EUNSUPPORTED, "ns3d kernels need power-of-two extents in [8, 1024]");
+    // extents outside the fused kernels' range run the generic step
+    const bool generic = sid == 2 ? !skg::ns2d_supported(n[0], n[1]) : !skg::ns3d_supported(n[0], n[1], n[2]);
+    if (generic && (world > 1 || (sid == 3 && slab_one)))
+        return fail(SKG_EUNSUPPORTED,
+                    "slab and compact layouts need the fused kernels' extents (powers of two)");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -986,6 +1030,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         c->kscale[d] = kTwoPi / c->L[d];
         c->kc[d] = cut_index(n[d], c->L[d], dealias_coef, d == dims - 1);
     }
+    c->generic = generic;
     c->nh = n[dims - 1] / 2 + 1;
     c->S = c->nh;
     c->P = 1;
@@ -1108,7 +1153,16 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         for (int i = 0; i < 3 && ok; ++i) ok = alloc((void**)&c->k[i], sizeof(cd) * S * c->nvars);
         if (sid == 2) c->inter_elems = 5 * S;  // 4 intermediates + tendency rows
         else c->inter_elems = 11 * (size_t)n[0] * n[1] * c->nh;  // A[5] (C aliases) + B[6] (D aliases)
+        if (c->generic) c->inter_elems = 1;
         ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
+        if (c->generic) {
+            const size_t P = (size_t)c->P;
+            ok = ok && alloc((void**)&c->gs.w, sizeof(cd) * S * c->nvars);
+            ok = ok && alloc((void**)&c->gs.spec, sizeof(cd) * S * (sid == 2 ? 4 : 3));
+            ok = ok && alloc((void**)&c->gs.nl, sizeof(cd) * S * c->nvars);
+            ok = ok && alloc((void**)&c->gs.phys, sizeof(double) * P * (sid == 2 ? 4 : 6));
+            ok = ok && alloc((void**)&c->gs.work, sizeof(cd) * S);
+        }
     }
     ok = ok && alloc((void**)&c->io, sizeof(cd) * S * c->nvars);
     int ext_total = 0;
@@ -1122,6 +1176,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     for (int d = 0; d < dims; ++d) {
         c->tw[d] = twiddle_table(device, n[d]);
         if (!c->tw[d]) return cleanup(SKG_ECUDA, "twiddle table allocation failed");
+        c->gs.tw[d] = c->tw[d];
     }
     // cudaMemset above runs on the legacy default stream, which does not order
     // against the context's non-blocking stream: finish it before any kernel.
@@ -1146,6 +1201,11 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->d_count);
     cudaFree(c->d_red);
     cudaFree(c->d_dyn);
+    cudaFree(c->gs.w);
+    cudaFree(c->gs.spec);
+    cudaFree(c->gs.nl);
+    cudaFree(c->gs.phys);
+    cudaFree(c->gs.work);
     harvest(c);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (Part& p : c->parts) {
@@ -1298,7 +1358,16 @@ static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax
     const bool keep_pruned = c->pruned;
     int rc = decide_pruned(c, c->io);
     if (rc) return rc;
-    if (c->solver == 2) {
+    if (c->generic) {  // reference layout throughout; tendency into gs.nl
+        skg::GenArgs a = args_gen(c, 1.0);
+        a.dyn = umax ? c->d_dyn : nullptr;
+        skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+        if (umax) CUDA_TRY(cudaMemsetAsync(c->d_dyn, 0, sizeof(skg::DynStep), c->stream));
+        CUDA_TRY(skg::generic_tendency(a, c->io, 1, nullptr, c->gs, c->stream, &c->launches));
+        CUDA_TRY(cudaMemcpyAsync(c->io, c->gs.nl, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    } else if (c->solver == 2) {
         // input (CM) in k[2], tendency into k[0]
         CUDA_TRY(skg::launch_transpose_c(c->io, c->k[2], c->n[0], c->nh, 0, c->stream, &c->launches));
         rc = refresh_exp(c, c->cached_dt > 0 ? c->cached_dt : 1.0);
@@ -1496,7 +1565,7 @@ int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, doub
 int skg_energy(skg_ctx* c, double* energy, double* enstrophy) {
     if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_energy on a slab-decomposed context");
     CUDA_TRY(cudaSetDevice(c->device));
-    CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 1 : 0,
+    CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, energy_mode(c),
                                 c->d_red, c->stream, &c->launches));
     double h[3];
     CUDA_TRY(cudaMemcpyAsync(h, c->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));

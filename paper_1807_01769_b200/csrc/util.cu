@@ -90,7 +90,8 @@ __global__ void grid_dump(MaskGeo g, int axis, double kscale, double* k, unsigne
 struct EnGeo {
     MaskGeo m;
     double ks[3];
-    int solver2d;  // 1: ns2d on the CM layout ([ky][kx]); 0: reference layout
+    int solver2d;  // 1: ns2d metric (solvers.cpp:211-218); 0: default (simulation.cpp:163-170)
+    int cm;        // 1: ns2d CM layout [ky][kx]; 0: reference layout
     double nu;
 };
 
@@ -105,7 +106,7 @@ __global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < S;
          q += (long long)gridDim.x * blockDim.x) {
         int ix[3];
-        if (g.solver2d) {  // CM: q = ky * nx + kx
+        if (g.cm) {  // CM: q = ky * nx + kx
             ix[0] = (int)(q % g.m.n[0]);
             ix[1] = (int)(q / g.m.n[0]);
         } else {
@@ -251,7 +252,8 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
     EnGeo g{};
     g.m = make_geo(dims, n, kc);
     for (int d = 0; d < dims; ++d) g.ks[d] = kscale[d];
-    g.solver2d = solver2d;
+    g.solver2d = solver2d != 0;  // 1: ns2d on the CM layout, 2: ns2d on the reference layout
+    g.cm = solver2d == 1;
     g.nu = nu;
     long long S = 1;
     for (int d = 0; d < dims; ++d) S *= (d == dims - 1 ? g.m.nh : n[d]);
