@@ -8,8 +8,14 @@
 //          fft.cpp:100-106), then c2r rows (two rows packed), dropping the
 //          imaginary parts of the last-axis index-0 and Nyquist entries.
 // Power-of-two extents use the register Stockham FFT of fft_block.cuh; other
-// extents fall back to a direct O(n^2) line DFT in shared memory (still on
-// the GPU; these shapes only occur in the reference's small operator tests).
+// extents up to 4096 use Bluestein's chirp convolution on that FFT, larger
+// ones a direct O(n^2) line DFT in shared memory (still on the GPU).
+#include <cmath>
+#include <complex>
+#include <map>
+#include <mutex>
+#include <vector>
+
 #include "skg_internal.h"
 
 namespace skg {
@@ -163,6 +169,165 @@ __global__ void dft_c2r_generic(const cd* in, double* u, int n, const cd* __rest
     }
 }
 
+// -------------------------------------------------- Bluestein (any n <= 4096)
+// X_k = c_k sum_j (x_j c_j) conj(c_{k-j}),  c_j = exp(s i pi j^2 / n): the
+// convolution runs as two power-of-two register FFTs of length M >= 2n - 1
+// (one CTA per line), against the precomputed spectrum of the conj(c) chirp.
+struct BlueTab {
+    int M = 0;
+    cd* chirp[2] = {nullptr, nullptr};  // [sign < 0, sign > 0], n entries
+    cd* bhat[2] = {nullptr, nullptr};   // M entries
+    cd* twm = nullptr;                  // W_M table for the register FFT
+};
+
+// mode 0: c2c along an axis of [outer][n][inner] (in place);
+// 1: r2c of real rows (n) into half rows (n/2+1); 2: c2r of half rows.
+template <int M, int S>
+__global__ void __launch_bounds__(BFFT<M>::T) bluestein_line(cd* data, long long inner, int n, int mode,
+                                                             const double* ureal, double* ureal_out,
+                                                             const cd* __restrict__ chirp,
+                                                             const cd* __restrict__ bhat,
+                                                             const cd* __restrict__ twm) {
+    using F = BFFT<M>;
+    constexpr int T = F::T, E = F::E;
+    extern __shared__ cd smem[];
+    const int t = threadIdx.x;
+    const long long line = blockIdx.x;
+    const int h = n / 2 + 1;
+    cd* base = nullptr;
+    if (mode == 0) base = data + (line / inner) * n * inner + (line % inner);
+    const typename F::Bases wb = F::bases(t, twm);
+    cd v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int j = t + T * e;
+        cd x = zero();
+        if (j < n) {
+            if (mode == 0) {
+                x = base[(long long)j * inner];
+            } else if (mode == 1) {
+                x = mk(ureal[line * n + j], 0.0);
+            } else {  // Hermitian extension; c2r ignores Im of the DC/Nyquist entries
+                const int k = j <= n / 2 ? j : n - j;
+                x = data[line * h + k];
+                if (k == 0 || 2 * k == n) x.y = 0.0;
+                if (j > n / 2) x = conj(x);
+            }
+            x = mul(x, chirp[j]);
+        }
+        v[e] = x;
+    }
+    F::template run<-1>(v, smem, t, wb);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = mul(v[e], bhat[t + T * e]);
+    F::template run<+1>(v, smem, t, wb);
+    const double im = 1.0 / (double)M;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int k = t + T * e;
+        if (k >= n) continue;
+        const cd X = scale(mul(v[e], chirp[k]), im);
+        if (mode == 0) base[(long long)k * inner] = X;
+        else if (mode == 1) { if (k < h) data[line * h + k] = X; }
+        else ureal_out[line * n + k] = X.x;
+    }
+}
+
+std::mutex g_blue_mu;
+std::map<std::pair<int, int>, BlueTab> g_blue;
+
+// Tables for length n on the current device (built once, before any graph
+// capture: the first step of a batch runs eagerly).
+const BlueTab* blue_tab(int n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_blue_mu);
+    auto key = std::make_pair(dev, n);
+    auto it = g_blue.find(key);
+    if (it != g_blue.end()) return &it->second;
+    int M = 16;
+    while (M < 2 * n - 1) M *= 2;
+    if (M > 8192) return nullptr;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    BlueTab tb;
+    tb.M = M;
+    std::vector<cd> wm(M);
+    for (int m = 0; m < M; ++m) {
+        const long double a = -2.0L * pi * (long double)m / (long double)M;
+        wm[m] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    for (int si = 0; si < 2; ++si) {
+        const long double sg = si == 0 ? -1.0L : 1.0L;
+        std::vector<std::complex<long double>> c(n);
+        for (int j = 0; j < n; ++j) {
+            const long long j2 = ((long long)j * j) % (2LL * n);  // exact angle reduction
+            const long double a = sg * pi * (long double)j2 / (long double)n;
+            c[j] = std::complex<long double>(cosl(a), sinl(a));
+        }
+        // b_m = conj(c_|m|) wrapped onto [0, M); bhat = FFT_M(b), exact sums
+        std::vector<cd> ch(n), bh(M);
+        for (int j = 0; j < n; ++j) ch[j] = make_double2((double)c[j].real(), (double)c[j].imag());
+        std::vector<std::complex<long double>> wml(M);
+        for (int m = 0; m < M; ++m) {
+            const long double a = -2.0L * pi * (long double)m / (long double)M;
+            wml[m] = std::complex<long double>(cosl(a), sinl(a));
+        }
+        for (int q = 0; q < M; ++q) {
+            std::complex<long double> acc = std::conj(c[0]);
+            for (int m = 1; m < n; ++m) {
+                const std::complex<long double> b = std::conj(c[m]);
+                acc += b * (wml[(int)(((long long)q * m) % M)] + wml[(int)(((long long)q * (M - m)) % M)]);
+            }
+            bh[q] = make_double2((double)acc.real(), (double)acc.imag());
+        }
+        cudaMalloc(&tb.chirp[si], sizeof(cd) * n);
+        cudaMalloc(&tb.bhat[si], sizeof(cd) * M);
+        cudaMemcpy(tb.chirp[si], ch.data(), sizeof(cd) * n, cudaMemcpyHostToDevice);
+        cudaMemcpy(tb.bhat[si], bh.data(), sizeof(cd) * M, cudaMemcpyHostToDevice);
+    }
+    cudaMalloc(&tb.twm, sizeof(cd) * M);
+    cudaMemcpy(tb.twm, wm.data(), sizeof(cd) * M, cudaMemcpyHostToDevice);
+    return &(g_blue[key] = tb);
+}
+
+template <int M>
+cudaError_t launch_blue_m(const BlueTab& tb, int si, cd* data, long long lines, long long inner, int n,
+                          int mode, const double* ur, double* uo, cudaStream_t s) {
+    using F = BFFT<M>;
+    const size_t smem = sizeof(cd) * F::SMEM;
+    static bool init[2] = {false, false};
+    if (!init[si]) {
+        if (si == 0)
+            cudaFuncSetAttribute(bluestein_line<M, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        else
+            cudaFuncSetAttribute(bluestein_line<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        init[si] = true;
+    }
+    if (si == 0)
+        bluestein_line<M, -1><<<(unsigned)lines, F::T, smem, s>>>(data, inner, n, mode, ur, uo,
+                                                                  tb.chirp[0], tb.bhat[0], tb.twm);
+    else
+        bluestein_line<M, 1><<<(unsigned)lines, F::T, smem, s>>>(data, inner, n, mode, ur, uo,
+                                                                 tb.chirp[1], tb.bhat[1], tb.twm);
+    return cudaGetLastError();
+}
+
+// false when n needs M > 8192 (caller falls back to the direct DFT)
+bool bluestein(int n, int sign, cd* data, long long lines, long long inner, int mode, const double* ur,
+               double* uo, cudaStream_t s, cudaError_t* err) {
+    const BlueTab* tb = blue_tab(n);
+    if (!tb) return false;
+    const int si = sign < 0 ? 0 : 1;
+    switch (tb->M) {
+#define BCASE(M) \
+    case M: *err = launch_blue_m<M>(*tb, si, data, lines, inner, n, mode, ur, uo, s); return true;
+        BCASE(16) BCASE(32) BCASE(64) BCASE(128) BCASE(256) BCASE(512) BCASE(1024) BCASE(2048)
+        BCASE(4096) BCASE(8192)
+#undef BCASE
+        default: return false;
+    }
+}
+
 __global__ void scale_kernel(cd* d, long long n, double s) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
          q += (long long)gridDim.x * blockDim.x)
@@ -225,6 +390,8 @@ cudaError_t c2c(cd* data, long long outer, int n, long long inner, int sign, con
 #undef CASE
         default: {
             const long long lines = outer * inner;
+            cudaError_t e = cudaSuccess;
+            if (bluestein(n, sign, data, lines, inner, 0, nullptr, nullptr, s, &e)) return e;
             dft_axis_generic<<<(unsigned)lines, 128, sizeof(cd) * n, s>>>(data, outer, n, inner, sign, tw);
             return cudaGetLastError();
         }
@@ -237,9 +404,12 @@ cudaError_t r2c(const double* u, cd* out, long long rows, int n, const cd* tw, c
     case N: return launch_r2c<N>(u, out, rows, tw, s);
         SKG_POW2_CASES(CASE)
 #undef CASE
-        default:
+        default: {
+            cudaError_t e = cudaSuccess;
+            if (bluestein(n, -1, out, rows, 1, 1, u, nullptr, s, &e)) return e;
             dft_r2c_generic<<<(unsigned)rows, 128, sizeof(double) * n, s>>>(u, out, n, tw);
             return cudaGetLastError();
+        }
     }
 }
 
@@ -249,9 +419,12 @@ cudaError_t c2r(const cd* in, double* u, long long rows, int n, const cd* tw, cu
     case N: return launch_c2r<N>(in, u, rows, tw, s);
         SKG_POW2_CASES(CASE)
 #undef CASE
-        default:
+        default: {
+            cudaError_t e = cudaSuccess;
+            if (bluestein(n, 1, const_cast<cd*>(in), rows, 1, 2, nullptr, u, s, &e)) return e;
             dft_c2r_generic<<<(unsigned)rows, 128, sizeof(cd) * (n / 2 + 1), s>>>(in, u, n, tw);
             return cudaGetLastError();
+        }
     }
 }
 

@@ -84,3 +84,35 @@ def test_generic_rejects_slab():
         api.Simulation("ns2d", (96, 96), 1e-3, 1e-3, world=2)
     with pytest.raises(api.UnsupportedError):
         api.Simulation("ns3d", (12, 12, 12), 1e-3, 1e-3, compact=True)
+
+
+@pytest.mark.parametrize("shape", [(6,), (96,), (1000,), (3000,), (5000,), (96, 160), (12, 20, 36)])
+def test_non_pow2_transforms(shape):
+    """Bluestein (n <= 4096) and direct-DFT (larger) line transforms against
+    numpy: FftPlan::forward = rfftn / N, inverse = irfftn * N."""
+    rng = np.random.default_rng(11)
+    u = rng.standard_normal(shape)
+    uh = api.fft_forward(u)
+    ref = np.fft.rfftn(u) / u.size
+    assert np.abs(uh - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
+    back = api.fft_inverse(uh, shape)
+    assert np.abs(back - u).max() < 1e-12
+
+
+def test_generic_384_is_fast(ref_lib):
+    """A 3 x 2^7 grid through the generic path: parity and a sane step time."""
+    import time
+    n = (384, 384)
+    u0 = ic.ns2d_ic(n, seed=3)
+    dt = ic.cfl_dt("ns2d", n, u0)
+    g = api.Simulation("ns2d", n, 1e-4, dt)
+    g.set_state(u0)
+    g.step(2)
+    t0 = time.perf_counter()
+    g.step(10)
+    ms = (time.perf_counter() - t0) / 10 * 1e3
+    r = ref_lib.RefSimulation("ns2d", n, 1e-4, dt)
+    r.set_state(u0)
+    r.step(12)
+    assert per_field(g.get_state(), r.get_state()) < PARITY
+    assert ms < 50.0, ms
