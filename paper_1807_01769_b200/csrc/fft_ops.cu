@@ -25,7 +25,7 @@ namespace {
 // -------------------------------------------------- power-of-two lines
 // c2c along one axis of a [outer][N][inner] complex array, in place.
 template <int N, int S>
-__global__ void __launch_bounds__(256) c2c_axis_tw(cd* data, long long outer, long long inner,
+__global__ void __launch_bounds__(BFFT<N>::T > 256 ? BFFT<N>::T : 256) c2c_axis_tw(cd* data, long long outer, long long inner,
                                                    const cd* __restrict__ tw) {
     using F = BFFT<N>;
     constexpr int T = F::T, E = F::E;
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) c2c_axis_tw(cd* data, long long outer, lo
 
 // r2c of real rows of length N, two rows per thread group; out rows N/2+1.
 template <int N>
-__global__ void __launch_bounds__(256) r2c_rows(const double* __restrict__ u, cd* __restrict__ out,
+__global__ void __launch_bounds__(BFFT<N>::T > 256 ? BFFT<N>::T : 256) r2c_rows(const double* __restrict__ u, cd* __restrict__ out,
                                                 long long rows, const cd* __restrict__ tw) {
     using F = BFFT<N>;
     constexpr int T = F::T, E = F::E;
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) r2c_rows(const double* __restrict__ u, cd
 
 // c2r of half rows (N/2+1) into real rows of length N, two rows per group.
 template <int N>
-__global__ void __launch_bounds__(256) c2r_rows(const cd* __restrict__ in, double* __restrict__ u,
+__global__ void __launch_bounds__(BFFT<N>::T > 256 ? BFFT<N>::T : 256) c2r_rows(const cd* __restrict__ in, double* __restrict__ u,
                                                 long long rows, const cd* __restrict__ tw) {
     using F = BFFT<N>;
     constexpr int T = F::T, E = F::E;

@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
 }
 
 template <int NX>
-__global__ void __launch_bounds__(256, 2) k4_xfwd(Ns2dArgs a, int stage) {
+__global__ void __launch_bounds__(BFFT<NX>::T > 256 ? BFFT<NX>::T : 256, BFFT<NX>::T > 256 ? 1 : 2)
+    k4_xfwd(Ns2dArgs a, int stage) {
     using F = BFFT<NX>;
     constexpr int T = F::T, E = F::E;
     constexpr int LPC = T >= 256 ? 1 : 256 / T;
@@ -462,7 +463,8 @@ __global__ void k4_decay(Ns2dArgs a) {
 // y pass, one row per group iteration, persistent over rows; the next row's
 // two input lines stream into shared memory (cp.async) during the FFTs.
 template <int NY, bool CFL>
-__global__ void __launch_bounds__(256, 2) k3b_phys(Ns2dArgs a) {
+__global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY>::T > 256 ? 1 : 2)
+    k3b_phys(Ns2dArgs a) {
     using F = BFFT<NY>;
     constexpr int T = F::T, E = F::E;
     constexpr int G = T >= 256 ? 1 : 256 / T;

@@ -17,12 +17,73 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
 #include <nccl.h>
+#include <type_traits>
 
 #include "../../include/skgpu.h"
 #include "skg_internal.h"
 
 using skg::cd;
+
+namespace {
+
+// NCCL is loaded on first use (multi-GPU contexts only) instead of at link
+// time: a process that imports PyTorch after this library would otherwise
+// bind torch's NCCL symbols to whichever libnccl.so.2 came first.  When torch
+// is already loaded, dlopen returns its (newer) NCCL.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&::ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&::ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&::ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&::ncclGroupStart) GroupStart = nullptr;
+    decltype(&::ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&::ncclSend) Send = nullptr;
+    decltype(&::ncclRecv) Recv = nullptr;
+    decltype(&::ncclAllReduce) AllReduce = nullptr;
+    decltype(&::ncclGetErrorString) GetErrorString = nullptr;
+};
+
+const char* nccl_unloaded_error(ncclResult_t) { return "NCCL not loaded"; }
+
+NcclApi load_nccl() {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    a.GetErrorString = nccl_unloaded_error;
+    if (!h) {
+        const char* e = dlerror();
+        a.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+        return a;
+    }
+    bool ok = true;
+    auto sym = [&](auto& f, const char* name) {
+        f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+        if (!f) ok = false;
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.AllReduce, "ncclAllReduce");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    if (!a.GetErrorString) a.GetErrorString = nccl_unloaded_error;
+    a.ok = ok;
+    if (!ok) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+}
+
+NcclApi& nccl() {
+    static NcclApi a = load_nccl();
+    return a;
+}
+
+}  // namespace
 
 namespace {
 
@@ -554,7 +615,7 @@ int exchange(skg_ctx* c, int which) {
     } else {
         const Part& me = c->parts[0];
         const int r = me.r;
-        ncclResult_t nr = ncclGroupStart();
+        ncclResult_t nr = nccl().GroupStart();
         for (int q = 0; q < G && nr == ncclSuccess; ++q) {
             for (int f = 0; f < 2 && nr == ncclSuccess; ++f) {
                 cd *sptr, *rptr;
@@ -574,14 +635,14 @@ int exchange(skg_ctx* c, int which) {
                     if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
                     continue;
                 }
-                if (scnt) nr = ncclSend(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
-                if (nr == ncclSuccess && rcnt) nr = ncclRecv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
+                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
                 bytes += scnt * sizeof(cd);
             }
         }
-        ncclResult_t ne = ncclGroupEnd();
+        ncclResult_t ne = nccl().GroupEnd();
         if (nr != ncclSuccess || ne != ncclSuccess)
-            return fail(SKG_ENCCL, std::string("all-to-all: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+            return fail(SKG_ENCCL, std::string("all-to-all: ") + nccl().GetErrorString(nr != ncclSuccess ? nr : ne));
     }
     hook.end(4, bytes);
     ++c->launches;
@@ -624,7 +685,7 @@ int exchange3(skg_ctx* c, int which) {
     } else {
         const Part& me = c->parts[0];
         const int r = me.r;
-        ncclResult_t nr = ncclGroupStart();
+        ncclResult_t nr = nccl().GroupStart();
         for (int q = 0; q < G && nr == ncclSuccess; ++q) {
             for (int f = 0; f < nf && nr == ncclSuccess; ++f) {
                 const size_t scnt = count(r, q), rcnt = count(q, r);
@@ -634,14 +695,14 @@ int exchange3(skg_ctx* c, int which) {
                     if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
                     continue;
                 }
-                if (scnt) nr = ncclSend(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
-                if (nr == ncclSuccess && rcnt) nr = ncclRecv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
+                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
                 bytes += scnt * sizeof(cd);
             }
         }
-        ncclResult_t ne = ncclGroupEnd();
+        ncclResult_t ne = nccl().GroupEnd();
         if (nr != ncclSuccess || ne != ncclSuccess)
-            return fail(SKG_ENCCL, std::string("all-to-all: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+            return fail(SKG_ENCCL, std::string("all-to-all: ") + nccl().GetErrorString(nr != ncclSuccess ? nr : ne));
     }
     hook.end(4, bytes);
     ++c->launches;
@@ -650,9 +711,9 @@ int exchange3(skg_ctx* c, int which) {
 
 int dist_dt_update(skg_ctx* c, long* counter) {
     if (c->comm) {  // global max |u_d| over the ranks' x rows
-        const ncclResult_t nr = ncclAllReduce(c->d_dyn->umax, c->d_dyn->umax, 3, ncclDouble, ncclMax,
+        const ncclResult_t nr = nccl().AllReduce(c->d_dyn->umax, c->d_dyn->umax, 3, ncclDouble, ncclMax,
                                               c->comm, c->stream);
-        if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+        if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
     }
     CUDA_TRY(skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale, c->nu,
                                    c->stream, counter));
@@ -893,9 +954,9 @@ int store_state_to_io(skg_ctx* c, const cd* src) {
             if (rc2) return rc2;
         }
         if (c->comm) {
-            const ncclResult_t nr = ncclAllReduce(c->io, c->io, 2 * 3 * (size_t)c->S, ncclDouble,
+            const ncclResult_t nr = nccl().AllReduce(c->io, c->io, 2 * 3 * (size_t)c->S, ncclDouble,
                                                   ncclSum, c->comm, c->stream);
-            if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
         }
         return SKG_OK;
     }
@@ -906,9 +967,9 @@ int store_state_to_io(skg_ctx* c, const cd* src) {
                 CUDA_TRY(cudaMemcpyAsync(c->cmfull + (size_t)p.c0 * c->n[0], p.u,
                                          sizeof(cd) * p.ncols * c->n[0], cudaMemcpyDeviceToDevice, c->stream));
         if (c->comm) {
-            const ncclResult_t nr = ncclAllReduce(c->cmfull, c->cmfull, 2 * (size_t)c->S, ncclDouble,
+            const ncclResult_t nr = nccl().AllReduce(c->cmfull, c->cmfull, 2 * (size_t)c->S, ncclDouble,
                                                   ncclSum, c->comm, c->stream);
-            if (nr != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(nr));
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
         }
         CUDA_TRY(skg::launch_transpose_c(c->cmfull, c->io, c->nh, c->n[0], 0, c->stream, &c->launches));
         return SKG_OK;
@@ -975,8 +1036,9 @@ int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, c
 
 int skg_nccl_unique_id(char* out128) {
     ncclUniqueId id;
-    const ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) return fail(SKG_ENCCL, ncclGetErrorString(r));
+    if (!nccl().ok) return fail(SKG_ENCCL, nccl().why);
+    const ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(r));
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(out128, &id, sizeof(id));
     return SKG_OK;
@@ -1118,8 +1180,9 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         if (ok && nccl_id) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
-            const ncclResult_t nr = ncclCommInitRank(&c->comm, world, id, rank);
-            if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
+            if (!nccl().ok) return cleanup(SKG_ENCCL, nccl().why);
+            const ncclResult_t nr = nccl().CommInitRank(&c->comm, world, id, rank);
+            if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(nr));
         }
     } else if (c->dist) {
         const int Kc = c->kc[1] + 1, PP = (Kc + 1) / 2;
@@ -1145,8 +1208,9 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         if (ok && nccl_id) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
-            const ncclResult_t nr = ncclCommInitRank(&c->comm, world, id, rank);
-            if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(nr));
+            if (!nccl().ok) return cleanup(SKG_ENCCL, nccl().why);
+            const ncclResult_t nr = nccl().CommInitRank(&c->comm, world, id, rank);
+            if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(nr));
         }
     } else {
         ok = ok && alloc((void**)&c->u, sizeof(cd) * S * c->nvars);
@@ -1225,7 +1289,7 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->cmfull);
     cudaFree(c->d_kowner);
     cudaFree(c->d_cstart);
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) nccl().CommDestroy(c->comm);
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;

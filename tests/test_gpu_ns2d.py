@@ -219,3 +219,22 @@ def test_run_series_matches_reference(ref_lib, n, noise):
         assert abs(series[i, 1] - r.enstrophy) < 1e-11 * r.enstrophy
         assert abs(series[i, 2] - eps) < 1e-11 * eps
     assert O.rel_l2(g.get_state(), r.get_state()) < PARITY
+
+
+def test_largest_fused_extent_8192(ref_lib):
+    """8192 x 8192 (512-thread lines) through the fused path and the transform
+    operators: 2 RK4 steps vs the reference (multi-threaded CPU oracle)."""
+    n = (8192, 8192)
+    u0 = ic.ns2d_ic(n, seed=5)
+    dt = ic.cfl_dt("ns2d", n, u0)
+    g = api.Simulation("ns2d", n, 1e-4, dt)
+    g.set_state(u0)
+    assert g.pruned
+    g.step(2)
+    ref_lib.set_workers(16)
+    r = ref_lib.RefSimulation("ns2d", n, 1e-4, dt)
+    r.set_state(u0)
+    r.step(2)
+    assert O.rel_l2(g.get_state()[0], r.get_state()[0]) < 1e-10
+    u = np.random.default_rng(1).standard_normal((8192,))
+    assert np.abs(api.fft_forward(u) - np.fft.rfft(u) / u.size).max() < 1e-14
