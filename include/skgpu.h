@@ -62,6 +62,8 @@ const char* skg_last_error(void);
  * Extents: any even n >= 4, as the reference (grid.cpp:34-44).  Powers of
  * two (ns2d 4..8192, ns3d 8..1024) run the fused kernels; other extents run
  * the generic step (one pass per reference operator, csrc/generic.cu).
+ * ns3d grids whose full layout would not fit in free device memory get the
+ * compact layout of skg_create_dist(world = 1) (dealiased states only).
  */
 int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                double dealias_coef, double nu, int scheme, int device);

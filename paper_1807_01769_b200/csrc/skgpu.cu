@@ -1116,6 +1116,15 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     bool ok = true;
     // slab layout: several partitions, or the compact one-partition ns3d
     // layout requested through skg_create_dist(world = 1)
+    // ns3d on one GPU: the compact layout when the full one would not fit
+    // (1024^3: ~220 GB full vs ~135 GB compact); it needs dealiased states
+    if (sid == 3 && world == 1 && !slab_one && !generic) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const double full = 16.0 * (double)c->S * (3.0 * 4 + 3.0) +
+                            16.0 * 11.0 * (double)n[0] * n[1] * c->nh;
+        if (full > 0.92 * (double)fr) slab_one = true;
+    }
     c->dist = world > 1 || (sid == 3 && slab_one);
     c->G = world;
     c->grank = rank;
@@ -1627,10 +1636,16 @@ int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, doub
 }
 
 int skg_energy(skg_ctx* c, double* energy, double* enstrophy) {
-    if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_energy on a slab-decomposed context");
     CUDA_TRY(cudaSetDevice(c->device));
-    CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, energy_mode(c),
-                                c->d_red, c->stream, &c->launches));
+    if (c->dist) {  // gather the slabs into the reference layout (io), reduce there
+        int rc = store_state_to_io(c, c->u);
+        if (rc) return rc;
+        CUDA_TRY(skg::launch_energy(c->io, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 2 : 0,
+                                    c->d_red, c->stream, &c->launches));
+    } else {
+        CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, energy_mode(c),
+                                    c->d_red, c->stream, &c->launches));
+    }
     double h[3];
     CUDA_TRY(cudaMemcpyAsync(h, c->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));

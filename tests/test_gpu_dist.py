@@ -26,6 +26,9 @@ def test_slab_matches_single_partition(n, world):
     # same kernels and arithmetic per element: expected bit-identical
     assert O.rel_l2(a, b) < 1e-14
     assert d.iteration == 5
+    ea, za = d.energy_enstrophy()
+    eb, zb = one.energy_enstrophy()
+    assert abs(ea - eb) <= 1e-13 * eb and abs(za - zb) <= 1e-13 * zb
 
 
 def test_slab_matches_reference(ref_lib):
@@ -134,6 +137,9 @@ def test_compact_layout_matches_full(n):
         assert O.rel_l2(s[v], r[v]) < 1e-14
     mask = O.dealias_mask(n).astype(bool)
     assert np.all(s[:, ~mask] == 0)
+    e1, _ = c.energy_enstrophy()
+    e2, _ = one.energy_enstrophy()
+    assert abs(e1 - e2) <= 1e-13 * e2
 
 
 def test_compact_layout_rejects_undealiased_state():
