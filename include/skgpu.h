@@ -177,6 +177,9 @@ int skg_last_divergence(const skg_ctx* ctx, long* iteration, int* var);
 /* Energy / enstrophy of the current state (Simulation::energy/enstrophy,
  * simulation.cpp:592-615), reduced on the device. */
 int skg_energy(skg_ctx* ctx, double* energy, double* enstrophy);
+/* Simulation::energy, enstrophy and dissipation_rate (simulation.cpp:592-615)
+ * of the current state in one device reduction: out3 = {E, Z, eps}. */
+int skg_diagnostics(skg_ctx* ctx, double* out3);
 
 /* 1 if the dealiased (pruned) fast path is active for the current state. */
 int skg_pruned(const skg_ctx* ctx);

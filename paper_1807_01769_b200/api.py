@@ -24,6 +24,8 @@ SKG_OK, SKG_ECONFIG, SKG_ESHAPE, SKG_EDIVERGENCE, SKG_ECUDA, SKG_ENCCL, SKG_EUNS
 SKG_RK4, SKG_RK2 = 0, 1
 
 KEYS_STATE_SPECT = {"ns2d": ["rot_fft"], "ns3d": ["vx_fft", "vy_fft", "vz_fft"]}
+KEYS_STATE_PHYS = {"ns2d": ["rot"], "ns3d": ["vx", "vy", "vz"]}
+KEYS_COMPUTABLE = {"ns2d": ["ux", "uy"], "ns3d": ["rotz"]}  # solvers.cpp:196, 359
 
 EXPORTS = [
     "skg_version", "skg_last_error", "skg_create", "skg_destroy", "skg_set_stream",
@@ -33,7 +35,7 @@ EXPORTS = [
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
-    "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity",
+    "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
 ]
 
 
@@ -117,6 +119,7 @@ def load_library():
     L.skg_last_dt.restype = C.c_double
     L.skg_set_time.argtypes = [vp, C.c_double]
     L.skg_max_velocity.argtypes = [vp, C.c_void_p, C.c_void_p]
+    L.skg_diagnostics.argtypes = [vp, C.c_void_p]
     _lib = L
     return L
 
@@ -234,6 +237,60 @@ class Simulation:
         self._h = h
         self.nvars = L_.skg_nvars(h)
         self.keys_state_spect = KEYS_STATE_SPECT[solver]
+        self.L = tuple(float(x) for x in (L if L is not None else [2 * np.pi] * self.dims))
+        self._cfl = None          # (cfl_coef, dt_max) when the dt is adaptive
+        self._t_end = None        # stopping rule of run() (Simulation::run)
+        self._n_iters = None
+
+    # --------------------------------------------- reference-style construction
+    @classmethod
+    def from_params(cls, params, device: int = 0, **kw):
+        """From the reference's parameter leaves (create_default_params,
+        simulation.cpp:73-125): a dict (or anything with .get) keyed by leaf
+        path -- "solver", "nu_2", "oper.nx", "oper.Lx", "oper.dealias_coef",
+        "time_stepping.scheme", "fixed_dt", "cfl_coef", "dt_max", "t_end",
+        "n_iters".  fixed_dt = 0 selects the CFL dt.  Exactly one stopping
+        rule, as the reference checks (simulation.cpp:246-251)."""
+        g = params.get
+        solver = g("solver")
+        if solver not in KEYS_STATE_SPECT:
+            raise ConfigError(f"unknown solver '{solver}' (registered: ns2d, ns3d)")
+        dims = 2 if solver == "ns2d" else 3
+        n = tuple(int(g(f"oper.{a}", 16)) for a in ("nx", "ny", "nz")[:dims])
+        L = [float(g(f"oper.L{a}", 2 * np.pi)) for a in "xyz"[:dims]]
+        t_end = float(g("time_stepping.t_end", 1.0))
+        n_iters = int(g("time_stepping.n_iters", -1))
+        if (t_end >= 0.0) == (n_iters >= 0):
+            raise ConfigError("exactly one stopping rule: set time_stepping.t_end >= 0 "
+                              "or time_stepping.n_iters >= 0, not both")
+        fixed_dt = float(g("time_stepping.fixed_dt", 0.0))
+        if fixed_dt < 0.0:
+            raise ConfigError("time_stepping.fixed_dt must be >= 0")
+        sim = cls(solver, n, float(g("nu_2", 0.0)), fixed_dt, str(g("time_stepping.scheme", "RK4")),
+                  L=L, dealias_coef=float(g("oper.dealias_coef", 2.0 / 3.0)), device=device, **kw)
+        if fixed_dt == 0.0:
+            sim.set_cfl(float(g("time_stepping.cfl_coef", 0.5)), float(g("time_stepping.dt_max", 0.1)))
+        if n_iters >= 0:
+            sim.set_n_iters(n_iters)
+        else:
+            sim.set_t_end(t_end)
+        return sim
+
+    @property
+    def solver_name(self) -> str:
+        return self.solver
+
+    @property
+    def shape(self):
+        return list(self.n)
+
+    @property
+    def state_keys(self):
+        return list(KEYS_STATE_PHYS[self.solver])
+
+    @property
+    def computable_keys(self):
+        return list(KEYS_COMPUTABLE[self.solver])
 
     # ------------------------------------------------------------ lifecycle
     def close(self):
@@ -288,6 +345,41 @@ class Simulation:
     def step_once(self, dt: float | None = None) -> None:
         self.step(1, dt)
 
+    def set_fixed_dt(self, dt: float) -> None:
+        """Simulation::set_fixed_dt: a fixed dt (> 0) instead of the CFL dt."""
+        if not dt > 0.0:
+            raise ConfigError("fixed dt must be > 0")
+        self.dt = float(dt)
+        if self._cfl is not None:
+            self._call("skg_set_cfl", C.c_double(0.0), C.c_double(0.1), C.c_double(-1.0))
+            self._cfl = None
+
+    def set_n_iters(self, n: int) -> None:
+        """Simulation::set_n_iters: run() takes n steps (simulation.cpp:617-620)."""
+        self._n_iters, self._t_end = int(n), None
+        if self._cfl is not None:
+            self._call("skg_set_cfl", C.c_double(self._cfl[0]), C.c_double(self._cfl[1]), C.c_double(-1.0))
+
+    def set_t_end(self, t_end: float) -> None:
+        """Simulation::set_t_end: run() stops at t_end, the last dt clamped."""
+        self._t_end, self._n_iters = float(t_end), None
+        if self._cfl is not None:
+            self._call("skg_set_cfl", C.c_double(self._cfl[0]), C.c_double(self._cfl[1]),
+                       C.c_double(self._t_end))
+
+    def compute_dt(self) -> float:
+        """Simulation::compute_dt (simulation.cpp:463-476) for the current state."""
+        if self._cfl is None:
+            dt = self.dt
+        else:
+            m = self.max_velocity(self.get_state())
+            dt = self._cfl[1]
+            for d in range(self.dims):
+                dt = min(dt, self._cfl[0] * (self.L[d] / self.n[d]) / max(abs(m[d]), 1e-30))
+        if self._t_end is not None and self._t_end >= 0.0:
+            dt = min(dt, self._t_end - self.t)
+        return dt
+
     def set_cfl(self, cfl_coef: float = 0.5, dt_max: float = 0.1, t_end: float | None = None) -> None:
         """Adaptive dt as the reference's time_stepping with fixed_dt = 0
         (compute_dt, simulation.cpp:463-476): per step
@@ -295,6 +387,9 @@ class Simulation:
         computed on the device.  cfl_coef <= 0 returns to the fixed dt."""
         self._call("skg_set_cfl", C.c_double(cfl_coef), C.c_double(dt_max),
                    C.c_double(-1.0 if t_end is None else float(t_end)))
+        self._cfl = (float(cfl_coef), float(dt_max)) if cfl_coef > 0 else None
+        if t_end is not None:
+            self._t_end, self._n_iters = float(t_end), None
 
     @property
     def last_dt(self) -> float:
@@ -314,15 +409,46 @@ class Simulation:
     def sync(self) -> None:
         self._call("skg_sync")
 
-    def run(self, n_iters: int, dt: float | None = None):
-        """Simulation::run with n_iters (simulation.cpp:565-590).  Returns the
-        per-step means the reference's OutputManager records every step
-        (output.cpp:204-214): an (n_iters, 3) array of energy, enstrophy and
-        dissipation rate after each step."""
-        dt = self.dt if dt is None else float(dt)
-        series = np.zeros((int(n_iters), 3), np.float64)
-        self._call("skg_run", C.c_double(dt), C.c_long(int(n_iters)), _ptr(series))
-        return series
+    def run(self, n_iters: int | None = None, dt: float | None = None):
+        """Simulation::run (simulation.cpp:565-590).
+
+        With n_iters: that many steps; returns the per-step means the
+        reference's OutputManager records every step (output.cpp:204-214) --
+        an (n_iters, 3) array of energy, enstrophy and dissipation rate.
+        Without: the configured stopping rule (set_n_iters / set_t_end; t_end
+        clamps the last dt like compute_dt and stops at t >= t_end - 1e-12);
+        returns the RunSummary fields {"iterations", "t_final", "walltime"}
+        plus "means" (the per-step series)."""
+        if n_iters is not None:
+            dt = self.dt if dt is None else float(dt)
+            series = np.zeros((int(n_iters), 3), np.float64)
+            self._call("skg_run", C.c_double(dt), C.c_long(int(n_iters)), _ptr(series))
+            return series
+        import time as _time
+        t0 = _time.perf_counter()
+        chunks = []
+        if self._n_iters is not None:
+            chunks.append(self.run(self._n_iters) if self._n_iters > 0 else np.zeros((0, 3)))
+        elif self._t_end is not None:
+            while self.t < self._t_end - 1e-12:
+                if self._cfl is not None:   # the device clamps dt to t_end
+                    chunks.append(self.run(1))
+                    continue
+                # fixed dt: the full steps, then one clamped step (t += dt in
+                # double, as step_once accumulates it)
+                k, t = 0, self.t
+                while self._t_end - t >= self.dt and t < self._t_end - 1e-12:
+                    t += self.dt
+                    k += 1
+                if k:
+                    chunks.append(self.run(k))
+                if self.t < self._t_end - 1e-12:
+                    chunks.append(self.run(1, dt=self._t_end - self.t))
+        else:
+            raise ConfigError("run(): no stopping rule (set_n_iters or set_t_end)")
+        means = np.concatenate(chunks) if chunks else np.zeros((0, 3))
+        return {"iterations": len(means), "t_final": self.t,
+                "walltime": _time.perf_counter() - t0, "means": means}
 
     def max_velocity(self, spect: np.ndarray) -> np.ndarray:
         """Solver::max_velocity_per_axis of `spect` (solvers.cpp:176-194, 341-357)."""
@@ -406,8 +532,54 @@ class Simulation:
         self._call("skg_energy", C.byref(e), C.byref(z))
         return e.value, z.value
 
+    def diagnostics(self):
+        """(energy, enstrophy, dissipation rate) of the current state."""
+        out = np.zeros(3, np.float64)
+        self._call("skg_diagnostics", _ptr(out))
+        return tuple(float(x) for x in out)
+
     def energy(self) -> float:
         return self.energy_enstrophy()[0]
 
     def enstrophy(self) -> float:
         return self.energy_enstrophy()[1]
+
+    def dissipation_rate(self) -> float:
+        """Simulation::dissipation_rate (simulation.cpp:608-615)."""
+        return self.diagnostics()[2]
+
+    # ---------------------------------------------------- physical fields
+    def get_phys(self, key: str) -> np.ndarray:
+        """Physical values of a state or computable field (bindings.cpp:123-129):
+        ns2d "rot", "ux", "uy" (velocity_from_vorticity2d, grid.cpp:251-274);
+        ns3d "vx", "vy", "vz", "rotz" (solvers.cpp:361-375).  Transforms on
+        the GPU (FftPlan::inverse)."""
+        s = self.get_state()
+        if key in KEYS_STATE_PHYS[self.solver]:
+            return self.fft_inverse(s[KEYS_STATE_PHYS[self.solver].index(key)])
+        if key not in KEYS_COMPUTABLE[self.solver]:
+            raise ConfigError(f"unknown state variable '{key}'")
+        ks, _ = self.grid()
+        if self.solver == "ns2d":
+            kx, ky = ks[0][:, None], ks[1][None, :]
+            ksq = kx * kx + ky * ky
+            with np.errstate(divide="ignore", invalid="ignore"):
+                psi = np.where(ksq == 0.0, 0.0, s[0] / np.where(ksq == 0.0, 1.0, ksq))
+            f = 1j * ky * psi if key == "ux" else -1j * kx * psi
+        else:
+            kx, ky = ks[0][:, None, None], ks[1][None, :, None]
+            f = 1j * kx * s[1] - 1j * ky * s[0]
+        return self.fft_inverse(np.ascontiguousarray(f))
+
+    def set_phys(self, key: str, values: np.ndarray) -> None:
+        """StateSet::load_phys (state.cpp:59-69): one state variable from
+        physical values (forward transform on the GPU); no sanitizing."""
+        keys = KEYS_STATE_PHYS[self.solver]
+        if key not in keys:
+            raise ConfigError(f"unknown state variable '{key}'")
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if v.shape != self.n:
+            raise ShapeError("array shape does not match the grid")
+        s = self.get_state()
+        s[keys.index(key)] = self.fft_forward(v)
+        self.set_state(s)

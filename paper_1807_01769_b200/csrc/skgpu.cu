@@ -1636,21 +1636,32 @@ int skg_kernel_stats(skg_ctx* c, int cls, double* total_ms, long* launches, doub
 }
 
 int skg_energy(skg_ctx* c, double* energy, double* enstrophy) {
+    double d[3];
+    int rc = skg_diagnostics(c, d);
+    if (rc) return rc;
+    if (energy) *energy = d[0];
+    if (enstrophy) *enstrophy = d[1];
+    return SKG_OK;
+}
+
+int skg_diagnostics(skg_ctx* c, double* out3) {
+    if (!out3) return fail(SKG_ECONFIG, "skg_diagnostics: null output");
     CUDA_TRY(cudaSetDevice(c->device));
     if (c->dist) {  // gather the slabs into the reference layout (io), reduce there
         int rc = store_state_to_io(c, c->u);
         if (rc) return rc;
         CUDA_TRY(skg::launch_energy(c->io, c->dims, c->n, c->kscale, c->nvars, c->solver == 2 ? 2 : 0,
-                                    c->d_red, c->stream, &c->launches));
+                                    c->d_red, c->stream, &c->launches, c->nu));
     } else {
         CUDA_TRY(skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, energy_mode(c),
-                                    c->d_red, c->stream, &c->launches));
+                                    c->d_red, c->stream, &c->launches, c->nu));
     }
     double h[3];
     CUDA_TRY(cudaMemcpyAsync(h, c->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (energy) *energy = h[0];
-    if (enstrophy) *enstrophy = c->solver == 2 ? h[1] : 0.0;
+    out3[0] = h[0];
+    out3[1] = c->solver == 2 ? h[1] : 0.0;  // ns3d: no enstrophy (simulation.cpp:599-606)
+    out3[2] = h[2];
     return SKG_OK;
 }
 
