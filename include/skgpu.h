@@ -122,6 +122,20 @@ int skg_get_state_device(skg_ctx* ctx, double* d_spect_out);
  * cfl_coef <= 0 returns to the caller's fixed dt.  skg_last_dt = the dt of
  * the last completed step; skg_set_time sets t (restart).
  */
+/*
+ * Random band forcing (forcing.enable, simulation.cpp:482-548): before each
+ * step a unit-magnitude random field in the shell band [k_lo, k_hi]
+ * (random_field, grid.cpp:276-306; white noise from the reference's own
+ * std::mt19937_64(seed) + std::normal_distribution on the host, the rest on
+ * the device) is split so that it injects exactly `rate` (or the unit-energy
+ * fallback) and is added to the tendency of every RK stage.  The band must
+ * exclude the mean shell and lie inside the dealiasing cut.  Steps with
+ * forcing are not graph-replayed (host noise every step).
+ * skg_last_injection = Simulation::last_injection of the last step.
+ */
+int skg_set_forcing(skg_ctx* ctx, int enable, double k_lo, double k_hi, double rate, long seed);
+double skg_last_injection(const skg_ctx* ctx);
+
 int skg_set_cfl(skg_ctx* ctx, double cfl_coef, double dt_max, double t_end);
 double skg_last_dt(const skg_ctx* ctx);
 int skg_set_time(skg_ctx* ctx, double t);

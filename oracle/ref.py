@@ -46,6 +46,11 @@ def lib():
         L.skref_create.argtypes = [C.POINTER(C.c_void_p), C.c_char_p, C.c_int, ip,
                                    C.c_double, C.c_double, C.c_int, C.c_double]
         L.skref_destroy.argtypes = [C.c_void_p]
+        L.skref_create_forced.argtypes = [C.POINTER(C.c_void_p), C.c_char_p, C.c_int, ip,
+                                          C.c_double, C.c_double, C.c_int, C.c_double,
+                                          C.c_double, C.c_double, C.c_double, C.c_long]
+        L.skref_last_injection.argtypes = [C.c_void_p]
+        L.skref_last_injection.restype = C.c_double
         for f in ("skref_spect_size", "skref_phys_size", "skref_iteration"):
             getattr(L, f).argtypes = [C.c_void_p]
             getattr(L, f).restype = C.c_long
@@ -103,14 +108,21 @@ class RefSimulation:
     and forcing off, fixed dt and an injected spectral state."""
 
     def __init__(self, solver: str, n, nu: float, dt: float, scheme: str = "RK4",
-                 dealias_coef: float = 2.0 / 3.0):
+                 dealias_coef: float = 2.0 / 3.0, forcing=None):
+        """forcing: None, or (k_lo, k_hi, rate, seed) for forcing.enable = true."""
         self.solver = solver
         self.n = tuple(int(x) for x in n)
         h = C.c_void_p()
         cn = (C.c_int * len(self.n))(*self.n)
-        _check(lib().skref_create(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
-                                  float(dt), 1 if scheme.upper() == "RK2" else 0,
-                                  float(dealias_coef)))
+        rk2 = 1 if scheme.upper() == "RK2" else 0
+        if forcing is None:
+            _check(lib().skref_create(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
+                                      float(dt), rk2, float(dealias_coef)))
+        else:
+            klo, khi, rate, seed = forcing
+            _check(lib().skref_create_forced(C.byref(h), solver.encode(), len(self.n), cn,
+                                             float(nu), float(dt), rk2, float(dealias_coef),
+                                             float(klo), float(khi), float(rate), int(seed)))
         self._h = h
         self.nvars = lib().skref_nvars(h)
         self.spect_shape = self.n[:-1] + (self.n[-1] // 2 + 1,)
@@ -178,6 +190,10 @@ class RefSimulation:
     @property
     def enstrophy(self) -> float:
         return lib().skref_enstrophy(self._h)
+
+    @property
+    def last_injection(self) -> float:
+        return lib().skref_last_injection(self._h)
 
     @property
     def t(self) -> float:

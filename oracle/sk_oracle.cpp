@@ -86,8 +86,30 @@ const char* skref_last_error(void) { return g_err.c_str(); }
 
 void skref_set_workers(int n) { set_fft_workers(n); }
 
+static int create_impl(RefSim** out, const char* solver, int dims, const int* n, double nu,
+                       double fixed_dt, int scheme_rk2, double dealias_coef, int forcing,
+                       double k_lo, double k_hi, double rate, long seed);
+
 int skref_create(RefSim** out, const char* solver, int dims, const int* n, double nu,
                  double fixed_dt, int scheme_rk2, double dealias_coef) {
+    return create_impl(out, solver, dims, n, nu, fixed_dt, scheme_rk2, dealias_coef, 0, 2.0, 4.0,
+                       1.0, 1234);
+}
+
+// The same with forcing.enable = true and its band, rate and seed
+// (create_default_params forcing.*, simulation.cpp:112-117).
+int skref_create_forced(RefSim** out, const char* solver, int dims, const int* n, double nu,
+                        double fixed_dt, int scheme_rk2, double dealias_coef, double k_lo,
+                        double k_hi, double rate, long seed) {
+    return create_impl(out, solver, dims, n, nu, fixed_dt, scheme_rk2, dealias_coef, 1, k_lo, k_hi,
+                       rate, seed);
+}
+
+double skref_last_injection(RefSim* rs) { return rs->sim->last_injection(); }
+
+static int create_impl(RefSim** out, const char* solver, int dims, const int* n, double nu,
+                       double fixed_dt, int scheme_rk2, double dealias_coef, int forcing,
+                       double k_lo, double k_hi, double rate, long seed) {
     *out = nullptr;
     return guard([&] {
         ensure_builtin_solvers();
@@ -98,7 +120,13 @@ int skref_create(RefSim** out, const char* solver, int dims, const int* n, doubl
         if (dealias_coef > 0) p.set("oper.dealias_coef", dealias_coef);
         p.set("nu_2", nu);
         p.set("output.enable_files", false);
-        p.set("forcing.enable", false);
+        p.set("forcing.enable", forcing != 0);
+        if (forcing) {
+            p.set("forcing.k_lo", k_lo);
+            p.set("forcing.k_hi", k_hi);
+            p.set("forcing.rate", rate);
+            p.set("forcing.seed", static_cast<std::int64_t>(seed));
+        }
         p.set("time_stepping.scheme", std::string(scheme_rk2 ? "RK2" : "RK4"));
         p.set("time_stepping.fixed_dt", fixed_dt);
         p.set("time_stepping.t_end", -1.0);

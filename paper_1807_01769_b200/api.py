@@ -36,6 +36,7 @@ EXPORTS = [
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
+    "skg_set_forcing", "skg_last_injection",
 ]
 
 
@@ -120,6 +121,9 @@ def load_library():
     L.skg_set_time.argtypes = [vp, C.c_double]
     L.skg_max_velocity.argtypes = [vp, C.c_void_p, C.c_void_p]
     L.skg_diagnostics.argtypes = [vp, C.c_void_p]
+    L.skg_set_forcing.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_double, C.c_long]
+    L.skg_last_injection.argtypes = [vp]
+    L.skg_last_injection.restype = C.c_double
     _lib = L
     return L
 
@@ -274,6 +278,9 @@ class Simulation:
             sim.set_n_iters(n_iters)
         else:
             sim.set_t_end(t_end)
+        if g("forcing.enable", False):
+            sim.set_forcing(float(g("forcing.k_lo", 2.0)), float(g("forcing.k_hi", 4.0)),
+                            float(g("forcing.rate", 1.0)), int(g("forcing.seed", 1234)))
         return sim
 
     @property
@@ -344,6 +351,19 @@ class Simulation:
     # ---------------------------------------------------------------- stepping
     def step_once(self, dt: float | None = None) -> None:
         self.step(1, dt)
+
+    def set_forcing(self, k_lo: float = 2.0, k_hi: float = 4.0, rate: float = 1.0, seed: int = 1234,
+                    enable: bool = True) -> None:
+        """forcing.* (simulation.cpp:112-117, 482-548): random band forcing
+        injecting `rate`, refreshed before every step from the reference's
+        own generator seeded with `seed`."""
+        self._call("skg_set_forcing", C.c_int(1 if enable else 0), C.c_double(k_lo),
+                   C.c_double(k_hi), C.c_double(rate), C.c_long(int(seed)))
+
+    @property
+    def last_injection(self) -> float:
+        """Simulation::last_injection of the last step."""
+        return load_library().skg_last_injection(self._h)
 
     def set_fixed_dt(self, dt: float) -> None:
         """Simulation::set_fixed_dt: a fixed dt (> 0) instead of the CFL dt."""

@@ -164,8 +164,10 @@ __global__ void g_post(GenArgs a, cd* nl, int stage, cd* kout) {
             const cd sp = mk(dot.x / m.ksq, dot.y / m.ksq);
             for (int v = 0; v < 3; ++v) c[v] = sub(c[v], scale(sp, m.k[v]));
         }
-        for (int v = 0; v < a.nvars; ++v)
+        for (int v = 0; v < a.nvars; ++v) {
             if (!m.kept || mean) c[v] = zero();
+            if (a.force) c[v] = add(c[v], a.force[(size_t)v * a.S + q]);  // simulation.cpp:544-547
+        }
         const double e1 = a.has_sigma ? efac(a.e1, a, m) : 1.0;
         const double e2 = a.has_sigma ? efac(a.e2, a, m) : 1.0;
         for (int v = 0; v < a.nvars; ++v) {

@@ -382,8 +382,9 @@ __global__ void __launch_bounds__(BFFT<NX>::T > 256 ? BFFT<NX>::T : 256, BFFT<NX
         bool keep = abs(si) <= a.kcx;
         if (i == 0 && ky == 0) keep = false;  // mean mode of the tendency is 0
         if (!keep && a.pruned) continue;
-        const cd kv = keep ? v[e] : zero();
         const size_t idx = (size_t)ky * NX + i;
+        cd kv = keep ? v[e] : zero();
+        if (a.force && keep) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
         if (!final) {
             kout[idx] = kv;
         } else {
@@ -639,8 +640,9 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
             continue;
         }
         const double kxv = a.kx_scale * (double)si;
-        const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
         const size_t idx = (size_t)kyl * NX + i;
+        cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
+        if (a.force) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
         cd wn = zero();  // next stage state (fused)
         if (!final) {
             kout[idx] = kv;

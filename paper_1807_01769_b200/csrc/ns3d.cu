@@ -643,7 +643,8 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const size_t idx = base + c * a.vstride;
-            const cd kv = kc[c];
+            cd kv = kc[c];
+            if (a.force && keep) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
             if (!final) {
                 kout[idx] = kv;
                 continue;

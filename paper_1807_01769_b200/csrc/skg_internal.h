@@ -90,6 +90,7 @@ struct Ns2dArgs {
     double dt, hdt, sdt;
     DynStep* dyn;       // adaptive dt (nullptr: the fixed dt above)
     int ystage;         // RK stage of the physical pass (stage 1 feeds the CFL max)
+    const cd* force;    // forcing addend in the state layout (nullptr: off)
     const double* e1x;  // exp(0.5 dt (-nu kx^2)) per kx index (nx)
     const double* e1y;  // exp(0.5 dt (-nu ky^2)) per ky index (nh)
     const double* e2x;  // exp(dt (-nu kx^2))
@@ -175,6 +176,7 @@ struct Ns3dArgs {
     double dt, hdt, sdt;
     DynStep* dyn;       // adaptive dt (nullptr: the fixed dt above)
     int ystage;         // RK stage of the physical pass (stage 1 feeds the CFL max)
+    const cd* force;    // forcing addend in the state layout (nullptr: off)
     const double *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
     cd* u;               // 3 variables, each nx*ny*nh (reference layout)
     cd* k1;
@@ -277,6 +279,7 @@ struct GenArgs {
     const double* e2[3];
     cd *u, *k1, *k2, *k3;
     DevFlags* flags;
+    const cd* force;  // forcing addend (nullptr: off)
 };
 struct GenScratch {
     cd* w;        // stage state (nvars S)
@@ -291,6 +294,20 @@ cudaError_t generic_stage(const GenArgs& a, int stage, GenScratch& g, cudaStream
 // when a.dyn is set.
 cudaError_t generic_tendency(const GenArgs& a, const cd* w, int stage, cd* kout, GenScratch& g,
                              cudaStream_t s, long* launches);
+
+// Random band forcing (forcing.cu), reference layout.
+struct ForceGeo {
+    int dims, n[3], nh, kc[3], nvars;
+    double ks[3];
+    long long S;
+    double delta_k, k_lo, k_hi;
+};
+// band filter + unit magnitude + prepare_forcing of the transformed noise f
+cudaError_t forcing_shape(const ForceGeo& g, cd* f, cudaStream_t s, long* launches);
+// reductions against the state u, the rate split, f <- alpha f + beta ub;
+// red: 8 doubles (red[6] = last injection, red[7] = 1 on the fallback)
+cudaError_t forcing_finish(const ForceGeo& g, const cd* u, cd* f, double rate, double* red,
+                           cudaStream_t s, long* launches);
 
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KP, typename... A>

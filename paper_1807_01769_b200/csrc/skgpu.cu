@@ -13,6 +13,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <random>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -229,6 +230,17 @@ struct skg_ctx {
     bool generic = false;
     skg::GenScratch gs{};
 
+    // random band forcing (skg_set_forcing): host generator of the reference
+    bool forcing = false;
+    double f_klo = 2.0, f_khi = 4.0, f_rate = 1.0;
+    std::mt19937_64 f_rng;
+    cd* f_ref = nullptr;       // nvars S, reference layout
+    cd* f_cm = nullptr;        // ns2d fused kernels: CM layout copy
+    double* f_noise = nullptr; // pinned host, nvars P
+    double* f_red = nullptr;   // device: reductions, coefficients, injection
+    double last_injection = 0.0;
+    long forcing_fallbacks = 0;
+
     // adaptive (CFL) dt: skg_set_cfl
     bool adaptive = false;
     double cfl = 0.5, dt_max = 0.1, t_end = -1.0, last_dt = 0.0;
@@ -365,6 +377,7 @@ skg::Ns2dArgs args2d(skg_ctx* c, double dt) {
     a.e2x = etab_ptr(c, 1, 0);
     a.e2y = etab_ptr(c, 1, 1);
     a.dyn = c->adaptive ? c->d_dyn : nullptr;
+    a.force = c->forcing ? (c->f_cm ? c->f_cm : c->f_ref) : nullptr;
     a.u = c->u;
     a.k1 = c->k[0];
     a.k2 = c->k[1];
@@ -448,6 +461,7 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.e2y = etab_ptr(c, 1, 1);
     a.e2z = etab_ptr(c, 1, 2);
     a.dyn = c->adaptive ? c->d_dyn : nullptr;
+    a.force = c->forcing ? c->f_ref : nullptr;
     a.u = c->u;
     a.k1 = c->k[0];
     a.k2 = c->k[1];
@@ -531,7 +545,62 @@ skg::GenArgs args_gen(skg_ctx* c, double dt) {
     a.k2 = c->k[1];
     a.k3 = c->k[2];
     a.flags = c->flags;
+    a.force = c->forcing ? c->f_ref : nullptr;
     return a;
+}
+
+skg::ForceGeo force_geo(const skg_ctx* c) {
+    skg::ForceGeo g{};
+    g.dims = c->dims;
+    double Lmax = 0.0;
+    for (int d = 0; d < c->dims; ++d) {
+        g.n[d] = c->n[d];
+        g.kc[d] = c->kc[d];
+        g.ks[d] = c->kscale[d];
+        Lmax = std::max(Lmax, c->L[d]);
+    }
+    g.nh = c->nh;
+    g.nvars = c->nvars;
+    g.S = c->S;
+    g.delta_k = kTwoPi / Lmax;  // grid.cpp:65
+    g.k_lo = c->f_klo;
+    g.k_hi = c->f_khi;
+    return g;
+}
+
+int store_state_to_io(skg_ctx* c, const cd* src);
+
+// Simulation::refresh_forcing (simulation.cpp:482-533) before a step: the
+// reference's generator fills the white noise on the host (one
+// normal_distribution per variable, random_field grid.cpp:285-288), the rest
+// runs on the device (forcing.cu).
+int refresh_forcing(skg_ctx* c) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // the pinned noise buffer is reused
+    const size_t P = (size_t)c->P;
+    const cd* tw[3] = {c->tw[0], c->tw[1], c->tw[2]};
+    for (int v = 0; v < c->nvars; ++v) {
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        double* h = c->f_noise + v * P;
+        for (size_t i = 0; i < P; ++i) h[i] = gauss(c->f_rng);
+    }
+    const skg::ForceGeo g = force_geo(c);
+    for (int v = 0; v < c->nvars; ++v) {
+        CUDA_TRY(cudaMemcpyAsync(c->phys, c->f_noise + v * P, sizeof(double) * P, cudaMemcpyHostToDevice,
+                                 c->stream));
+        CUDA_TRY(skg::fft_forward_dev(c->dims, c->n, c->phys, c->f_ref + (size_t)v * c->S, c->work, tw,
+                                      c->stream, &c->launches));
+    }
+    CUDA_TRY(skg::forcing_shape(g, c->f_ref, c->stream, &c->launches));
+    const cd* uref = c->u;
+    if (c->f_cm) {  // ns2d fused kernels keep the state in CM layout
+        int rc = store_state_to_io(c, c->u);
+        if (rc) return rc;
+        uref = c->io;
+    }
+    CUDA_TRY(skg::forcing_finish(g, uref, c->f_ref, c->f_rate, c->f_red, c->stream, &c->launches));
+    if (c->f_cm)
+        CUDA_TRY(skg::launch_transpose_c(c->f_ref, c->f_cm, c->n[0], c->nh, 0, c->stream, &c->launches));
+    return SKG_OK;
 }
 
 int sync_and_check(skg_ctx* c, long nsteps, double dt) {
@@ -539,6 +608,11 @@ int sync_and_check(skg_ctx* c, long nsteps, double dt) {
     harvest(c);
     skg::DevFlags f;
     CUDA_TRY(cudaMemcpy(&f, c->flags, sizeof(f), cudaMemcpyDeviceToHost));
+    if (c->forcing) {
+        double r[8];
+        CUDA_TRY(cudaMemcpy(r, c->f_red, sizeof(r), cudaMemcpyDeviceToHost));
+        c->last_injection = r[6];
+    }
     skg::DynStep dyn{};
     if (c->adaptive) {
         CUDA_TRY(cudaMemcpy(&dyn, c->d_dyn, sizeof(dyn), cudaMemcpyDeviceToHost));
@@ -841,6 +915,14 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
         return e;
     };
     long s = 0;
+    if (c->forcing) {  // host noise every step: no graph replay
+        for (; s < nsteps; ++s) {
+            int rc2 = refresh_forcing(c);
+            if (rc2) return rc2;
+            CUDA_TRY(one_step(&c->launches, s == 0, s == nsteps - 1));
+        }
+        return SKG_OK;
+    }
     if (nsteps > 0) {  // first step eagerly (also sets kernel attributes)
         CUDA_TRY(one_step(&c->launches, true, nsteps == 1));
         s = 1;
@@ -1274,6 +1356,10 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->d_count);
     cudaFree(c->d_red);
     cudaFree(c->d_dyn);
+    cudaFree(c->f_ref);
+    cudaFree(c->f_cm);
+    cudaFree(c->f_red);
+    if (c->f_noise) cudaFreeHost(c->f_noise);
     cudaFree(c->gs.w);
     cudaFree(c->gs.spec);
     cudaFree(c->gs.nl);
@@ -1434,6 +1520,7 @@ static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax
     if (c->generic) {  // reference layout throughout; tendency into gs.nl
         skg::GenArgs a = args_gen(c, 1.0);
         a.dyn = umax ? c->d_dyn : nullptr;
+        a.force = nullptr;  // Solver::tendency has no forcing addend
         skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
         if (umax) CUDA_TRY(cudaMemsetAsync(c->d_dyn, 0, sizeof(skg::DynStep), c->stream));
@@ -1448,6 +1535,7 @@ static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax
         skg::Ns2dArgs a = args2d(c, c->cached_dt);
         a.u = c->k[2];
         a.dyn = umax ? c->d_dyn : nullptr;
+        a.force = nullptr;
         skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
         if (umax) CUDA_TRY(cudaMemsetAsync(c->d_dyn, 0, sizeof(skg::DynStep), c->stream));
@@ -1462,6 +1550,7 @@ static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax
         skg::Ns3dArgs a = args3d(c, c->cached_dt);
         a.u = c->k[2];
         a.dyn = umax ? c->d_dyn : nullptr;
+        a.force = nullptr;
         skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
         CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
         if (umax) CUDA_TRY(cudaMemsetAsync(c->d_dyn, 0, sizeof(skg::DynStep), c->stream));
@@ -1601,6 +1690,48 @@ int skg_set_cfl(skg_ctx* c, double cfl_coef, double dt_max, double t_end) {
 }
 
 double skg_last_dt(const skg_ctx* c) { return c->last_dt; }
+
+int skg_set_forcing(skg_ctx* c, int enable, double k_lo, double k_hi, double rate, long seed) {
+    if (!enable) {
+        c->forcing = false;
+        return SKG_OK;
+    }
+    // simulation.cpp:269-273 and random_field's checks (grid.cpp:277-280)
+    if (k_lo > k_hi) return fail(SKG_ECONFIG, "forcing band: k_lo must be <= k_hi");
+    if (!std::isfinite(rate)) return fail(SKG_ECONFIG, "forcing.rate must be finite");
+    if (!(k_lo >= 0) || !(k_hi > k_lo)) return fail(SKG_ECONFIG, "random_field: need 0 <= k_lo < k_hi");
+    if (c->dist) return fail(SKG_EUNSUPPORTED, "forcing on a slab-decomposed context");
+    double Lmax = 0.0, kmax2 = 0.0, kcut = 1e300;
+    for (int d = 0; d < c->dims; ++d) {
+        Lmax = std::max(Lmax, c->L[d]);
+        const double km = c->kscale[d] * (d == c->dims - 1 ? c->n[d] / 2 : c->n[d] / 2);
+        kmax2 += km * km;
+        kcut = std::min(kcut, c->coef * (kTwoPi / c->L[d]) * (c->n[d] / 2));  // grid.cpp:83-84
+    }
+    const double dk = kTwoPi / Lmax;
+    if (k_lo > std::sqrt(kmax2))
+        return fail(SKG_ECONFIG, "random_field: band lies above the largest resolved |k|");
+    if (k_lo < 0.5 * dk || k_hi + 0.5 * dk > kcut)
+        return fail(SKG_EUNSUPPORTED,
+                    "forcing band must exclude the mean shell and lie inside the dealiasing cut");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_fft_bufs(c)) return rc;
+    if (!c->f_ref) {
+        CUDA_TRY(cudaMalloc(&c->f_ref, sizeof(cd) * c->S * c->nvars));
+        CUDA_TRY(cudaMalloc(&c->f_red, 8 * sizeof(double)));
+        CUDA_TRY(cudaMallocHost(&c->f_noise, sizeof(double) * c->P * c->nvars));
+        if (c->solver == 2 && !c->generic) CUDA_TRY(cudaMalloc(&c->f_cm, sizeof(cd) * c->S));
+    }
+    c->forcing = true;
+    c->f_klo = k_lo;
+    c->f_khi = k_hi;
+    c->f_rate = rate;
+    c->f_rng.seed(static_cast<std::uint64_t>(seed));  // simulation.cpp:338-339
+    c->last_injection = 0.0;
+    return SKG_OK;
+}
+
+double skg_last_injection(const skg_ctx* c) { return c->last_injection; }
 
 int skg_set_time(skg_ctx* c, double t) {
     c->t = t;
