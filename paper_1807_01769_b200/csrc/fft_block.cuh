@@ -207,6 +207,22 @@ __device__ __forceinline__ void apply_twiddles(cd* u, cd w) {
     }
 }
 
+// Barrier of the threads that share one exchange buffer: the whole CTA
+// (bar == 0); otherwise only this line's T threads -- a named barrier
+// (bar = 1..15, T a multiple of 32) or the T-lane slice of one warp (T < 32)
+// -- so independent lines of one CTA do not wait for each other.
+template <int T>
+__device__ __forceinline__ void line_sync(int bar) {
+    if (bar == 0) {
+        __syncthreads();
+    } else if constexpr (T >= 32) {
+        asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(T) : "memory");
+    } else {
+        const unsigned lane = threadIdx.x & 31u;
+        __syncwarp(((1u << T) - 1u) << (lane & ~(unsigned)(T - 1)));
+    }
+}
+
 // Block FFT of a power-of-two length N in natural layout.  SPLIT exchanges
 // the real and imaginary parts in two rounds through an N-double buffer
 // (half the shared memory, twice the barriers).
@@ -280,7 +296,8 @@ struct BFFT {
     // salt (0..7) is XORed into the 16-byte slot index: lines interleaved
     // lane-by-lane in one warp (strided-axis kernels) then hit distinct banks.
     template <int S, int Ns, int P>
-    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const Bases& wb, int salt) {
+    __device__ __forceinline__ static void pass(cd* v, cd* sm, int t, const Bases& wb, int salt,
+                                                int bar) {
         constexpr int rem = N / Ns;
         constexpr int R = rem >= E ? E : rem;
         constexpr int B = E / R;  // butterflies per thread in this pass (> 1 only in the last)
@@ -316,34 +333,36 @@ struct BFFT {
                 const int base = (t / Ns) * Ns * R + (t & (Ns - 1));
 #pragma unroll
                 for (int r = 0; r < R; ++r) sd[pad8(base + r * Ns)] = v[r].x;
-                __syncthreads();
+                line_sync<T>(bar);
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e].x = sd[pad8(t + T * e)];
-                __syncthreads();
+                line_sync<T>(bar);
 #pragma unroll
                 for (int r = 0; r < R; ++r) sd[pad8(base + r * Ns)] = v[r].y;
-                __syncthreads();
+                line_sync<T>(bar);
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e].y = sd[pad8(t + T * e)];
-                __syncthreads();
+                line_sync<T>(bar);
             } else {
-                __syncthreads();
+                line_sync<T>(bar);
 #pragma unroll
                 for (int e = 0; e < E; ++e) v[e] = sm[pad(t + T * e) ^ salt];
-                __syncthreads();
+                line_sync<T>(bar);
             }
-            pass<S, Ns * R, P + 1>(v, sm, t, wb, salt);
+            pass<S, Ns * R, P + 1>(v, sm, t, wb, salt, bar);
         }
     }
 
+    // bar: 0 = CTA-wide barriers; otherwise this line's own (line_sync)
     template <int S>
-    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const Bases& wb, int salt = 0) {
-        pass<S, 1, 0>(v, sm, t, wb, salt);
+    __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const Bases& wb, int salt = 0,
+                                               int bar = 0) {
+        pass<S, 1, 0>(v, sm, t, wb, salt, bar);
     }
     template <int S>
     __device__ __forceinline__ static void run(cd* v, cd* sm, int t, const cd* __restrict__ tw,
-                                               int salt = 0) {
-        pass<S, 1, 0>(v, sm, t, bases(t, tw), salt);
+                                               int salt = 0, int bar = 0) {
+        pass<S, 1, 0>(v, sm, t, bases(t, tw), salt, bar);
     }
 };
 

@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     const int ld = a.ld_i;
     const int slot = F::SMEM + NY / 2 + 2 * ld;
     const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const int bar = G > 1 ? g + 1 : 0;  // the groups' own barriers (line_sync)
     const int xa = 2 * (blockIdx.x * G + g);
     const bool active = xa < a.nx;
     pdl_wait();
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     for (int k = 0; k < 4; ++k) {
         const int q = k & 1;
         cp_async_wait_all();
-        __syncthreads();
+        line_sync<T>(bar);
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -307,10 +308,10 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
             // packed spectrum of (a + i b) over the full ky range
             v[e] = mirror ? mk(ah.x + bh.y, bh.x - ah.y) : mk(ah.x - bh.y, ah.y + bh.x);
         }
-        __syncthreads();  // stage consumed
+        line_sync<T>(bar);  // stage consumed
         if (k < 3) issue(k + 1);
         cp_async_commit();
-        F::template run<+1>(v, sm, t, wb);
+        F::template run<+1>(v, sm, t, wb, 0, bar);
         if constexpr (cfl) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
@@ -335,12 +336,12 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = mk(prow[t + T * e], acc[e]);
-    F::template run<-1>(v, sm, t, wb);
+    F::template run<-1>(v, sm, t, wb, 0, bar);
     // exchange + prow form one contiguous N-complex buffer now
     using FF = BFFT<NY, false, EM>;
 #pragma unroll
     for (int e = 0; e < E; ++e) sm[FF::pad(t + T * e)] = v[e];
-    __syncthreads();
+    line_sync<T>(bar);
     if (active) {
         const double h = 0.5 * a.inv_n;
         cd* rp = a.nl + (size_t)(xa >> 1) * a.ld_o * 2;  // row pair block
@@ -473,6 +474,7 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     const int ld = a.ld_i;
     const int slot = F::SMEM + 2 * ld;
     const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const int bar = G > 1 ? g + 1 : 0;  // the groups' own barriers (line_sync)
     pdl_wait();
     if (a.flags->diverged) return;
     if (a.ystage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     for (int it = 0; it < iters; ++it, x += stride) {
         const bool active = x < a.nrl;
         cp_async_wait_all();
-        __syncthreads();
+        line_sync<T>(bar);
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -538,10 +540,10 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
             }
             v[e] = mirror ? mk(ah.x + bh.y, bh.x - ah.y) : mk(ah.x - bh.y, ah.y + bh.x);
         }
-        __syncthreads();  // stage consumed
+        line_sync<T>(bar);  // stage consumed
         issue(x + stride);
         cp_async_commit();
-        F::template run<+1>(v, sm, t, wb);  // u + i v on the row
+        F::template run<+1>(v, sm, t, wb, 0, bar);  // u + i v on the row
         if constexpr (cfl) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
@@ -554,10 +556,10 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
             const double u = v[e].x, w = v[e].y;
             v[e] = mk(w * w - u * u, u * w);  // (v^2 - u^2) + i (u v)
         }
-        F::template run<-1>(v, sm, t, wb);
+        F::template run<-1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
-        __syncthreads();
+        line_sync<T>(bar);
         if (active) {
             for (int k = t; k < a.ld_o; k += T) {
                 const cd zk = sm[F::pad(k)];

@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     pdl_wait();
     if (a.flags->diverged) return;
     cd* sm = smem + g * Z3<NZ>::SLOT;
+    const int bar = G > 1 ? g + 1 : 0;  // the groups' own barriers (line_sync)
     double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
     const typename F::Bases wb = F::bases(t, a.twz);
     const cd* B = a.B;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         // w + i wx
         fetch_pair<NZ>(a, FP[0], FQ[0], row, active, t, p, q);
         pack_pair<NZ>(t, p, q, v);
-        F::template run<+1>(v, sm, t, wb);
+        F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             st[0 * NZ + t + T * e] = v[e].x;
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         // wy + i wz
         fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
         pack_pair<NZ>(t, p, q, v);
-        F::template run<+1>(v, sm, t, wb);
+        F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             st[2 * NZ + t + T * e] = v[e].x;
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         // u + i v, then the cross product (solvers.cpp:321-325)
         fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
         pack_pair<NZ>(t, p, q, v);
-        F::template run<+1>(v, sm, t, wb);
+        F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int y = t + T * e;
@@ -481,10 +482,10 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             v[e] = mk(cx, cy);
             st[(rr == 0 ? 4 : 0) * NZ + y] = cz;  // row b reuses the dead w row
         }
-        F::template run<-1>(v, sm, t, wb);
+        F::template run<-1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
-        __syncthreads();
+        line_sync<T>(bar);
         if (active) {
             cd* o0 = a.A + (size_t)(r0 + rr) * a.kz_o;
             cd* o1 = o0 + fs;
@@ -495,16 +496,16 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
                 o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
             }
         }
-        __syncthreads();
+        line_sync<T>(bar);
     }
     if constexpr (cfl) umax_accumulate(a.dyn, 3, mx, my, mz);
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = mk(st[4 * NZ + t + T * e], st[0 * NZ + t + T * e]);
-    F::template run<-1>(v, sm, t, wb);
+    F::template run<-1>(v, sm, t, wb, 0, bar);
 #pragma unroll
     for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
-    __syncthreads();
+    line_sync<T>(bar);
     if (active) {
         cd* oa = a.A + 2 * fs + (size_t)r0 * a.kz_o;
         cd* ob = oa + a.kz_o;
