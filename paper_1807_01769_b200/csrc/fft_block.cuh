@@ -215,7 +215,9 @@ template <int T>
 __device__ __forceinline__ void line_sync(int bar) {
     if (bar == 0) {
         __syncthreads();
-    } else if constexpr (T >= 32) {
+    } else if constexpr (T == 32) {
+        __syncwarp();
+    } else if constexpr (T > 32) {
         asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(T) : "memory");
     } else {
         const unsigned lane = threadIdx.x & 31u;
