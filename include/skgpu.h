@@ -178,6 +178,12 @@ int skg_fft_inverse(skg_ctx* ctx, const double* uhat, double* u);
  * as plan_fft checks in fft.cpp:34-44): FftPlan::forward / inverse. */
 int skg_plan_forward(int rank, const int* shape, const double* u, double* uhat, int device);
 int skg_plan_inverse(int rank, const int* shape, const double* uhat, double* u, int device);
+/* The same transforms in FFTW's conventions, for a GPU-backed FFTW-API shim
+ * under the reference's unmodified FftPlan (fft.cpp:67-104):
+ * skg_dft_r2c = fftw_execute_dft_r2c (unnormalised, forward sign -1),
+ * skg_dft_c2r = fftw_execute_dft_c2r (unnormalised, input left intact). */
+int skg_dft_r2c(int rank, const int* shape, const double* in, double* out, int device);
+int skg_dft_c2r(int rank, const int* shape, const double* in, double* out, int device);
 
 /* Wavenumbers and dealias mask computed ON THE DEVICE from indices, copied
  * back for a bit-exact comparison with make_grid (grid.cpp:49-100).

@@ -33,12 +33,18 @@ def available() -> bool:
     return LIB_PATH.exists()
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not LIB_PATH.exists():
-            raise FileNotFoundError(f"{LIB_PATH} missing: run `make -C oracle`")
-        L = C.CDLL(str(LIB_PATH))
+_libs = {}
+
+
+def lib(path=None):
+    """The compiled reference (default oracle/_ref/libskref.so); `path` loads
+    another build of the same driver, e.g. the reference core linked against
+    the GPU-backed FFTW API (integration/_build/libskref_gpufft.so)."""
+    key = str(path or LIB_PATH)
+    if key not in _libs:
+        if not Path(key).exists():
+            raise FileNotFoundError(f"{key} missing: run `make -C oracle`")
+        L = C.CDLL(key)
         dp = C.POINTER(C.c_double)
         ip = C.POINTER(C.c_int)
         L.skref_last_error.restype = C.c_char_p
@@ -67,8 +73,8 @@ def lib():
         L.skref_last_divergence.argtypes = [C.c_void_p, C.POINTER(C.c_long), ip]
         L.skref_fft_forward.argtypes = [C.c_int, ip, dp, dp]
         L.skref_fft_inverse.argtypes = [C.c_int, ip, dp, dp]
-        _lib = L
-    return _lib
+        _libs[key] = L
+    return _libs[key]
 
 
 def _check(rc: int):
@@ -108,28 +114,29 @@ class RefSimulation:
     and forcing off, fixed dt and an injected spectral state."""
 
     def __init__(self, solver: str, n, nu: float, dt: float, scheme: str = "RK4",
-                 dealias_coef: float = 2.0 / 3.0, forcing=None):
+                 dealias_coef: float = 2.0 / 3.0, forcing=None, library=None):
         """forcing: None, or (k_lo, k_hi, rate, seed) for forcing.enable = true."""
         self.solver = solver
         self.n = tuple(int(x) for x in n)
+        self._L = lib(library)
         h = C.c_void_p()
         cn = (C.c_int * len(self.n))(*self.n)
         rk2 = 1 if scheme.upper() == "RK2" else 0
         if forcing is None:
-            _check(lib().skref_create(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
+            _check(self._L.skref_create(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
                                       float(dt), rk2, float(dealias_coef)))
         else:
             klo, khi, rate, seed = forcing
-            _check(lib().skref_create_forced(C.byref(h), solver.encode(), len(self.n), cn,
+            _check(self._L.skref_create_forced(C.byref(h), solver.encode(), len(self.n), cn,
                                              float(nu), float(dt), rk2, float(dealias_coef),
                                              float(klo), float(khi), float(rate), int(seed)))
         self._h = h
-        self.nvars = lib().skref_nvars(h)
+        self.nvars = self._L.skref_nvars(h)
         self.spect_shape = self.n[:-1] + (self.n[-1] // 2 + 1,)
 
     def close(self):
         if self._h:
-            lib().skref_destroy(self._h)
+            self._L.skref_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -140,30 +147,30 @@ class RefSimulation:
 
     def set_state(self, s: np.ndarray) -> None:
         s = np.ascontiguousarray(s, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)
-        _check(lib().skref_set_state(self._h, _dp(s.view(np.float64))))
+        _check(self._L.skref_set_state(self._h, _dp(s.view(np.float64))))
 
     def get_state(self) -> np.ndarray:
         out = np.empty((self.nvars,) + self.spect_shape, np.complex128)
-        _check(lib().skref_get_state(self._h, _dp(out.view(np.float64))))
+        _check(self._L.skref_get_state(self._h, _dp(out.view(np.float64))))
         return out
 
     def step(self, nsteps: int = 1) -> float:
         """step_once x nsteps (simulation.cpp:535-555); returns wall seconds."""
         sec = C.c_double(0.0)
-        _check(lib().skref_step(self._h, int(nsteps), C.byref(sec)))
+        _check(self._L.skref_step(self._h, int(nsteps), C.byref(sec)))
         return sec.value
 
     def run(self, nsteps: int) -> float:
         """Simulation::run with n_iters = nsteps (simulation.cpp:565-590)."""
         sec = C.c_double(0.0)
-        _check(lib().skref_run(self._h, int(nsteps), C.byref(sec)))
+        _check(self._L.skref_run(self._h, int(nsteps), C.byref(sec)))
         return sec.value
 
     def tendency(self, s: np.ndarray) -> np.ndarray:
         """Solver::tendency via Simulation::compute_tendency (simulation.cpp:478-480)."""
         s = np.ascontiguousarray(s, dtype=np.complex128).reshape((self.nvars,) + self.spect_shape)
         out = np.empty_like(s)
-        _check(lib().skref_tendency(self._h, _dp(s.view(np.float64)), _dp(out.view(np.float64))))
+        _check(self._L.skref_tendency(self._h, _dp(s.view(np.float64)), _dp(out.view(np.float64))))
         return out
 
     def grid(self):
@@ -172,7 +179,7 @@ class RefSimulation:
         mask = np.empty(self.spect_shape, np.uint8)
         for ax in range(len(self.n)):
             k = np.empty(self.spect_shape[ax], np.float64)
-            _check(lib().skref_grid(self._h, ax, _dp(k),
+            _check(self._L.skref_grid(self._h, ax, _dp(k),
                                     mask.ctypes.data_as(C.POINTER(C.c_ubyte))))
             ks.append(k)
         return ks, mask
@@ -180,25 +187,25 @@ class RefSimulation:
     def last_divergence(self):
         it = C.c_long(-1)
         var = C.c_int(-1)
-        lib().skref_last_divergence(self._h, C.byref(it), C.byref(var))
+        self._L.skref_last_divergence(self._h, C.byref(it), C.byref(var))
         return it.value, var.value
 
     @property
     def energy(self) -> float:
-        return lib().skref_energy(self._h)
+        return self._L.skref_energy(self._h)
 
     @property
     def enstrophy(self) -> float:
-        return lib().skref_enstrophy(self._h)
+        return self._L.skref_enstrophy(self._h)
 
     @property
     def last_injection(self) -> float:
-        return lib().skref_last_injection(self._h)
+        return self._L.skref_last_injection(self._h)
 
     @property
     def t(self) -> float:
-        return lib().skref_time(self._h)
+        return self._L.skref_time(self._h)
 
     @property
     def iteration(self) -> int:
-        return lib().skref_iteration(self._h)
+        return self._L.skref_iteration(self._h)

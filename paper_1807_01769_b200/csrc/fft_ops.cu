@@ -433,7 +433,7 @@ cudaError_t c2r(const cd* in, double* u, long long rows, int n, const cd* tw, cu
 bool fft_pow2(int n) { return n >= 4 && n <= 8192 && (n & (n - 1)) == 0; }
 
 cudaError_t fft_forward_dev(int rank, const int* n, const double* d_u, cd* d_uhat, cd*,
-                            const cd* const* tw, cudaStream_t s, long* launches) {
+                            const cd* const* tw, cudaStream_t s, long* launches, bool normalize) {
     long long rows = 1, P = 1;
     for (int d = 0; d < rank - 1; ++d) rows *= n[d];
     for (int d = 0; d < rank; ++d) P *= n[d];
@@ -449,6 +449,7 @@ cudaError_t fft_forward_dev(int rank, const int* n, const double* d_u, cd* d_uha
         if ((err = c2c(d_uhat, outer, n[a], inner, -1, tw[a], s)) != cudaSuccess) return err;
         ++*launches;
     }
+    if (!normalize) return cudaSuccess;  // FFTW convention (fftw_execute_dft_r2c)
     scale_kernel<<<592, 256, 0, s>>>(d_uhat, rows * h, 1.0 / (double)P);
     ++*launches;
     return cudaGetLastError();

@@ -337,7 +337,7 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
 // Plain transforms on the context grid / arbitrary shapes (fft_ops.cu).
 // u: row-major real (n0..n_{d-1}); uhat: row-major half spectrum.
 cudaError_t fft_forward_dev(int rank, const int* n, const double* d_u, cd* d_uhat, cd* d_work,
-                            const cd* const* tw, cudaStream_t s, long* launches);
+                            const cd* const* tw, cudaStream_t s, long* launches, bool normalize = true);
 cudaError_t fft_inverse_dev(int rank, const int* n, const cd* d_uhat, double* d_u, cd* d_work,
                             const cd* const* tw, cudaStream_t s, long* launches);
 bool fft_pow2(int n);

@@ -1608,48 +1608,67 @@ static int plan_common(int rank, const int* shape, long long* P, long long* S) {
     return SKG_OK;
 }
 
-int skg_plan_forward(int rank, const int* shape, const double* u, double* uhat, int device) {
+// Device buffers of the shape-level transforms, reused across calls (the
+// reference calls FftPlan::forward/inverse many times per step).
+struct PlanBufs {
+    double* u = nullptr;
+    cd* h = nullptr;
+    cd* w = nullptr;
+    long long P = 0, S = 0;
+};
+std::mutex g_plan_mu;
+std::map<int, PlanBufs> g_plan_bufs;
+
+static int plan_run(int rank, const int* shape, const double* in, double* out, int device, bool forward,
+                    bool normalize) {
     long long P, S;
     int rc = plan_common(rank, shape, &P, &S);
     if (rc) return rc;
     CUDA_TRY(cudaSetDevice(device));
-    double* du;
-    cd* dh;
-    CUDA_TRY(cudaMalloc(&du, sizeof(double) * P));
-    CUDA_TRY(cudaMalloc(&dh, sizeof(cd) * S));
-    CUDA_TRY(cudaMemcpy(du, u, sizeof(double) * P, cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    PlanBufs& b = g_plan_bufs[device];
+    if (b.P < P || b.S < S) {
+        cudaFree(b.u);
+        cudaFree(b.h);
+        cudaFree(b.w);
+        b = PlanBufs{};
+        CUDA_TRY(cudaMalloc(&b.u, sizeof(double) * P));
+        CUDA_TRY(cudaMalloc(&b.h, sizeof(cd) * S));
+        CUDA_TRY(cudaMalloc(&b.w, sizeof(cd) * S));
+        b.P = P;
+        b.S = S;
+    }
     const cd* tw[3] = {nullptr, nullptr, nullptr};
     for (int d = 0; d < rank; ++d) tw[d] = twiddle_table(device, shape[d]);
     long l = 0;
-    cudaError_t e = skg::fft_forward_dev(rank, shape, du, dh, nullptr, tw, 0, &l);
-    if (e == cudaSuccess) e = cudaMemcpy(uhat, dh, sizeof(cd) * S, cudaMemcpyDeviceToHost);
-    cudaFree(du);
-    cudaFree(dh);
+    cudaError_t e;
+    if (forward) {
+        e = cudaMemcpy(b.u, in, sizeof(double) * P, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = skg::fft_forward_dev(rank, shape, b.u, b.h, nullptr, tw, 0, &l, normalize);
+        if (e == cudaSuccess) e = cudaMemcpy(out, b.h, sizeof(cd) * S, cudaMemcpyDeviceToHost);
+    } else {
+        e = cudaMemcpy(b.h, in, sizeof(cd) * S, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = skg::fft_inverse_dev(rank, shape, b.h, b.u, b.w, tw, 0, &l);
+        if (e == cudaSuccess) e = cudaMemcpy(out, b.u, sizeof(double) * P, cudaMemcpyDeviceToHost);
+    }
     if (e != cudaSuccess) return fail(SKG_ECUDA, cudaGetErrorString(e));
     return SKG_OK;
 }
 
+int skg_plan_forward(int rank, const int* shape, const double* u, double* uhat, int device) {
+    return plan_run(rank, shape, u, uhat, device, true, true);
+}
+
 int skg_plan_inverse(int rank, const int* shape, const double* uhat, double* u, int device) {
-    long long P, S;
-    int rc = plan_common(rank, shape, &P, &S);
-    if (rc) return rc;
-    CUDA_TRY(cudaSetDevice(device));
-    double* du;
-    cd *dh, *dw;
-    CUDA_TRY(cudaMalloc(&du, sizeof(double) * P));
-    CUDA_TRY(cudaMalloc(&dh, sizeof(cd) * S));
-    CUDA_TRY(cudaMalloc(&dw, sizeof(cd) * S));
-    CUDA_TRY(cudaMemcpy(dh, uhat, sizeof(cd) * S, cudaMemcpyHostToDevice));
-    const cd* tw[3] = {nullptr, nullptr, nullptr};
-    for (int d = 0; d < rank; ++d) tw[d] = twiddle_table(device, shape[d]);
-    long l = 0;
-    cudaError_t e = skg::fft_inverse_dev(rank, shape, dh, du, dw, tw, 0, &l);
-    if (e == cudaSuccess) e = cudaMemcpy(u, du, sizeof(double) * P, cudaMemcpyDeviceToHost);
-    cudaFree(du);
-    cudaFree(dh);
-    cudaFree(dw);
-    if (e != cudaSuccess) return fail(SKG_ECUDA, cudaGetErrorString(e));
-    return SKG_OK;
+    return plan_run(rank, shape, uhat, u, device, false, false);
+}
+
+int skg_dft_r2c(int rank, const int* shape, const double* in, double* out, int device) {
+    return plan_run(rank, shape, in, out, device, true, false);
+}
+
+int skg_dft_c2r(int rank, const int* shape, const double* in, double* out, int device) {
+    return plan_run(rank, shape, in, out, device, false, false);
 }
 
 int skg_get_grid(skg_ctx* c, int axis, double* k_axis, unsigned char* mask) {

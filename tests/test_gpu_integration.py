@@ -61,3 +61,27 @@ def test_reference_simulation_cfl_on_gpu(solver, n):
     gpu = _run(L, solver + "_gpu", n, 1e-3, 0.0, u0, 4)
     for v in range(u0.shape[0]):
         assert O.rel_l2(gpu[v], cpu[v]) < 1e-10
+
+
+GPUFFT = Path(__file__).resolve().parents[1] / "integration" / "_build" / "libskref_gpufft.so"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("solver,n,steps", [("ns2d", (64, 64), 4), ("ns2d", (24, 40), 3),
+                                            ("ns3d", (16, 16, 16), 2), ("ns3d", (12, 8, 16), 2)])
+def test_reference_core_on_gpu_fftw(ref_lib, solver, n, steps):
+    """B1: the reference's own Simulation with every FftPlan transform on the
+    GPU (integration/fftw_gpu.cpp in place of FFTW) vs the CPU reference."""
+    if not GPUFFT.exists():
+        pytest.skip("GPU FFTW shim not built (needs /root/reference at build time)")
+    u0 = np.ascontiguousarray(ic.initial_state(solver, n, 4))
+    dt = ic.cfl_dt(solver, n, u0)
+    cpu = ref_lib.RefSimulation(solver, n, 1e-3, dt)
+    gpu = ref_lib.RefSimulation(solver, n, 1e-3, dt, library=GPUFFT)
+    for r in (cpu, gpu):
+        r.set_state(u0)
+        r.step(steps)
+    a, b = gpu.get_state(), cpu.get_state()
+    for v in range(u0.shape[0]):
+        assert O.rel_l2(a[v], b[v]) < 1e-12
+    assert abs(gpu.energy - cpu.energy) <= 1e-12 * cpu.energy
