@@ -133,6 +133,10 @@ int skg_get_state_device(skg_ctx* ctx, double* d_spect_out);
  * forcing are not graph-replayed (host noise every step).
  * skg_last_injection = Simulation::last_injection of the last step.
  */
+/* Solver::sanitize_state on the current state: ns2d dealias + mean 0
+ * (solvers.cpp:263-267); ns3d Leray projection + dealias (solvers.cpp:377-381). */
+int skg_sanitize_state(skg_ctx* ctx);
+
 int skg_set_forcing(skg_ctx* ctx, int enable, double k_lo, double k_hi, double rate, long seed);
 double skg_last_injection(const skg_ctx* ctx);
 

@@ -36,7 +36,7 @@ EXPORTS = [
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
-    "skg_set_forcing", "skg_last_injection",
+    "skg_set_forcing", "skg_last_injection", "skg_sanitize_state",
 ]
 
 
@@ -124,6 +124,7 @@ def load_library():
     L.skg_set_forcing.argtypes = [vp, C.c_int, C.c_double, C.c_double, C.c_double, C.c_long]
     L.skg_last_injection.argtypes = [vp]
     L.skg_last_injection.restype = C.c_double
+    L.skg_sanitize_state.argtypes = [vp]
     _lib = L
     return L
 
@@ -359,6 +360,11 @@ class Simulation:
         own generator seeded with `seed`."""
         self._call("skg_set_forcing", C.c_int(1 if enable else 0), C.c_double(k_lo),
                    C.c_double(k_hi), C.c_double(rate), C.c_long(int(seed)))
+
+    def sanitize_state(self) -> None:
+        """Solver::sanitize_state on the device (dealias, ns2d mean 0, ns3d
+        Leray projection), as the reference applies to initial fields."""
+        self._call("skg_sanitize_state")
 
     @property
     def last_injection(self) -> float:

@@ -74,7 +74,7 @@ __global__ void f_band(ForceGeo g, cd* f) {
 
 // prepare_forcing: ns2d dealias + mean 0 (solvers.cpp:269-272); ns3d Leray
 // projection (grid.cpp:227-249), then dealias + mean 0 (solvers.cpp:383-389)
-__global__ void f_prepare(ForceGeo g, cd* f) {
+__global__ void f_prepare(ForceGeo g, cd* f, int zero_mean) {
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < g.S;
          q += (long long)gridDim.x * blockDim.x) {
         const FMode m = fmode(g, q);
@@ -86,7 +86,7 @@ __global__ void f_prepare(ForceGeo g, cd* f) {
             for (int v = 0; v < 3; ++v) c[v] = sub(c[v], scale(sp, m.k[v]));
         }
         for (int v = 0; v < g.nvars; ++v)
-            f[(size_t)v * g.S + q] = (!m.kept || m.mean) ? zero() : c[v];
+            f[(size_t)v * g.S + q] = (!m.kept || (zero_mean && m.mean)) ? zero() : c[v];
     }
 }
 
@@ -174,8 +174,16 @@ __global__ void f_make(ForceGeo g, const cd* u, cd* f, const double* coef) {
 
 cudaError_t forcing_shape(const ForceGeo& g, cd* f, cudaStream_t s, long* launches) {
     f_band<<<FB, FT, 0, s>>>(g, f);
-    f_prepare<<<FB, FT, 0, s>>>(g, f);
+    f_prepare<<<FB, FT, 0, s>>>(g, f, 1);
     *launches += 2;
+    return cudaGetLastError();
+}
+
+// Solver::sanitize_state: ns2d dealias + mean 0 (solvers.cpp:263-267); ns3d
+// Leray projection + dealias (solvers.cpp:377-381), the mean kept.
+cudaError_t sanitize_dev(const ForceGeo& g, cd* f, cudaStream_t s, long* launches) {
+    f_prepare<<<FB, FT, 0, s>>>(g, f, g.nvars == 1 ? 1 : 0);
+    ++*launches;
     return cudaGetLastError();
 }
 

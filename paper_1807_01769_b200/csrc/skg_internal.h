@@ -304,6 +304,8 @@ struct ForceGeo {
 };
 // band filter + unit magnitude + prepare_forcing of the transformed noise f
 cudaError_t forcing_shape(const ForceGeo& g, cd* f, cudaStream_t s, long* launches);
+// Solver::sanitize_state of a reference-layout state
+cudaError_t sanitize_dev(const ForceGeo& g, cd* f, cudaStream_t s, long* launches);
 // reductions against the state u, the rate split, f <- alpha f + beta ub;
 // red: 8 doubles (red[6] = last injection, red[7] = 1 on the fallback)
 cudaError_t forcing_finish(const ForceGeo& g, const cd* u, cd* f, double rate, double* red,

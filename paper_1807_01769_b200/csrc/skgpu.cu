@@ -1752,6 +1752,21 @@ int skg_set_forcing(skg_ctx* c, int enable, double k_lo, double k_hi, double rat
 
 double skg_last_injection(const skg_ctx* c) { return c->last_injection; }
 
+int skg_sanitize_state(skg_ctx* c) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    int rc = store_state_to_io(c, c->u);
+    if (rc) return rc;
+    CUDA_TRY(skg::sanitize_dev(force_geo(c), c->io, c->stream, &c->launches));
+    rc = load_state_from_io(c);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
 int skg_set_time(skg_ctx* c, double t) {
     c->t = t;
     return SKG_OK;

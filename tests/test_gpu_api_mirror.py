@@ -89,3 +89,29 @@ def test_t_end_with_fixed_dt(solver, n):
     h.step(1, dt=5.5 * dt - h.t)
     assert per_field(g.get_state(), h.get_state()) == 0.0
     assert g.run()["iterations"] == 0  # already at t_end
+
+
+@pytest.mark.parametrize("solver,n", [("ns2d", (32, 32)), ("ns2d", (24, 40)), ("ns3d", (16, 16, 16)),
+                                      ("ns3d", (12, 12, 12))])
+def test_sanitize_state(solver, n):
+    """Solver::sanitize_state (solvers.cpp:263-267, 377-381) on the device."""
+    nv = 1 if solver == "ns2d" else 3
+    rng = np.random.default_rng(6)
+    v = np.stack([O.forward(rng.standard_normal(n)) for _ in range(nv)])
+    g = api.Simulation(solver, n, 1e-3, 1e-3)
+    g.set_state(v)
+    assert not g.pruned
+    g.sanitize_state()
+    mask = O.dealias_mask(n)
+    if solver == "ns2d":
+        ref = v * mask[None]
+        ref[0, 0, 0] = 0.0
+    else:
+        kx, ky, kz = O.k_axes(n)
+        K = [kx[:, None, None], ky[None, :, None], kz[None, None, :]]
+        ksq = O.k_sq(n)
+        s = (K[0] * v[0] + K[1] * v[1] + K[2] * v[2]) / np.where(ksq == 0, 1.0, ksq)
+        ref = np.stack([np.where(ksq == 0, v[c], v[c] - K[c] * s) for c in range(3)]) * mask[None]
+    out = g.get_state()
+    assert np.abs(out - ref).max() <= 1e-15 * np.abs(ref).max()
+    assert g.pruned or n[0] % 2  # masked modes are now exactly zero
