@@ -213,6 +213,7 @@ __device__ __forceinline__ void apply_twiddles(cd* u, cd w) {
 // -- so independent lines of one CTA do not wait for each other.
 template <int T>
 __device__ __forceinline__ void line_sync(int bar) {
+#if defined(__CUDA_ARCH__)
     if (bar == 0) {
         __syncthreads();
     } else if constexpr (T == 32) {
@@ -223,6 +224,10 @@ __device__ __forceinline__ void line_sync(int bar) {
         const unsigned lane = threadIdx.x & 31u;
         __syncwarp(((1u << T) - 1u) << (lane & ~(unsigned)(T - 1)));
     }
+#else
+    (void)bar;  // host emulation (tests/host_emu): one barrier domain
+    __syncthreads();
+#endif
 }
 
 // Block FFT of a power-of-two length N in natural layout.  SPLIT exchanges
