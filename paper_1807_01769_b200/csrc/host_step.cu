@@ -1,0 +1,398 @@
+// host_step.cu -- step enqueueing of libskgpu (see host_ctx.h): the per-step
+// launch sequences (fused 2D/3D paths, generic path, CUDA-graph replay),
+// the adaptive-dt and forcing hooks, the slab all-to-all exchanges and the
+// post-step divergence / time bookkeeping.
+#include "host_ctx.h"
+
+namespace skh {
+
+// Simulation::refresh_forcing (simulation.cpp:482-533) before a step: the
+// reference's generator fills the white noise on the host (one
+// normal_distribution per variable, random_field grid.cpp:285-288), the rest
+// runs on the device (forcing.cu).
+int refresh_forcing(skg_ctx* c) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // the pinned noise buffer is reused
+    const size_t P = (size_t)c->P;
+    const cd* tw[3] = {c->tw[0], c->tw[1], c->tw[2]};
+    for (int v = 0; v < c->nvars; ++v) {
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        double* h = c->f_noise + v * P;
+        for (size_t i = 0; i < P; ++i) h[i] = gauss(c->f_rng);
+    }
+    const skg::ForceGeo g = force_geo(c);
+    for (int v = 0; v < c->nvars; ++v) {
+        CUDA_TRY(cudaMemcpyAsync(c->phys, c->f_noise + v * P, sizeof(double) * P, cudaMemcpyHostToDevice,
+                                 c->stream));
+        CUDA_TRY(skg::fft_forward_dev(c->dims, c->n, c->phys, c->f_ref + (size_t)v * c->S, c->work, tw,
+                                      c->stream, &c->launches));
+    }
+    CUDA_TRY(skg::forcing_shape(g, c->f_ref, c->stream, &c->launches));
+    const cd* uref = c->u;
+    if (c->f_cm) {  // ns2d fused kernels keep the state in CM layout
+        int rc = store_state_to_io(c, c->u);
+        if (rc) return rc;
+        uref = c->io;
+    }
+    CUDA_TRY(skg::forcing_finish(g, uref, c->f_ref, c->f_rate, c->f_red, c->stream, &c->launches));
+    if (c->f_cm)
+        CUDA_TRY(skg::launch_transpose_c(c->f_ref, c->f_cm, c->n[0], c->nh, 0, c->stream, &c->launches));
+    return SKG_OK;
+}
+
+int sync_and_check(skg_ctx* c, long nsteps, double dt) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    harvest(c);
+    skg::DevFlags f;
+    CUDA_TRY(cudaMemcpy(&f, c->flags, sizeof(f), cudaMemcpyDeviceToHost));
+    if (c->forcing) {
+        double r[8];
+        CUDA_TRY(cudaMemcpy(r, c->f_red, sizeof(r), cudaMemcpyDeviceToHost));
+        c->last_injection = r[6];
+    }
+    skg::DynStep dyn{};
+    if (c->adaptive) {
+        CUDA_TRY(cudaMemcpy(&dyn, c->d_dyn, sizeof(dyn), cudaMemcpyDeviceToHost));
+        c->last_dt = dyn.last_dt;
+    }
+    if (f.bad_dt) {  // compute_dt gave dt <= 0 (past t_end): the step did not run
+        c->it += f.div_step - 1;
+        c->t = dyn.t;
+        return fail(SKG_ECONFIG, "step: nonpositive dt (past t_end?)");
+    }
+    if (f.diverged) {
+        const long done = f.div_step;
+        if (c->adaptive) c->t = dyn.t;
+        else
+            for (long i = 0; i < done; ++i) c->t += dt;
+        c->it += done;
+        c->div_it = c->it;
+        c->div_var = f.div_var;
+        static const char* keys2[] = {"rot_fft"};
+        static const char* keys3[] = {"vx_fft", "vy_fft", "vz_fft"};
+        const char* key = c->solver == 2 ? keys2[0] : keys3[f.div_var >= 0 && f.div_var < 3 ? f.div_var : 0];
+        return fail(SKG_EDIVERGENCE, std::string("non-finite value in field '") + key +
+                                         "' at iteration " + std::to_string(c->it));
+    }
+    if (c->adaptive) {
+        c->t = dyn.t;
+    } else {
+        for (long i = 0; i < nsteps; ++i) c->t += dt;
+        if (nsteps > 0) c->last_dt = dt;
+    }
+    c->it += nsteps;
+    return SKG_OK;
+}
+
+// All-to-all of the slab decomposition.  which = 0: x-inverse outputs
+// (rows(q) x cols(r) from r to q), 1: product spectra (cols(q) x rows(r)).
+// Single-process mode: device-to-device copies; otherwise NCCL send/recv
+// on the context stream (grouped, one block per peer).
+int exchange3(skg_ctx* c, int which);
+
+int exchange(skg_ctx* c, int which) {
+    if (c->solver == 3) return exchange3(c, which);
+    const int G = c->G;
+    const size_t nrl = (size_t)c->nrl;
+    auto ncol = [&](int q) { return c->cstart[q + 1] - c->cstart[q]; };
+    auto npair = [&](int q) { return (size_t)(ncol(q) + 1) / 2; };
+    // block (source r -> destination q): pointers and element count
+    auto block = [&](const Part& src, const Part& dst, int f, cd** from, cd** to, size_t* cnt) {
+        const int r = src.r, q = dst.r;
+        if (which == 0) {
+            *cnt = nrl * ncol(r);
+            *from = src.sI[f] + (size_t)q * nrl * ncol(r);
+            *to = dst.rI[f] + nrl * c->cstart[r];
+        } else {
+            *cnt = 2 * npair(q) * nrl;
+            *from = src.sA[f] + (size_t)(c->cstart[q] / 2) * 2 * nrl;
+            *to = dst.rA[f] + (size_t)r * 2 * npair(q) * nrl;
+        }
+    };
+    const skg::LaunchHook hook = hook_of(c);
+    hook.begin(4);
+    double bytes = 0.0;
+    if (c->comm == nullptr) {  // all partitions local
+        for (const Part& src : c->parts)
+            for (const Part& dst : c->parts)
+                for (int f = 0; f < 2; ++f) {
+                    cd *from, *to;
+                    size_t cnt;
+                    block(src, dst, f, &from, &to, &cnt);
+                    if (cnt == 0) continue;
+                    CUDA_TRY(cudaMemcpyAsync(to, from, cnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    if (src.r != dst.r) bytes += cnt * sizeof(cd);
+                }
+    } else {
+        const Part& me = c->parts[0];
+        const int r = me.r;
+        ncclResult_t nr = nccl().GroupStart();
+        for (int q = 0; q < G && nr == ncclSuccess; ++q) {
+            for (int f = 0; f < 2 && nr == ncclSuccess; ++f) {
+                cd *sptr, *rptr;
+                size_t scnt, rcnt;
+                if (which == 0) {
+                    sptr = me.sI[f] + (size_t)q * nrl * ncol(r);
+                    scnt = nrl * ncol(r);
+                    rptr = me.rI[f] + nrl * c->cstart[q];
+                    rcnt = nrl * ncol(q);
+                } else {
+                    sptr = me.sA[f] + (size_t)(c->cstart[q] / 2) * 2 * nrl;
+                    scnt = 2 * npair(q) * nrl;
+                    rptr = me.rA[f] + (size_t)q * 2 * npair(r) * nrl;
+                    rcnt = 2 * npair(r) * nrl;
+                }
+                if (q == r) {
+                    if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    continue;
+                }
+                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
+                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                bytes += scnt * sizeof(cd);
+            }
+        }
+        ncclResult_t ne = nccl().GroupEnd();
+        if (nr != ncclSuccess || ne != ncclSuccess)
+            return fail(SKG_ENCCL, std::string("all-to-all: ") + nccl().GetErrorString(nr != ncclSuccess ? nr : ne));
+    }
+    hook.end(4, bytes);
+    ++c->launches;
+    return SKG_OK;
+}
+
+// ns3d all-to-alls.  which = 0: x-inverse outputs, 5 fields, block r -> q =
+// rows(q) x lines(r) ([xl][kyl_r][kz_in]); 1: y-forward outputs, 3 fields,
+// block r -> q = rows(r) x lines(q) ([xl][kyl_q][kz_o]).
+int exchange3(skg_ctx* c, int which) {
+    const int G = c->G;
+    if (G == 1) return SKG_OK;  // one partition: receive buffers alias the send buffers
+    const size_t nrl = (size_t)c->nrl;
+    const size_t kz = (size_t)c->kc[2] + 1;  // kz_in = kz_o (pruned)
+    auto nl = [&](int q) { return (size_t)(c->cstart[q + 1] - c->cstart[q]); };
+    const int nf = which == 0 ? 5 : 3;
+    // block from rank r (buffers src) to rank q (buffers dst), field f
+    auto src_ptr = [&](const Part& src, int q, int f) {
+        return which == 0 ? src.A3 + f * src.fs + (size_t)q * nrl * nl(src.r) * kz
+                          : src.sD3 + f * src.rfs + nrl * c->cstart[q] * kz;
+    };
+    auto dst_ptr = [&](const Part& dst, int r, int f) {
+        return which == 0 ? dst.rA3 + f * dst.rfs + nrl * c->cstart[r] * kz
+                          : dst.B3 + f * dst.fs + (size_t)r * nrl * nl(dst.r) * kz;
+    };
+    auto count = [&](int r, int q) { return nrl * kz * (which == 0 ? nl(r) : nl(q)); };
+    const skg::LaunchHook hook = hook_of(c);
+    hook.begin(4);
+    double bytes = 0.0;
+    if (c->comm == nullptr) {
+        for (const Part& src : c->parts)
+            for (const Part& dst : c->parts)
+                for (int f = 0; f < nf; ++f) {
+                    const size_t cnt = count(src.r, dst.r);
+                    if (!cnt) continue;
+                    CUDA_TRY(cudaMemcpyAsync(dst_ptr(dst, src.r, f), src_ptr(src, dst.r, f),
+                                             cnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    if (src.r != dst.r) bytes += cnt * sizeof(cd);
+                }
+    } else {
+        const Part& me = c->parts[0];
+        const int r = me.r;
+        ncclResult_t nr = nccl().GroupStart();
+        for (int q = 0; q < G && nr == ncclSuccess; ++q) {
+            for (int f = 0; f < nf && nr == ncclSuccess; ++f) {
+                const size_t scnt = count(r, q), rcnt = count(q, r);
+                cd* sptr = src_ptr(me, q, f);
+                cd* rptr = dst_ptr(me, q, f);
+                if (q == r) {
+                    if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    continue;
+                }
+                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
+                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                bytes += scnt * sizeof(cd);
+            }
+        }
+        ncclResult_t ne = nccl().GroupEnd();
+        if (nr != ncclSuccess || ne != ncclSuccess)
+            return fail(SKG_ENCCL, std::string("all-to-all: ") + nccl().GetErrorString(nr != ncclSuccess ? nr : ne));
+    }
+    hook.end(4, bytes);
+    ++c->launches;
+    return SKG_OK;
+}
+
+int dist_dt_update(skg_ctx* c, long* counter) {
+    if (c->comm) {  // global max |u_d| over the ranks' x rows
+        const ncclResult_t nr = nccl().AllReduce(c->d_dyn->umax, c->d_dyn->umax, 3, ncclDouble, ncclMax,
+                                              c->comm, c->stream);
+        if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
+    }
+    CUDA_TRY(skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale, c->nu,
+                                   c->stream, counter));
+    return SKG_OK;
+}
+
+// One step of a slab-decomposed context.  ns2d: the x-forward of every stage
+// runs fused with the next stage's x-inverse (first: the step opens the
+// batch and runs its own stage-1 x-inverse; last: no next stage).
+int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool last) {
+    const int nst = c->scheme == SKG_RK2 ? 2 : 4;
+    const skg::LaunchHook hook = hook_of(c);
+    int rc;
+    if (c->solver == 3) {
+        for (int st = 1; st <= nst; ++st) {
+            for (int pass = 0; pass < 3; ++pass) {
+                for (const Part& p : c->parts) {
+                    skg::Ns3dArgs a = args3d_part(c, dt, p);
+                    CUDA_TRY(skg::ns3d_pass(a, pass, st, c->stream, counter, hook));
+                }
+                if (pass < 2 && (rc = exchange(c, pass))) return rc;
+            }
+            if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;
+        }
+        return SKG_OK;
+    }
+    auto run_pass = [&](int pass, int st, int next) -> int {
+        for (const Part& p : c->parts) {
+            skg::Ns2dArgs a = args2d_part(c, dt, p);
+            a.lead = p.r == 0 ? 1 : 0;
+            CUDA_TRY(skg::ns2d_fast_pass(a, pass, st, c->stream, counter, hook, next));
+        }
+        return SKG_OK;
+    };
+    if (first) {
+        if ((rc = run_pass(0, 1, 0)) || (rc = exchange(c, 0))) return rc;
+    }
+    for (int st = 1; st <= nst; ++st) {
+        if ((rc = run_pass(1, st, 0)) || (rc = exchange(c, 1))) return rc;
+        if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;
+        const int next = st < nst || !last;
+        if ((rc = run_pass(3, st, next))) return rc;
+        if (next && (rc = exchange(c, 0))) return rc;
+    }
+    return SKG_OK;
+}
+
+int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
+    if (c->adaptive) dt = -1.0;  // device-resident: compute_dt per step
+    else if (!(dt > 0.0)) return fail(SKG_ECONFIG, "step: nonpositive dt");
+    if (nsteps < 0) return fail(SKG_ECONFIG, "step: negative step count");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->adaptive) {
+        skg::DynStep d{};
+        d.t = c->t;
+        d.t_end = c->t_end;
+        d.cfl = c->cfl;
+        d.dt_max = c->dt_max;
+        for (int k = 0; k < c->dims; ++k) d.dx[k] = c->L[k] / c->n[k];  // grid.cpp:50
+        d.last_dt = c->last_dt;
+        CUDA_TRY(cudaMemcpyAsync(c->d_dyn, &d, sizeof(d), cudaMemcpyHostToDevice, c->stream));
+        c->cached_dt = -1.0;  // the device owns the factor tables now
+    } else {
+        int rc = refresh_exp(c, dt);
+        if (rc) return rc;
+    }
+    skg::DevFlags init{0, std::numeric_limits<int>::max(), 0, 0};
+    CUDA_TRY(cudaMemcpyAsync(c->flags, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    const int nst = c->scheme == SKG_RK2 ? 2 : 4;
+    const skg::LaunchHook hook = hook_of(c);
+    if (c->dist) {
+        for (long s = 0; s < nsteps; ++s) {
+            int rc2 = enqueue_dist_step(c, dt, &c->launches, s == 0, s == nsteps - 1);
+            if (rc2) return rc2;
+        }
+        return SKG_OK;
+    }
+    // first: the step opens the batch; last: it closes it.  On the ns2d fast
+    // path the x-forward of each stage is fused with the next stage's
+    // x-inverse (across the step boundary too), so only the batch's first
+    // step runs a standalone x-inverse and the last one no trailing one.
+    auto one_step = [&](long* counter, bool first, bool last) -> cudaError_t {
+        cudaError_t e = cudaSuccess;
+        bool fused = false;
+        auto dt_update = [&]() {
+            return skg::launch_dt_update(c->d_dyn, c->flags, c->etab, c->dims, c->n, c->kscale, c->nu,
+                                         c->stream, counter);
+        };
+        if (c->generic) {
+            skg::GenArgs a = args_gen(c, dt);
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                e = skg::generic_stage(a, st, c->gs, c->stream, counter);
+                if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+            }
+        } else if (c->solver == 2) {
+            skg::Ns2dArgs a = args2d(c, dt);
+            fused = skg::ns2d_fast_ok(a);
+            if (!fused) a.diag = nullptr;
+            if (fused) {
+                if (first) e = skg::ns2d_fast_pass(a, 0, 1, c->stream, counter, hook);
+                for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                    e = skg::ns2d_fast_pass(a, 1, st, c->stream, counter, hook);
+                    if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+                    if (e == cudaSuccess)
+                        e = skg::ns2d_fast_pass(a, 3, st, c->stream, counter, hook, st < nst || !last);
+                }
+            } else {
+                for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                    e = skg::ns2d_launch_stage(a, st, c->stream, counter, hook);
+                    if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+                }
+            }
+        } else {
+            skg::Ns3dArgs a = args3d(c, dt);
+            fused = c->pruned;
+            if (!fused) a.diag = nullptr;
+            for (int st = 1; st <= nst && e == cudaSuccess; ++st) {
+                e = skg::ns3d_launch_stage(a, st, c->stream, counter, hook);
+                if (st == 1 && c->adaptive && e == cudaSuccess) e = dt_update();
+            }
+        }
+        if (e == cudaSuccess && c->diag && !fused)  // unfused paths: one reduction per step
+            e = skg::launch_energy(c->u, c->dims, c->n, c->kscale, c->nvars, energy_mode(c),
+                                   c->diag, c->stream, counter, c->nu, &c->flags->steps, false);
+        return e;
+    };
+    long s = 0;
+    if (c->forcing) {  // host noise every step: no graph replay
+        for (; s < nsteps; ++s) {
+            int rc2 = refresh_forcing(c);
+            if (rc2) return rc2;
+            CUDA_TRY(one_step(&c->launches, s == 0, s == nsteps - 1));
+        }
+        return SKG_OK;
+    }
+    if (nsteps > 0) {  // first step eagerly (also sets kernel attributes)
+        CUDA_TRY(one_step(&c->launches, true, nsteps == 1));
+        s = 1;
+    }
+    // middle steps: replay of a captured step; the last step eagerly
+    if (nsteps - s >= 3 && !c->timing && c->stream != nullptr) {
+        if (c->gexec && (c->g_dt != dt || c->g_pruned != c->pruned || c->g_stream != c->stream ||
+                         c->g_diag != c->diag)) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        if (!c->gexec) {
+            cudaGraph_t graph;
+            long dummy = 0;
+            CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = one_step(&dummy, false, false);
+            cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
+            CUDA_TRY(e);
+            CUDA_TRY(e2);
+            CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
+            cudaGraphDestroy(graph);
+            c->g_launches = dummy;
+            c->g_dt = dt;
+            c->g_diag = c->diag;
+            c->g_pruned = c->pruned;
+            c->g_stream = c->stream;
+        }
+        for (; s < nsteps - 1; ++s) {
+            CUDA_TRY(cudaGraphLaunch(c->gexec, c->stream));
+            c->launches += c->g_launches;
+        }
+    }
+    for (; s < nsteps; ++s) CUDA_TRY(one_step(&c->launches, false, s == nsteps - 1));
+    return SKG_OK;
+}
+
+}  // namespace skh
