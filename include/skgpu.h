@@ -135,6 +135,11 @@ int skg_get_state_device(skg_ctx* ctx, double* d_spect_out);
  */
 /* Solver::sanitize_state on the current state: ns2d dealias + mean 0
  * (solvers.cpp:263-267); ns3d Leray projection + dealias (solvers.cpp:377-381). */
+/* Shell spectra of the current state as OutputManager records them
+ * (output.cpp:231-257, bin_shells output.cpp:21-39): k = s delta_k, energy
+ * density E(k), nonlinear transfer T(k) (from the tendency) and dissipation
+ * D(k), s = 0..n_shells-1.  With k == NULL only *n_shells is returned. */
+int skg_spectra(skg_ctx* ctx, int cap, double* k, double* E, double* T, double* D, int* n_shells);
 int skg_sanitize_state(skg_ctx* ctx);
 
 int skg_set_forcing(skg_ctx* ctx, int enable, double k_lo, double k_hi, double rate, long seed);

@@ -36,7 +36,7 @@ EXPORTS = [
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
-    "skg_set_forcing", "skg_last_injection", "skg_sanitize_state",
+    "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
 ]
 
 
@@ -125,6 +125,8 @@ def load_library():
     L.skg_last_injection.argtypes = [vp]
     L.skg_last_injection.restype = C.c_double
     L.skg_sanitize_state.argtypes = [vp]
+    L.skg_spectra.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.POINTER(C.c_int)]
     _lib = L
     return L
 
@@ -360,6 +362,60 @@ class Simulation:
         own generator seeded with `seed`."""
         self._call("skg_set_forcing", C.c_int(1 if enable else 0), C.c_double(k_lo),
                    C.c_double(k_hi), C.c_double(rate), C.c_long(int(seed)))
+
+    def spectra(self) -> dict:
+        """Shell spectra as the reference's OutputManager records them
+        (output.cpp:231-257): {"k", "E" (density), "T" (transfer), "D"}."""
+        ns = C.c_int()
+        self._call("skg_spectra", C.c_int(0), None, None, None, None, C.byref(ns))
+        arr = {key: np.zeros(ns.value, np.float64) for key in ("k", "E", "T", "D")}
+        self._call("skg_spectra", C.c_int(ns.value), _ptr(arr["k"]), _ptr(arr["E"]), _ptr(arr["T"]),
+                   _ptr(arr["D"]), C.byref(ns))
+        return arr
+
+    # ------------------------------------------------------- snapshot files
+    def save_fld(self, path, digest: str = "") -> None:
+        """The reference's physical snapshot format (snapshot.cpp:65-100:
+        "spectralkit-fld 1" header, time, shape, vars, digest, blank line,
+        little-endian doubles per variable).  `digest` is the reference's
+        params_digest when the file must pass its restart check."""
+        keys = self.state_keys
+        with open(path, "wb") as f:
+            f.write(b"spectralkit-fld 1\n")
+            f.write(f"time={self.t:.17g}\n".encode())
+            f.write(("shape=" + "x".join(str(x) for x in self.n) + "\n").encode())
+            f.write(("vars=" + ",".join(keys) + "\n").encode())
+            f.write(f"digest={digest}\n\n".encode())
+            for key in keys:
+                f.write(np.ascontiguousarray(self.get_phys(key), dtype="<f8").tobytes())
+
+    def load_fld(self, path, set_time: bool = True) -> dict:
+        """Load a "spectralkit-fld 1" snapshot (snapshot.cpp:117-160) into the
+        state (StateSet::load_phys per variable); returns its header."""
+        with open(path, "rb") as f:
+            if f.readline().rstrip(b"\n") != b"spectralkit-fld 1":
+                raise ConfigError(f"'{path}': not a spectralkit-fld file")
+            hdr = {}
+            for key in ("time", "shape", "vars", "digest"):
+                line = f.readline().decode().rstrip("\n")
+                if not line.startswith(key + "="):
+                    raise ConfigError(f"'{path}': expected header field '{key}', got '{line}'")
+                hdr[key] = line[len(key) + 1:]
+            if f.readline().strip():
+                raise ConfigError(f"'{path}': header must end with a blank line")
+            shape = tuple(int(x) for x in hdr["shape"].split("x"))
+            if shape != self.n:
+                raise ShapeError(f"snapshot shape {shape} does not match the grid {self.n}")
+            size = int(np.prod(shape))
+            for key in hdr["vars"].split(","):
+                data = np.frombuffer(f.read(8 * size), dtype="<f8")
+                if data.size != size:
+                    raise ConfigError(f"'{path}': truncated payload for variable '{key}'")
+                self.set_phys(key, data.reshape(shape))
+        hdr["time"] = float(hdr["time"])
+        if set_time:
+            self.set_time(hdr["time"])
+        return hdr
 
     def sanitize_state(self) -> None:
         """Solver::sanitize_state on the device (dealias, ns2d mean 0, ns3d

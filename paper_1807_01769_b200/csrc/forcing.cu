@@ -170,7 +170,43 @@ __global__ void f_make(ForceGeo g, const cd* u, cd* f, const double* coef) {
     }
 }
 
+// Shell spectra of OutputManager::save_records_and_snapshot (output.cpp:231-257,
+// bin_shells output.cpp:21-39): per-mode energy (solver metric), transfer
+// w Re(conj(s) N) (ns2d / |k|^2, solvers.cpp:232-240; default simulation.cpp:176-185)
+// and dissipation -2 nu |k|^2 e, binned by shell = round(|k| / delta_k).
+__global__ void f_spectra(ForceGeo g, const cd* u, const cd* nl, double nu, int nsh, double* E,
+                          double* Tr, double* D) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < g.S;
+         q += (long long)gridDim.x * blockDim.x) {
+        const FMode m = fmode(g, q);
+        const long long sh = llround(sqrt(m.ksq) / g.delta_k);
+        if (sh < 0 || sh >= nsh) continue;
+        double s = m.w;
+        if (g.nvars == 1) {
+            if (!(m.ksq > 0.0)) continue;
+            s = m.w / m.ksq;
+        }
+        double e = 0.0, t = 0.0;
+        for (int v = 0; v < g.nvars; ++v) {
+            const cd a = u[(size_t)v * g.S + q], b = nl[(size_t)v * g.S + q];
+            e += 0.5 * s * (a.x * a.x + a.y * a.y);
+            t += s * (a.x * b.x + a.y * b.y);
+        }
+        atomicAdd(E + sh, e);
+        atomicAdd(Tr + sh, t);
+        atomicAdd(D + sh, -2.0 * nu * m.ksq * e);
+    }
+}
+
 }  // namespace
+
+cudaError_t spectra_dev(const ForceGeo& g, const cd* u, const cd* nl, double nu, int nsh, double* out3,
+                        cudaStream_t s, long* launches) {
+    SKG_TRY(cudaMemsetAsync(out3, 0, sizeof(double) * 3 * nsh, s));
+    f_spectra<<<FB, FT, 0, s>>>(g, u, nl, nu, nsh, out3, out3 + nsh, out3 + 2 * nsh);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t forcing_shape(const ForceGeo& g, cd* f, cudaStream_t s, long* launches) {
     f_band<<<FB, FT, 0, s>>>(g, f);

@@ -304,6 +304,9 @@ struct ForceGeo {
 };
 // band filter + unit magnitude + prepare_forcing of the transformed noise f
 cudaError_t forcing_shape(const ForceGeo& g, cd* f, cudaStream_t s, long* launches);
+// per-shell energy, transfer and dissipation into out3 = [E | T | D] (nsh each)
+cudaError_t spectra_dev(const ForceGeo& g, const cd* u, const cd* nl, double nu, int nsh, double* out3,
+                        cudaStream_t s, long* launches);
 // Solver::sanitize_state of a reference-layout state
 cudaError_t sanitize_dev(const ForceGeo& g, cd* f, cudaStream_t s, long* launches);
 // reductions against the state u, the rate split, f <- alpha f + beta ub;

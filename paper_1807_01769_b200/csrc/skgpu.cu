@@ -422,15 +422,9 @@ int skg_max_velocity(skg_ctx* c, const double* in, double* umax) {
 // Solver::tendency of `in` (host, reference layout) into `out` (or not, when
 // null); with umax, also max |u_d| of `in` (Solver::max_velocity_per_axis)
 // from the same physical pass.
-static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax) {
-    if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_tendency on a slab-decomposed context");
-    CUDA_TRY(cudaSetDevice(c->device));
-    if (c->pending_steps) {
-        int rc = skg_sync(c);
-        if (rc) return rc;
-    }
-    CUDA_TRY(cudaMemcpyAsync(c->io, in, sizeof(cd) * c->S * c->nvars, cudaMemcpyHostToDevice,
-                             c->stream));
+// Solver::tendency of the reference-layout state in c->io, left in c->io
+// (with umax: max |u_d| of it as well, from the same physical pass).
+static int tendency_dev(skg_ctx* c, double* umax) {
     const bool keep_pruned = c->pruned;
     int rc = decide_pruned(c, c->io);
     if (rc) return rc;
@@ -475,18 +469,83 @@ static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax
         rc = store_state_to_io(c, c->k[0]);
         if (rc) return rc;
     }
-    if (out)
-        CUDA_TRY(cudaMemcpyAsync(out, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToHost,
-                                 c->stream));
     if (umax) {
         skg::DynStep d;
         CUDA_TRY(cudaMemcpyAsync(&d, c->d_dyn, sizeof(d), cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         for (int k = 0; k < c->dims; ++k) umax[k] = d.umax[k];
     }
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->pruned = keep_pruned;
     return SKG_OK;
+}
+
+static int tendency_impl(skg_ctx* c, const double* in, double* out, double* umax) {
+    if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_tendency on a slab-decomposed context");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->io, in, sizeof(cd) * c->S * c->nvars, cudaMemcpyHostToDevice,
+                             c->stream));
+    if (int rc = tendency_dev(c, umax)) return rc;
+    if (out)
+        CUDA_TRY(cudaMemcpyAsync(out, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return SKG_OK;
+}
+
+int skg_spectra(skg_ctx* c, int cap, double* k, double* E, double* T, double* D, int* n_shells) {
+    // n_shells = round(k_norm_max / delta_k) + 1 (grid.cpp:95, 108)
+    double kmax2 = 0.0, Lmax = 0.0;
+    for (int d = 0; d < c->dims; ++d) {
+        const double km = c->kscale[d] * (c->n[d] / 2);
+        kmax2 += km * km;
+        Lmax = std::max(Lmax, c->L[d]);
+    }
+    const double dk = skh::kTwoPi / Lmax;
+    const int nsh = (int)std::llround(std::sqrt(kmax2) / dk) + 1;
+    if (n_shells) *n_shells = nsh;
+    if (!k || !E || !T || !D) return SKG_OK;  // size query
+    if (cap < nsh) return fail(SKG_ESHAPE, "skg_spectra: arrays shorter than n_shells");
+    if (c->dist) return fail(SKG_EUNSUPPORTED, "skg_spectra on a slab-decomposed context");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
+    // state (reference layout) kept in work buffers while io receives the tendency
+    if (int rc = ensure_fft_bufs(c)) return rc;
+    cd* st = nullptr;
+    double* d3 = nullptr;
+    CUDA_TRY(cudaMalloc(&st, sizeof(cd) * c->S * c->nvars));
+    CUDA_TRY(cudaMalloc(&d3, sizeof(double) * 3 * nsh));
+    int rc = store_state_to_io(c, c->u);
+    if (!rc) {
+        cudaMemcpyAsync(st, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToDevice, c->stream);
+        rc = tendency_dev(c, nullptr);
+    }
+    if (!rc) {
+        cudaError_t e = skg::spectra_dev(force_geo(c), st, c->io, c->nu, nsh, d3, c->stream, &c->launches);
+        std::vector<double> h(3 * (size_t)nsh);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d3, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                                                  c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) {
+            rc = fail(SKG_ECUDA, cudaGetErrorString(e));
+        } else {
+            for (int s = 0; s < nsh; ++s) {
+                k[s] = s * dk;
+                E[s] = h[s] / dk;  // bin_shells(..., density = true)
+                T[s] = h[nsh + s];
+                D[s] = h[2 * nsh + s];
+            }
+        }
+    }
+    cudaFree(st);
+    cudaFree(d3);
+    return rc;
 }
 
 int skg_fft_forward(skg_ctx* c, const double* u, double* uhat) {

@@ -115,3 +115,51 @@ def test_sanitize_state(solver, n):
     out = g.get_state()
     assert np.abs(out - ref).max() <= 1e-15 * np.abs(ref).max()
     assert g.pruned or n[0] % 2  # masked modes are now exactly zero
+
+
+@pytest.mark.parametrize("solver,n", [("ns2d", (64, 64)), ("ns2d", (24, 40)), ("ns3d", (16, 16, 16))])
+def test_spectra_match_reference_definitions(ref_lib, solver, n):
+    """OutputManager's shell spectra (output.cpp:231-257) from the GPU state and
+    tendency vs the same binning of the reference's tendency (numpy)."""
+    u0 = ic.initial_state(solver, n, seed=5)
+    nu = 1e-3
+    g = api.Simulation(solver, n, nu, 1e-3)
+    g.set_state(u0)
+    sp = g.spectra()
+    nl = ref_lib.RefSimulation(solver, n, nu, 1e-3).tendency(u0)
+    ksq = O.k_sq(n)
+    w = O.parseval_w(n)
+    dk = 1.0
+    shell = np.rint(np.sqrt(ksq) / dk).astype(int)
+    nsh = int(np.rint(np.sqrt(ksq).max() / dk)) + 1
+    if solver == "ns2d":
+        s = np.where(ksq > 0, w / np.where(ksq > 0, ksq, 1.0), 0.0)
+        e = 0.5 * s * np.abs(u0[0]) ** 2
+        t = s * (u0[0].real * nl[0].real + u0[0].imag * nl[0].imag)
+    else:
+        e = 0.5 * w * sum(np.abs(u0[c]) ** 2 for c in range(3))
+        t = w * sum(u0[c].real * nl[c].real + u0[c].imag * nl[c].imag for c in range(3))
+    E = np.bincount(shell.ravel(), e.ravel(), nsh) / dk
+    T = np.bincount(shell.ravel(), t.ravel(), nsh)
+    D = np.bincount(shell.ravel(), (-2 * nu * ksq * e).ravel(), nsh)
+    assert len(sp["k"]) == nsh and np.allclose(sp["k"], np.arange(nsh) * dk)
+    assert np.abs(sp["E"] - E).max() <= 1e-12 * np.abs(E).max()
+    assert np.abs(sp["T"] - T).max() <= 1e-10 * np.abs(T).max()
+    assert np.abs(sp["D"] - D).max() <= 1e-12 * np.abs(D).max()
+
+
+def test_fld_roundtrip(tmp_path):
+    n = (32, 16)
+    u0 = ic.ns2d_ic(n, seed=4)
+    g = api.Simulation("ns2d", n, 1e-3, 1e-3)
+    g.set_state(u0)
+    g.step(3)
+    p = tmp_path / "state_phys.fld"
+    g.save_fld(p, digest="abc")
+    head = p.read_bytes().split(b"\n")[:6]
+    assert head[0] == b"spectralkit-fld 1" and head[2] == b"shape=32x16" and head[3] == b"vars=rot"
+    assert head[4] == b"digest=abc" and head[5] == b""
+    h = api.Simulation("ns2d", n, 1e-3, 1e-3)
+    hdr = h.load_fld(p)
+    assert hdr["time"] == g.t and h.t == g.t
+    assert np.abs(h.get_state() - g.get_state()).max() < 1e-14
