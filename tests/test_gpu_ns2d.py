@@ -238,3 +238,39 @@ def test_largest_fused_extent_8192(ref_lib):
     assert O.rel_l2(g.get_state()[0], r.get_state()[0]) < 1e-10
     u = np.random.default_rng(1).standard_normal((8192,))
     assert np.abs(api.fft_forward(u) - np.fft.rfft(u) / u.size).max() < 1e-14
+
+
+@pytest.mark.parametrize("scheme,lo,hi,k0", [("RK4", 3.7, 4.3, 20), ("RK2", 1.8, 2.2, 80)])
+def test_temporal_order(scheme, lo, hi, k0):
+    """Measured global order of the GPU stepper on the nonlinear ns2d problem
+    (the property test_time_stepping.cpp:108-139 checks on scalar ODEs),
+    against a 16x finer run of the same code."""
+    n = (64, 64)
+    u0 = ic.ns2d_ic(n, seed=13) * 2.0
+    nu, T = 1e-3, 0.2
+
+    def run(nsteps):
+        g = api.Simulation("ns2d", n, nu, T / nsteps, scheme=scheme)
+        g.set_state(u0)
+        g.step(nsteps)
+        return g.get_state()
+
+    ref = run(32 * k0)
+    e1, e2, e3 = (np.linalg.norm(run(k) - ref) for k in (k0, 2 * k0, 4 * k0))
+    o1, o2 = np.log2(e1 / e2), np.log2(e2 / e3)
+    assert lo < o1 < hi and lo < o2 < hi, (o1, o2)
+
+
+def test_exp_factors_follow_dt_changes():
+    """time_stepping.cpp:160-166: a pure-decay mode (zero nonlinearity) with a
+    dt change decays by exp(-nu k^2 (dt1 + dt2)) to round-off."""
+    n = (32, 32)
+    x = np.arange(32) * 2 * math.pi / 32
+    w = np.cos(3 * x)[:, None] * np.ones((1, 32))       # kx = 3: u . grad w = 0
+    s = O.forward(w)[None]
+    nu = 0.05
+    g = api.Simulation("ns2d", n, nu, 0.01)
+    g.set_state(s)
+    g.step(1, dt=0.01)
+    g.step(1, dt=0.03)
+    assert np.abs(g.get_state() - s * math.exp(-nu * 9 * 0.04)).max() < 1e-15
