@@ -572,6 +572,56 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     if constexpr (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
 }
 
+// One kept mode (kx index i, local column kyl) of the x-forward epilogue:
+// tendency kv (+ forcing) -> k_j, or the final RK update of u with the
+// non-finite flag and the per-step diagnostics; returns the next stage state
+// (fused kernels: stage_combine, or the new u = stage 1 of the next step).
+__device__ __forceinline__ cd xf_point(const Ns2dArgs& a, int stage, bool final, bool fuse, int ky,
+                                       double kyv, double kxv, double pw, int i, size_t idx, cd kv,
+                                       bool& bad, double& sE, double& sZ, double& sD) {
+    if (a.force) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
+    if (!final) {
+        cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
+        kout[idx] = kv;
+        return fuse ? stage_combine(a, stage + 1, ky, i, a.u[idx], kv) : zero();
+    }
+    const cd u = a.u[idx];
+    cd un;
+    if (a.has_sigma) {
+        const double e1 = a.e1x[i] * a.e1y[ky];
+        const double e2 = a.e2x[i] * a.e2y[ky];
+        if (a.rk2) {
+            un = add(scale(u, e2), scale(kv, dt_of(a) * e1));
+        } else {
+            const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+            const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
+            un = add(scale(u, e2), scale(sum, sdt_of(a)));
+        }
+    } else {
+        cd delta;
+        if (a.rk2) {
+            delta = scale(kv, dt_of(a));
+        } else {
+            const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
+            delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), sdt_of(a));
+        }
+        un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
+    }
+    a.u[idx] = un;
+    bad |= !finite2(un);
+    if (a.diag) {
+        const double ksq = kxv * kxv + kyv * kyv;
+        const double n2 = un.x * un.x + un.y * un.y;
+        sZ += 0.5 * pw * n2;
+        if (ksq > 0.0) {
+            const double en = 0.5 * pw * n2 * __drcp_rn(ksq);
+            sE += en;
+            if (a.has_sigma) sD += 2.0 * a.nu * ksq * en;
+        }
+    }
+    return un;  // stage 1 of the next step
+}
+
 // x-forward of the two product spectra per kept ky column, combination
 // kx ky A + (kx^2 - ky^2) B, dealias + mean 0 + RK epilogue (as k4_xfwd).
 // FUSE (next != 0): the same CTA then runs the NEXT stage's x-inverse of its
@@ -619,7 +669,6 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
     for (int e = 0; e < E; ++e)
         v[e] = active ? a.rA[1][ridx(t + T * e)] : zero();
     F::template run<-1>(v, sm, t, wb);
-    cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     bool bad = false;
     // per-step E, Z, eps of the new state (Simulation::energy / enstrophy /
     // dissipation_rate, simulation.cpp:592-615; ns2d mode_energy solvers.cpp:211-218)
@@ -643,49 +692,8 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
         }
         const double kxv = a.kx_scale * (double)si;
         const size_t idx = (size_t)kyl * NX + i;
-        cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
-        if (a.force) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
-        cd wn = zero();  // next stage state (fused)
-        if (!final) {
-            kout[idx] = kv;
-            if (fuse) wn = stage_combine(a, stage + 1, ky, i, a.u[idx], kv);
-        } else {
-            const cd u = a.u[idx];
-            cd un;
-            if (a.has_sigma) {
-                const double e1 = a.e1x[i] * a.e1y[ky];
-                const double e2 = a.e2x[i] * a.e2y[ky];
-                if (a.rk2) {
-                    un = add(scale(u, e2), scale(kv, dt_of(a) * e1));
-                } else {
-                    const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                    const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
-                    un = add(scale(u, e2), scale(sum, sdt_of(a)));
-                }
-            } else {
-                cd delta;
-                if (a.rk2) {
-                    delta = scale(kv, dt_of(a));
-                } else {
-                    const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-                    delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), sdt_of(a));
-                }
-                un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
-            }
-            a.u[idx] = un;
-            wn = un;  // stage 1 of the next step
-            bad |= !finite2(un);
-            if (a.diag) {
-                const double ksq = kxv * kxv + kyv * kyv;
-                const double n2 = un.x * un.x + un.y * un.y;
-                sZ += 0.5 * pw * n2;
-                if (ksq > 0.0) {
-                    const double en = 0.5 * pw * n2 * __drcp_rn(ksq);
-                    sE += en;
-                    if (a.has_sigma) sD += 2.0 * a.nu * ksq * en;
-                }
-            }
-        }
+        const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
+        const cd wn = xf_point(a, stage, final, fuse, ky, kyv, kxv, pw, i, idx, kv, bad, sE, sZ, sD);
         if (fuse) {  // psi = w / |k|^2 of the next stage (k1_xinv prologue)
             const double ksq = kxv * kxv + kyv * kyv;
             const double r = __drcp_rn(ksq);  // ksq > 0: the mean mode was skipped
@@ -843,6 +851,7 @@ template <int NX, int CTW>
 cudaError_t launch_fast_x_w(const Ns2dArgs& a, int stage, int mode, cudaStream_t s) {
     constexpr int EM = fast_em<NX>();
     if (mode == 0) return launch_k1<NX, true, 2, EM, CTW>(a, stage, s);
+
     if (mode == 2) return launch_k4b<NX, CTW, true>(a, stage, s);
     return launch_k4b<NX, CTW, false>(a, stage, s);
 }
