@@ -236,6 +236,8 @@ def run_our_arm(args):
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
+        if args.p2p and solver == "ns2d":
+            sim.enable_p2p()
     else:
         compact = args.layout == "compact" or (args.layout == "auto" and args.config in COARSE_IC)
         sim = api.Simulation(solver, n, nu, dt, device=local, compact=compact)
@@ -408,6 +410,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--instrumented-steps", type=int, default=20)
+    ap.add_argument("--p2p", action="store_true",
+                    help="ns2d slab under torchrun: peer-memory exchange (CUDA IPC) instead of NCCL copies")
     ap.add_argument("--layout", choices=["auto", "full", "compact"], default="auto",
                     help="ns3d one-GPU layout (auto: compact where the full layout does not fit)")
     args = ap.parse_args()

@@ -84,6 +84,19 @@ int skg_destroy(skg_ctx* ctx);
  * State I/O is the full reference layout on every rank; tendency/energy are
  * not offered; the state must be dealiased (SKG_EUNSUPPORTED otherwise).
  */
+/*
+ * Peer-memory exchange of the ns2d slab (fused compute + transfer): the
+ * x-inverse and y-pass epilogues store directly into the destination
+ * partition's receive buffers, so each all-to-all becomes a barrier.
+ *   single process (nccl_id == NULL): skg_dist_p2p(ctx, 1);
+ *   one process per GPU: every rank calls skg_dist_ipc_handle (256 bytes:
+ *   CUDA IPC handles of its receive buffers), the caller all-gathers them in
+ *   rank order and every rank calls skg_dist_open_peers(ctx, all) (world x
+ *   256 bytes); the NCCL communicator then carries only a 1-double barrier.
+ */
+int skg_dist_p2p(skg_ctx* ctx, int enable);
+int skg_dist_ipc_handle(skg_ctx* ctx, char* out256);
+int skg_dist_open_peers(skg_ctx* ctx, const char* all_handles);
 int skg_nccl_unique_id(char* out128);
 int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                     double dealias_coef, double nu, int scheme, int device, int rank, int world,

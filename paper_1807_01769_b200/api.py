@@ -37,6 +37,7 @@ EXPORTS = [
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
     "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
+    "skg_dist_p2p", "skg_dist_ipc_handle", "skg_dist_open_peers",
 ]
 
 
@@ -125,6 +126,9 @@ def load_library():
     L.skg_last_injection.argtypes = [vp]
     L.skg_last_injection.restype = C.c_double
     L.skg_sanitize_state.argtypes = [vp]
+    L.skg_dist_p2p.argtypes = [vp, C.c_int]
+    L.skg_dist_ipc_handle.argtypes = [vp, C.c_char_p]
+    L.skg_dist_open_peers.argtypes = [vp, C.c_char_p]
     L.skg_spectra.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                               C.POINTER(C.c_int)]
     _lib = L
@@ -239,6 +243,7 @@ class Simulation:
                                self.nu, sch, int(device))
         self.world = int(world)
         self.rank = int(rank)
+        self._nccl = nccl_id
         if rc:
             _raise(rc)
         self._h = h
@@ -416,6 +421,27 @@ class Simulation:
         if set_time:
             self.set_time(hdr["time"])
         return hdr
+
+    def enable_p2p(self, all_gather=None) -> None:
+        """Peer-memory exchange for the ns2d slab: producers store straight
+        into the owners' receive buffers.  Single process: no argument.  One
+        process per GPU: `all_gather(bytes) -> list[bytes]` in rank order
+        (default: torch.distributed.all_gather_object)."""
+        if self.world <= 1:
+            raise UnsupportedError("peer exchange needs a slab-decomposed context")
+        if getattr(self, "_nccl", None) is None:
+            self._call("skg_dist_p2p", C.c_int(1))
+            return
+        mine = C.create_string_buffer(256)
+        self._call("skg_dist_ipc_handle", mine)
+        if all_gather is None:
+            import torch.distributed as dist
+            out = [None] * self.world
+            dist.all_gather_object(out, mine.raw)
+        else:
+            out = all_gather(mine.raw)
+        blob = b"".join(out)
+        self._call("skg_dist_open_peers", C.create_string_buffer(blob, len(blob)))
 
     def sanitize_state(self) -> None:
         """Solver::sanitize_state on the device (dealias, ns2d mean 0, ns3d

@@ -253,6 +253,13 @@ skg::Ns2dArgs args2d_part(skg_ctx* c, double dt, const Part& p) {
         a.sA[f] = p.sA[f];
         a.rA[f] = p.rA[f];
     }
+    a.p2p = c->p2p ? 1 : 0;
+    if (c->p2p)
+        for (int q = 0; q < c->G; ++q)
+            for (int f = 0; f < 2; ++f) {
+                a.peer_rI[q][f] = c->peer_rI[q][f];
+                a.peer_rA[q][f] = c->peer_rA[q][f];
+            }
     return a;
 }
 

@@ -137,6 +137,13 @@ struct skg_ctx {
     cd* cmfull = nullptr;     // full CM staging for set/get_state
     ncclComm_t comm = nullptr;
     double* diag = nullptr;   // per-step (E, Z, eps) series of skg_run (device)
+    // peer-memory exchange (ns2d slab): receive buffers of every partition
+    // (local parts, or CUDA-IPC-mapped peers); p2p replaces the copies
+    bool p2p = false;
+    cd* peer_rI[SKG_MAX_RANKS][2] = {};
+    cd* peer_rA[SKG_MAX_RANKS][2] = {};
+    std::vector<void*> ipc_opened;  // cudaIpcOpenMemHandle mappings to close
+    double* d_barrier = nullptr;    // one double all-reduced as the cross-rank barrier
 
     // per-kernel-class event timing (skg_set_timing)
     struct Pending {

@@ -91,6 +91,14 @@ int exchange3(skg_ctx* c, int which);
 
 int exchange(skg_ctx* c, int which) {
     if (c->solver == 3) return exchange3(c, which);
+    if (c->p2p) {  // the producers already stored into the receive buffers
+        if (c->comm) {  // cross-rank barrier: every rank's producer kernel has completed
+            const ncclResult_t nr = nccl().AllReduce(c->d_barrier, c->d_barrier, 1, ncclDouble, ncclSum,
+                                                     c->comm, c->stream);
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
+        }
+        return SKG_OK;
+    }
     const int G = c->G;
     const size_t nrl = (size_t)c->nrl;
     auto ncol = [&](int q) { return c->cstart[q + 1] - c->cstart[q]; };

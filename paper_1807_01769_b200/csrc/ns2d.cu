@@ -59,6 +59,29 @@ __device__ __forceinline__ size_t sidx_send(const Ns2dArgs& a, int x, int kyl) {
     return (size_t)q * a.nrl * a.ncols + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG);
 }
 
+// Where the x-inverse output m of (x, local column kyl) goes: this
+// partition's send block for the row's owner, or (p2p) directly the owner's
+// receive block (offset nrl * c0, same layout).
+__device__ __forceinline__ cd* xinv_dst(const Ns2dArgs& a, int m, int x, int kyl) {
+    if (!a.p2p) return a.sI[m] + sidx_send(a, x, kyl);
+    const int q = x >> a.lg_nrl, xl = x & (a.nrl - 1);
+    return a.peer_rI[q][m] + (size_t)a.nrl * a.c0 + ((size_t)(xl / RG) * a.ncols + kyl) * RG + (xl % RG);
+}
+
+// Where the y-pass output f of (local row x, kept column k) goes: the send
+// buffer in pair order, or (p2p) the column owner's receive block from this
+// partition (offset r * 2 npairs(q) nrl, layout ((k-c_q)/2 nrl + x) 2 + k%2).
+__device__ __forceinline__ cd* ypass_dst(const Ns2dArgs& a, int f, int x, int k) {
+    if (!a.p2p) return a.sA[f] + cpidx(x, k, a.nrl);
+    const int PP = (a.ky_in + 1) >> 1;
+    const int q = (((k >> 1) + 1) * a.G - 1) / PP;
+    const int cs = 2 * (q * PP / a.G);
+    const int nc = (q == a.G - 1 ? a.ky_in : 2 * ((q + 1) * PP / a.G)) - cs;
+    const size_t npq = (size_t)(nc + 1) >> 1;
+    return a.peer_rA[q][f] + (size_t)a.r * 2 * npq * a.nrl + ((size_t)((k - cs) >> 1) * a.nrl + x) * 2 +
+           (k & 1);
+}
+
 __device__ __forceinline__ cd* pick(const Ns2dArgs& a, int m) {
     return m == 0 ? a.I[0] : m == 1 ? a.I[1] : m == 2 ? a.I[2] : a.I[3];
 }
@@ -220,12 +243,8 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
         F::template run<+1>(v, sm, t, wb);
         if (active) {
             if constexpr (NM == 2) {
-                cd* out = m == 0 ? a.sI[0] : a.sI[1];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int x = t + T * e;
-                    out[sidx_send(a, x, kyl)] = v[e];
-                }
+                for (int e = 0; e < E; ++e) *xinv_dst(a, m, t + T * e, kyl) = v[e];
             } else {
                 cd* out = pick(a, m);
 #pragma unroll
@@ -233,6 +252,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
             }
         }
     }
+    if (NM == 2 && a.p2p) __threadfence_system();  // peer stores visible before the barrier
 }
 
 // y pass on a row pair (xa, xa+1).  Four inverse FFTs k = 0..3 over
@@ -484,8 +504,7 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     const int stride = gridDim.x * G;
     const cd* P = a.rI[0];  // X[psi]
     const cd* Q = a.rI[1];  // X[kx psi]
-    cd* outA = a.sA[0];     // FT_y(v^2 - u^2) / N
-    cd* outB = a.sA[1];     // FT_y(u v) / N
+    // outputs (ypass_dst): FT_y(v^2 - u^2) / N and FT_y(u v) / N
     // x runs over this partition's local rows; input column ky comes from
     // the receive block of its owner r' (layout of r')
     auto issue = [&](int x) {
@@ -564,12 +583,13 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
             for (int k = t; k < a.ld_o; k += T) {
                 const cd zk = sm[F::pad(k)];
                 const cd zm = sm[F::pad((NY - k) & (NY - 1))];
-                outA[cpidx(x, k, a.nrl)] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-                outB[cpidx(x, k, a.nrl)] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+                *ypass_dst(a, 0, x, k) = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                *ypass_dst(a, 1, x, k) = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
             }
         }
     }
     if constexpr (cfl) umax_accumulate(a.dyn, 2, mx, my, 0.0);
+    if (a.p2p) __threadfence_system();
 }
 
 // One kept mode (kx index i, local column kyl) of the x-forward epilogue:
@@ -723,14 +743,11 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
             }
             F::template run<+1>(v, sm, t, wb);
             if (active) {
-                cd* out = a.sI[m];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int x = t + T * e;
-                    out[sidx_send(a, x, kyl)] = v[e];
-                }
+                for (int e = 0; e < E; ++e) *xinv_dst(a, m, t + T * e, kyl) = v[e];
             }
         }
+        if (a.p2p) __threadfence_system();
     }
 }
 

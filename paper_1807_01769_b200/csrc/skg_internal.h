@@ -7,6 +7,8 @@
 
 #include "fft_block.cuh"
 
+#define SKG_MAX_RANKS 16  // slab partitions addressable by the peer-memory path
+
 namespace skg {
 
 // Device flags shared by every kernel of a context (one allocation).
@@ -125,6 +127,14 @@ struct Ns2dArgs {
     cd* rI[2];
     cd* sA[2];
     cd* rA[2];
+    // Peer-memory exchange (p2p = 1): the x-inverse and y-pass epilogues store
+    // straight into the destination partition's receive buffers -- the same
+    // GPU in the single-process mode, CUDA-IPC-mapped peer memory over NVLink
+    // across processes -- so the all-to-all copies disappear (the transfer
+    // overlaps the FFTs tile by tile) and only a barrier remains.
+    int p2p;
+    cd* peer_rI[SKG_MAX_RANKS][2];
+    cd* peer_rA[SKG_MAX_RANKS][2];
 };
 
 // Optional per-launch instrumentation: hook(user, cls, 0, 0) before a launch

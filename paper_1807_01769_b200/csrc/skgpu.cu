@@ -273,6 +273,8 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->d_count);
     cudaFree(c->d_red);
     cudaFree(c->d_dyn);
+    for (void* d : c->ipc_opened) cudaIpcCloseMemHandle(d);
+    cudaFree(c->d_barrier);
     cudaFree(c->f_ref);
     cudaFree(c->f_cm);
     cudaFree(c->f_red);
@@ -745,6 +747,73 @@ int skg_sanitize_state(skg_ctx* c) {
 
 int skg_set_time(skg_ctx* c, double t) {
     c->t = t;
+    return SKG_OK;
+}
+
+// ---- peer-memory exchange for the ns2d slab (include/skgpu.h)
+static const int kIpcBytes = 4 * (int)sizeof(cudaIpcMemHandle_t);
+
+int skg_dist_ipc_handle(skg_ctx* c, char* out) {
+    if (!c->dist || c->solver != 2 || c->parts.size() != 1)
+        return fail(SKG_EUNSUPPORTED, "IPC handles: one ns2d slab partition per process");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const Part& p = c->parts[0];
+    cd* bufs[4] = {p.rI[0], p.rI[1], p.rA[0], p.rA[1]};
+    for (int b = 0; b < 4; ++b) {
+        cudaIpcMemHandle_t h;
+        CUDA_TRY(cudaIpcGetMemHandle(&h, bufs[b]));
+        std::memcpy(out + b * sizeof(h), &h, sizeof(h));
+    }
+    return SKG_OK;
+}
+
+int skg_dist_open_peers(skg_ctx* c, const char* all) {
+    if (!c->dist || c->solver != 2 || c->parts.size() != 1 || !c->comm)
+        return fail(SKG_EUNSUPPORTED, "peer exchange across processes: NCCL ns2d slab contexts");
+    if (c->G > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const Part& me = c->parts[0];
+    for (int q = 0; q < c->G; ++q) {
+        cd* ptr[4];
+        if (q == me.r) {
+            ptr[0] = me.rI[0];
+            ptr[1] = me.rI[1];
+            ptr[2] = me.rA[0];
+            ptr[3] = me.rA[1];
+        } else {
+            for (int b = 0; b < 4; ++b) {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, all + (size_t)q * kIpcBytes + b * sizeof(h), sizeof(h));
+                void* d = nullptr;
+                CUDA_TRY(cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess));
+                c->ipc_opened.push_back(d);
+                ptr[b] = static_cast<cd*>(d);
+            }
+        }
+        c->peer_rI[q][0] = ptr[0];
+        c->peer_rI[q][1] = ptr[1];
+        c->peer_rA[q][0] = ptr[2];
+        c->peer_rA[q][1] = ptr[3];
+    }
+    if (!c->d_barrier) CUDA_TRY(cudaMalloc(&c->d_barrier, sizeof(double)));
+    c->p2p = true;
+    return SKG_OK;
+}
+
+int skg_dist_p2p(skg_ctx* c, int enable) {
+    if (!enable) {
+        c->p2p = false;
+        return SKG_OK;
+    }
+    if (!c->dist || c->solver != 2) return fail(SKG_EUNSUPPORTED, "peer exchange: ns2d slab contexts");
+    if (c->comm) return fail(SKG_ECONFIG, "multi-process contexts: skg_dist_open_peers");
+    if (c->G > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
+    for (const Part& p : c->parts)
+        for (int f = 0; f < 2; ++f) {
+            c->peer_rI[p.r][f] = p.rI[f];
+            c->peer_rA[p.r][f] = p.rA[f];
+        }
+    c->p2p = true;
     return SKG_OK;
 }
 
