@@ -423,8 +423,8 @@ class Simulation:
         return hdr
 
     def enable_p2p(self, all_gather=None) -> None:
-        """Peer-memory exchange for the ns2d slab: producers store straight
-        into the owners' receive buffers.  Single process: no argument.  One
+        """Peer-memory exchange for the slab (ns2d and ns3d): producers store
+        straight into the owners' receive buffers.  Single process: no argument.  One
         process per GPU: `all_gather(bytes) -> list[bytes]` in rank order
         (default: torch.distributed.all_gather_object)."""
         if self.world <= 1:

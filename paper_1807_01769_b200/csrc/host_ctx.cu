@@ -345,6 +345,15 @@ skg::Ns3dArgs args3d_part(skg_ctx* c, double dt, const Part& p) {
     a.ystate = p.ncols;
     a.slab = 1;
     a.sz = c->kc[2] + 1;
+    a.p2p = c->p2p ? 1 : 0;
+    if (c->p2p) {
+        a.rD = p.rD3;
+        a.dfs = c->dfs3;
+        for (int q = 0; q < c->G; ++q) {
+            a.peer_rA[q] = c->peer_rA3[q];
+            a.peer_D[q] = c->peer_D3[q];
+        }
+    }
     return a;
 }
 
@@ -516,6 +525,17 @@ int ensure_fft_bufs(skg_ctx* c) {
     if (c->phys && c->work) return SKG_OK;
     CUDA_TRY(cudaMalloc(&c->phys, sizeof(double) * (size_t)c->P));
     CUDA_TRY(cudaMalloc(&c->work, sizeof(cd) * (size_t)c->S));
+    return SKG_OK;
+}
+
+// ns3d peer exchange: the y-forward receive buffers (B stays private)
+int ensure_p2p_bufs(skg_ctx* c) {
+    if (c->solver != 3) return SKG_OK;
+    size_t maxcols = 0;
+    for (int q = 0; q < c->G; ++q) maxcols = std::max(maxcols, (size_t)(c->cstart[q + 1] - c->cstart[q]));
+    c->dfs3 = (size_t)c->n[0] * maxcols * ((size_t)c->kc[2] + 1);
+    for (Part& p : c->parts)
+        if (!p.rD3) CUDA_TRY(cudaMalloc(&p.rD3, sizeof(cd) * 3 * c->dfs3));
     return SKG_OK;
 }
 

@@ -81,6 +81,7 @@ struct Part {
     cd* B3 = nullptr;
     cd* rA3 = nullptr;
     cd* sD3 = nullptr;
+    cd* rD3 = nullptr;  // p2p: y-forward receive buffer (3 fields, stride dfs3)
     size_t vs = 0, fs = 0, rfs = 0;
 };
 
@@ -142,6 +143,9 @@ struct skg_ctx {
     bool p2p = false;
     cd* peer_rI[SKG_MAX_RANKS][2] = {};
     cd* peer_rA[SKG_MAX_RANKS][2] = {};
+    cd* peer_rA3[SKG_MAX_RANKS] = {};  // ns3d: x-inverse receive buffers
+    cd* peer_D3[SKG_MAX_RANKS] = {};   // ns3d: y-forward receive buffers (rD3)
+    size_t dfs3 = 0;                   // ns3d: their field stride (uniform)
     std::vector<void*> ipc_opened;  // cudaIpcOpenMemHandle mappings to close
     double* d_barrier = nullptr;    // one double all-reduced as the cross-rank barrier
 
@@ -214,6 +218,7 @@ int copy_slab3(skg_ctx* c, const Part& p, bool to_part);
 int load_state_from_io(skg_ctx* c);
 int store_state_to_io(skg_ctx* c, const cd* src);
 int ensure_fft_bufs(skg_ctx* c);
+int ensure_p2p_bufs(skg_ctx* c);
 cd* twiddle_table(int device, int n);
 // stepping (host_step.cu)
 int refresh_forcing(skg_ctx* c);

@@ -173,6 +173,14 @@ int exchange(skg_ctx* c, int which) {
 int exchange3(skg_ctx* c, int which) {
     const int G = c->G;
     if (G == 1) return SKG_OK;  // one partition: receive buffers alias the send buffers
+    if (c->p2p) {  // producers stored into the receive buffers: a barrier remains
+        if (c->comm) {
+            const ncclResult_t nr = nccl().AllReduce(c->d_barrier, c->d_barrier, 1, ncclDouble, ncclSum,
+                                                     c->comm, c->stream);
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
+        }
+        return SKG_OK;
+    }
     const size_t nrl = (size_t)c->nrl;
     const size_t kz = (size_t)c->kc[2] + 1;  // kz_in = kz_o (pruned)
     auto nl = [&](int q) { return (size_t)(c->cstart[q + 1] - c->cstart[q]); };

@@ -184,13 +184,44 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
             }
             F::template run<+1>(v, sm, t, wb, salt);
             if (active) {
-                cd* out = a.A + m * a.fstride;
+                if (!a.p2p) {
+                    cd* out = a.A + m * a.fstride;
 #pragma unroll
-                for (int e = 0; e < E; ++e)
-                    out[((size_t)(t + T * e) * a.ystate + ys) * a.kz_in + kz] = v[e];
+                    for (int e = 0; e < E; ++e)
+                        out[((size_t)(t + T * e) * a.ystate + ys) * a.kz_in + kz] = v[e];
+                } else {  // straight into the row owner's receive block (layout [xl][kyl][kz])
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int x = t + T * e, q = x / a.nrl, xl = x - q * a.nrl;
+                        a.peer_rA[q][m * a.rfs + (size_t)a.nrl * a.kys * a.kz_in +
+                                     ((size_t)xl * a.nkyl + ys) * a.kz_in + kz] = v[e];
+                    }
+                }
             }
         }
     }
+    if (a.p2p) __threadfence_system();  // peer stores visible before the barrier
+}
+
+// p2p y-forward destinations of line j for local row x: the owner q's receive
+// block from this rank, r nrl nk_q kz + (x nk_q + kyi - ks_q) kz (exchange3's
+// layout), and the owner in own[j]
+template <int NY>
+__device__ __forceinline__ void line_offsets_p2p(const Ns3dArgs& a, int x, int kzs, int* off, int* own) {
+    for (int j = threadIdx.x; j < NY; j += blockDim.x) {
+        const int sj = signed_index(j, NY);
+        int o = -1, qq = 0;
+        if (abs(sj) <= a.kcy) {
+            const int kyi = ky_compact(a, j);
+            int q, ks, nk;
+            line_owner(a, kyi, q, ks, nk);
+            o = a.r * a.nrl * nk * kzs + (x * nk + (kyi - ks)) * kzs;
+            qq = q;
+        }
+        off[j] = o;
+        own[j] = qq;
+    }
+    __syncthreads();
 }
 
 template <int NY>
@@ -535,7 +566,9 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
     int* loff = reinterpret_cast<int*>(smem + C * F::SMEM);
-    line_offsets<NY>(a, x, a.kz_o, loff);
+    int* lown = loff + NY;
+    if (a.p2p) line_offsets_p2p<NY>(a, x, a.kz_o, loff, lown);
+    else line_offsets<NY>(a, x, a.kz_o, loff);
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
         const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
@@ -550,11 +583,14 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int lo = loff[t + T * e];
-                if (lo >= 0 && abs(signed_index(t + T * e, NY)) <= a.kcy)  // masked: never read
-                    out[(size_t)lo + kz] = v[e];
+                if (lo >= 0 && abs(signed_index(t + T * e, NY)) <= a.kcy) {  // masked: never read
+                    if (a.p2p) a.peer_D[lown[t + T * e]][m * a.dfs + (size_t)lo + kz] = v[e];
+                    else out[(size_t)lo + kz] = v[e];
+                }
             }
         }
     }
+    if (a.p2p) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ x-forward + RK
@@ -588,7 +624,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     cd v[E];
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
-        cd* line = a.B + m * a.fstride + lbase;
+        cd* line = (a.p2p ? a.rD + m * a.dfs : a.B + m * a.fstride) + lbase;
 #pragma unroll
         for (int e = 0; e < E; ++e) v[e] = io ? line[(size_t)(t + T * e) * xstr] : zero();
         F::template run<-1>(v, sm, t, wb, salt);
@@ -601,8 +637,8 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     const double kyv = a.ky_scale * (double)sky;
     const double kzv = a.kz_scale * (double)kz;
-    const cd* l0 = a.B + lbase;
-    const cd* l1 = a.B + a.fstride + lbase;
+    const cd* l0 = (a.p2p ? a.rD : a.B) + lbase;
+    const cd* l1 = (a.p2p ? a.rD + a.dfs : a.B + a.fstride) + lbase;
     int bad = 3;
     // per-step E and eps of the new state (Solver::mode_energy default,
     // simulation.cpp:163-170; dissipation_rate simulation.cpp:608-615)
@@ -787,7 +823,7 @@ template <int NY, int CT>
 cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NY, CT>::C;
     using F = BFFT<NY>;
-    const size_t smem = sizeof(cd) * F::SMEM * C + sizeof(int) * NY;  // + line offsets
+    const size_t smem = sizeof(cd) * F::SMEM * C + 2 * sizeof(int) * NY;  // + line offsets, owners
     if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
                               sizeof(int) * NY;

@@ -219,6 +219,14 @@ struct Ns3dArgs {
     cd* rA;                 // received x-inverse outputs (5 fields, stride rfs), G > 1
     cd* sD;                 // y-forward outputs to send (3 fields, stride rfs), G > 1
     size_t rfs;
+    // peer-memory exchange (see Ns2dArgs): every rank's x-inverse receive
+    // buffer (5 fields, stride rfs) and y-forward receive buffer rD (3 fields,
+    // stride dfs, uniform over the ranks)
+    int p2p;
+    cd* peer_rA[SKG_MAX_RANKS];
+    cd* peer_D[SKG_MAX_RANKS];
+    cd* rD;                 // p2p: this rank's y-forward receive buffer (3 fields, stride dfs);
+    size_t dfs;             // B stays the y/z-pass intermediate, which peers must not touch
 };
 
 // Programmatic dependent launch (sm_90+): step kernels are launched with

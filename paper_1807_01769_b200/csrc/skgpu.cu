@@ -162,6 +162,8 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         // state lines and intermediates hold only the kept kz (slab layouts
         // need a dealiased state); one partition: no exchange buffers
         const size_t nx = n[0], ny = n[1], kzc = (size_t)c->kc[2] + 1, nrl = c->nrl;
+        size_t maxcols = 0;  // B's field stride is uniform over the ranks (peer exchange)
+        for (int q = 0; q < world; ++q) maxcols = std::max(maxcols, (size_t)(c->cstart[q + 1] - c->cstart[q]));
         for (int q = 0; q < world; ++q) {
             if (nccl_id && q != rank) continue;
             Part p;
@@ -169,7 +171,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
             p.c0 = c->cstart[q];
             p.ncols = c->cstart[q + 1] - c->cstart[q];
             p.vs = nx * p.ncols * kzc;
-            p.fs = std::max(p.vs, nrl * ny * kzc);
+            p.fs = std::max(nx * maxcols * kzc, nrl * ny * kzc);
             p.rfs = nrl * Kyc * kzc;
             ok = ok && alloc((void**)&p.u, sizeof(cd) * 3 * p.vs);
             for (int i = 0; i < 3; ++i) ok = ok && alloc((void**)&p.k[i], sizeof(cd) * 3 * p.vs);
@@ -295,6 +297,7 @@ int skg_destroy(skg_ctx* c) {
             cudaFree(p.sA[f]);
             cudaFree(p.rA[f]);
         }
+        cudaFree(p.rD3);
         if (p.rA3 != p.A3) cudaFree(p.rA3);
         if (p.sD3 != p.B3) cudaFree(p.sD3);
         cudaFree(p.A3);
@@ -754,12 +757,19 @@ int skg_set_time(skg_ctx* c, double t) {
 static const int kIpcBytes = 4 * (int)sizeof(cudaIpcMemHandle_t);
 
 int skg_dist_ipc_handle(skg_ctx* c, char* out) {
-    if (!c->dist || c->solver != 2 || c->parts.size() != 1)
-        return fail(SKG_EUNSUPPORTED, "IPC handles: one ns2d slab partition per process");
+    if (!c->dist || c->G < 2 || c->parts.size() != 1)
+        return fail(SKG_EUNSUPPORTED, "IPC handles: one slab partition per process");
     CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_p2p_bufs(c)) return rc;
     const Part& p = c->parts[0];
     cd* bufs[4] = {p.rI[0], p.rI[1], p.rA[0], p.rA[1]};
-    for (int b = 0; b < 4; ++b) {
+    if (c->solver == 3) {
+        bufs[0] = p.rA3;
+        bufs[1] = p.rD3;
+    }
+    const int nb = c->solver == 3 ? 2 : 4;
+    std::memset(out, 0, kIpcBytes);
+    for (int b = 0; b < nb; ++b) {
         cudaIpcMemHandle_t h;
         CUDA_TRY(cudaIpcGetMemHandle(&h, bufs[b]));
         std::memcpy(out + b * sizeof(h), &h, sizeof(h));
@@ -768,20 +778,21 @@ int skg_dist_ipc_handle(skg_ctx* c, char* out) {
 }
 
 int skg_dist_open_peers(skg_ctx* c, const char* all) {
-    if (!c->dist || c->solver != 2 || c->parts.size() != 1 || !c->comm)
-        return fail(SKG_EUNSUPPORTED, "peer exchange across processes: NCCL ns2d slab contexts");
+    if (!c->dist || c->G < 2 || c->parts.size() != 1 || !c->comm)
+        return fail(SKG_EUNSUPPORTED, "peer exchange across processes: NCCL slab contexts");
     if (c->G > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
     CUDA_TRY(cudaSetDevice(c->device));
     const Part& me = c->parts[0];
+    const int nb = c->solver == 3 ? 2 : 4;
     for (int q = 0; q < c->G; ++q) {
-        cd* ptr[4];
+        cd* ptr[4] = {nullptr, nullptr, nullptr, nullptr};
         if (q == me.r) {
-            ptr[0] = me.rI[0];
-            ptr[1] = me.rI[1];
+            ptr[0] = c->solver == 3 ? me.rA3 : me.rI[0];
+            ptr[1] = c->solver == 3 ? me.rD3 : me.rI[1];
             ptr[2] = me.rA[0];
             ptr[3] = me.rA[1];
         } else {
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < nb; ++b) {
                 cudaIpcMemHandle_t h;
                 std::memcpy(&h, all + (size_t)q * kIpcBytes + b * sizeof(h), sizeof(h));
                 void* d = nullptr;
@@ -789,6 +800,11 @@ int skg_dist_open_peers(skg_ctx* c, const char* all) {
                 c->ipc_opened.push_back(d);
                 ptr[b] = static_cast<cd*>(d);
             }
+        }
+        if (c->solver == 3) {
+            c->peer_rA3[q] = ptr[0];
+            c->peer_D3[q] = ptr[1];
+            continue;
         }
         c->peer_rI[q][0] = ptr[0];
         c->peer_rI[q][1] = ptr[1];
@@ -805,14 +821,21 @@ int skg_dist_p2p(skg_ctx* c, int enable) {
         c->p2p = false;
         return SKG_OK;
     }
-    if (!c->dist || c->solver != 2) return fail(SKG_EUNSUPPORTED, "peer exchange: ns2d slab contexts");
+    if (!c->dist || c->G < 2) return fail(SKG_EUNSUPPORTED, "peer exchange: slab-decomposed contexts");
     if (c->comm) return fail(SKG_ECONFIG, "multi-process contexts: skg_dist_open_peers");
     if (c->G > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
-    for (const Part& p : c->parts)
+    if (int rc = ensure_p2p_bufs(c)) return rc;
+    for (const Part& p : c->parts) {
+        if (c->solver == 3) {
+            c->peer_rA3[p.r] = p.rA3;
+            c->peer_D3[p.r] = p.rD3;
+            continue;
+        }
         for (int f = 0; f < 2; ++f) {
             c->peer_rI[p.r][f] = p.rI[f];
             c->peer_rA[p.r][f] = p.rA[f];
         }
+    }
     c->p2p = true;
     return SKG_OK;
 }

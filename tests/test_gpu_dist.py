@@ -193,3 +193,17 @@ def test_slab_peer_exchange_matches(n, world):
     assert np.array_equal(a.get_state(), b.get_state())
     ra, rb = a.run(3), b.run(3)
     assert np.allclose(ra, rb, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("n,world", [((32, 32, 32), 2), ((64, 64, 64), 4), ((128, 128, 128), 8)])
+def test_slab3d_peer_exchange_matches(n, world):
+    u0 = ic.ns3d_ic(n, seed=3)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    a = api.Simulation("ns3d", n, 1e-3, dt, world=world)
+    a.set_state(u0)
+    a.step(3)
+    b = api.Simulation("ns3d", n, 1e-3, dt, world=world)
+    b.enable_p2p()
+    b.set_state(u0)
+    b.step(3)
+    assert np.array_equal(a.get_state(), b.get_state())
