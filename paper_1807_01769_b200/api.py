@@ -37,7 +37,7 @@ EXPORTS = [
     "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
     "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
-    "skg_dist_p2p", "skg_dist_ipc_handle", "skg_dist_open_peers",
+    "skg_dist_p2p", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
 ]
 
 
