@@ -14,7 +14,7 @@ HEADER = Path(__file__).resolve().parents[1] / "include" / "skgpu.h"
 
 def declared():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"\b(skg_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(skg_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_lists_the_python_exports():
