@@ -12,6 +12,7 @@ Names and semantics follow spectralkit (paths relative to
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
@@ -79,9 +80,13 @@ def load_library():
     global _lib
     if _lib is not None:
         return _lib
-    if not _LIB_PATH.exists():
-        raise SkgError(f"{_LIB_PATH} is missing: run `python -m paper_1807_01769_b200.build`")
-    L = C.CDLL(str(_LIB_PATH))
+    # SKG_LIB_VARIANT=name loads _lib/variants/libskgpu_<name>.so (A/B builds
+    # of the same sources with different tuning macros; tools/variants.sh)
+    var = os.environ.get("SKG_LIB_VARIANT")
+    path = _LIB_PATH.parent / "variants" / f"libskgpu_{var}.so" if var else _LIB_PATH
+    if not path.exists():
+        raise SkgError(f"{path} is missing: run `python -m paper_1807_01769_b200.build`")
+    L = C.CDLL(str(path))
     vp, dp, ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)
     L.skg_version.restype = C.c_char_p
     L.skg_last_error.restype = C.c_char_p

@@ -490,6 +490,9 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     using F = BFFT<NY>;
     constexpr int T = F::T, E = F::E;
     constexpr int G = T >= 256 ? 1 : 256 / T;
+    // per-thread zero band: row elements e in [6, 10) (|ky| in [6T, 8T]) are
+    // masked on input and not needed on output (fast_ok: ky_in, ld_o <= 6T)
+    constexpr int ZLO = E == 16 ? 6 : E, ZHI = E == 16 ? 10 : E;
     extern __shared__ cd smem[];
     const int ld = a.ld_i;
     const int slot = F::SMEM + 2 * ld;
@@ -509,7 +512,12 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     // the receive block of its owner r' (layout of r')
     auto issue = [&](int x) {
         if (x >= a.nrl) return;
-        for (int i = t; i < a.ky_in; i += T) {
+        // ky_in <= ZLO T (fast_ok): a fixed trip count, unrolled, so the
+        // copies of one row are issued back to back
+#pragma unroll
+        for (int j = 0; j < ZLO; ++j) {
+            const int i = t + T * j;
+            if (i >= a.ky_in) break;
             size_t q;
             if (a.G == 1) {
                 q = ((size_t)(x / RG) * a.ky_in + i) * RG + (x % RG);
@@ -542,6 +550,10 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+            if (e >= ZLO && e < ZHI) {  // |ky| >= 6T > kcy: zero (fast_ok)
+                v[e] = zero();
+                continue;
+            }
             const int idx = t + T * e;
             const bool mirror = idx > NY / 2;
             const int ki = mirror ? NY - idx : idx;
@@ -576,13 +588,23 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
             v[e] = mk(w * w - u * u, u * w);  // (v^2 - u^2) + i (u v)
         }
         F::template run<-1>(v, sm, t, wb, 0, bar);
+        // Hermitian split of the packed spectrum Z = FT(a + i b): output
+        // k = t + T e (e < ZLO) pairs with NY - k = (T - t) + T (15 - e),
+        // element 15 - e of thread T - t (thread 0: its own element 16 - e),
+        // so each thread publishes its elements [ZHI, E) and reads its
+        // partner's -- one shared-memory round trip of 6 values.
+        static_assert(ZLO == 6 && ZHI == 10 && E == 16, "zero band layout");
 #pragma unroll
-        for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+        for (int e = ZHI; e < E; ++e) sm[(e - ZHI) * T + t] = v[e];
         line_sync<T>(bar);
         if (active) {
-            for (int k = t; k < a.ld_o; k += T) {
-                const cd zk = sm[F::pad(k)];
-                const cd zm = sm[F::pad((NY - k) & (NY - 1))];
+            const int tp = t == 0 ? 0 : T - t;
+#pragma unroll
+            for (int e = 0; e < ZLO; ++e) {
+                const int k = t + T * e;
+                if (k >= a.ld_o) break;
+                const cd zk = v[e];
+                const cd zm = t == 0 ? (e == 0 ? v[0] : v[16 - e]) : sm[(15 - e - ZHI) * T + tp];
                 *ypass_dst(a, 0, x, k) = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
                 *ypass_dst(a, 1, x, k) = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
             }
@@ -592,38 +614,67 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
     if (a.p2p) __threadfence_system();
 }
 
+// Operands of one kept mode of the x-forward epilogue, loaded for a chunk
+// of modes before any of them is computed (the k_j / u stores of a mode
+// would otherwise keep the compiler from hoisting the next mode's loads).
+struct XfOps {
+    cd u, k1, k2, k3;
+    double e1, e2;  // integrating factors of the mode (has_sigma)
+};
+
+__device__ __forceinline__ XfOps xf_load(const Ns2dArgs& a, bool final, bool fuse, int stage, double e1y,
+                                         double e2y, int i, size_t idx) {
+    XfOps o;
+    o.u = (final || fuse) ? a.u[idx] : zero();
+    if (final && !a.rk2) {
+        o.k1 = a.k1[idx];
+        o.k2 = a.k2[idx];
+        o.k3 = a.k3[idx];
+    }
+    o.e1 = o.e2 = 1.0;
+    if (a.has_sigma && (final || fuse)) {
+        o.e1 = a.e1x[i] * e1y;
+        if (final || stage + 1 == 4) o.e2 = a.e2x[i] * e2y;
+    }
+    return o;
+}
+
 // One kept mode (kx index i, local column kyl) of the x-forward epilogue:
 // tendency kv (+ forcing) -> k_j, or the final RK update of u with the
 // non-finite flag and the per-step diagnostics; returns the next stage state
 // (fused kernels: stage_combine, or the new u = stage 1 of the next step).
-__device__ __forceinline__ cd xf_point(const Ns2dArgs& a, int stage, bool final, bool fuse, int ky,
-                                       double kyv, double kxv, double pw, int i, size_t idx, cd kv,
+__device__ __forceinline__ cd xf_point(const Ns2dArgs& a, int stage, bool final, bool fuse, double kyv,
+                                       double kxv, double pw, size_t idx, cd kv, const XfOps& o,
                                        bool& bad, double& sE, double& sZ, double& sD) {
     if (a.force) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
     if (!final) {
         cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
         kout[idx] = kv;
-        return fuse ? stage_combine(a, stage + 1, ky, i, a.u[idx], kv) : zero();
+        if (!fuse) return zero();
+        // stage_combine of stage + 1 (time_stepping.cpp:128-170)
+        const int ns = stage + 1;
+        if (a.has_sigma) {
+            if (ns == 2) return scale(add(o.u, scale(kv, hdt_of(a))), o.e1);
+            if (ns == 3) return add(scale(o.u, o.e1), scale(kv, hdt_of(a)));
+            return add(scale(o.u, o.e2), scale(kv, dt_of(a) * o.e1));
+        }
+        return add(o.u, scale(kv, ns == 4 ? dt_of(a) : hdt_of(a)));
     }
-    const cd u = a.u[idx];
+    const cd u = o.u;
     cd un;
     if (a.has_sigma) {
-        const double e1 = a.e1x[i] * a.e1y[ky];
-        const double e2 = a.e2x[i] * a.e2y[ky];
         if (a.rk2) {
-            un = add(scale(u, e2), scale(kv, dt_of(a) * e1));
+            un = add(scale(u, o.e2), scale(kv, dt_of(a) * o.e1));
         } else {
-            const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-            const cd sum = add(add(scale(k1, e2), scale(add(k2, k3), 2.0 * e1)), kv);
-            un = add(scale(u, e2), scale(sum, sdt_of(a)));
+            const cd sum = add(add(scale(o.k1, o.e2), scale(add(o.k2, o.k3), 2.0 * o.e1)), kv);
+            un = add(scale(u, o.e2), scale(sum, sdt_of(a)));
         }
     } else {
         cd delta;
         if (a.rk2) {
             delta = scale(kv, dt_of(a));
         } else {
-            const cd k1 = a.k1[idx], k2 = a.k2[idx], k3 = a.k3[idx];
-            delta = scale(add(add(k1, scale(add(k2, k3), 2.0)), kv), sdt_of(a));
+            delta = scale(add(add(o.k1, scale(add(o.k2, o.k3), 2.0)), kv), sdt_of(a));
         }
         un = (delta.x != 0.0 || delta.y != 0.0) ? add(u, delta) : u;
     }
@@ -699,25 +750,40 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
         sZ += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
     }
     const bool fuse = FUSE && next;
+    const double e1y = a.has_sigma ? a.e1y[ky] : 1.0, e2y = a.has_sigma ? a.e2y[ky] : 1.0;
+    // chunks of CH kept modes: the chunk's operand loads, then its arithmetic
+    // (CH = 2 spills at 4096 and measured 262 vs 212 us)
+    constexpr int CH = 1;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
+    for (int e0 = 0; e0 < E; e0 += CH) {
         if (!active) break;
-        if (e >= ZLO && e < ZHI) continue;  // |kx| > kcx there
-        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
-        const int i = t + T * e;
-        const int si = signed_index(i, NX);
-        if (abs(si) > a.kcx || (i == 0 && ky == 0)) {
-            if (fuse) sv[slot * T + t] = zero();  // psi of the next stage: 0 here
-            continue;
+        XfOps ops[CH];
+        bool kp[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+            const int e = e0 + j, i = t + T * e;
+            kp[j] = !(e >= ZLO && e < ZHI) && abs(signed_index(i, NX)) <= a.kcx && !(i == 0 && ky == 0);
+            if (kp[j]) ops[j] = xf_load(a, final, fuse, stage, e1y, e2y, i, (size_t)kyl * NX + i);
         }
-        const double kxv = a.kx_scale * (double)si;
-        const size_t idx = (size_t)kyl * NX + i;
-        const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
-        const cd wn = xf_point(a, stage, final, fuse, ky, kyv, kxv, pw, i, idx, kv, bad, sE, sZ, sD);
-        if (fuse) {  // psi = w / |k|^2 of the next stage (k1_xinv prologue)
-            const double ksq = kxv * kxv + kyv * kyv;
-            const double r = __drcp_rn(ksq);  // ksq > 0: the mean mode was skipped
-            sv[slot * T + t] = mk(wn.x * r, wn.y * r);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+            const int e = e0 + j;
+            if (e >= ZLO && e < ZHI) continue;  // |kx| > kcx there
+            const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+            const int i = t + T * e;
+            if (!kp[j]) {
+                if (fuse) sv[slot * T + t] = zero();  // psi of the next stage: 0 here
+                continue;
+            }
+            const double kxv = a.kx_scale * (double)signed_index(i, NX);
+            const size_t idx = (size_t)kyl * NX + i;
+            const cd kv = add(sv[slot * T + t], scale(v[e], kxv * kxv - kyv * kyv));
+            const cd wn = xf_point(a, stage, final, fuse, kyv, kxv, pw, idx, kv, ops[j], bad, sE, sZ, sD);
+            if (fuse) {  // psi = w / |k|^2 of the next stage (k1_xinv prologue)
+                const double ksq = kxv * kxv + kyv * kyv;
+                const double r = __drcp_rn(ksq);  // ksq > 0: the mean mode was skipped
+                sv[slot * T + t] = mk(wn.x * r, wn.y * r);
+            }
         }
     }
     if (final && a.diag) diag_accumulate(a.diag + 3 * (a.flags->steps - 1), sE, sZ, sD);
@@ -934,7 +1000,7 @@ bool fast_ok(const Ns2dArgs& a) {
     if (!a.pruned || a.nx < 64 || a.ny < 64) return false;
     if (3 * a.kcx >= a.nx || 3 * a.kcy >= a.ny) return false;
     const int T = a.nx / 16;
-    return a.kcx <= 6 * T - 1;
+    return a.kcx <= 6 * T - 1 && a.ky_in <= 6 * (a.ny / 16) && a.ld_o <= 6 * (a.ny / 16);
 }
 
 }  // namespace
