@@ -70,16 +70,21 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(cfg_name):
-    """ncu dram bytes per launch of the dominant kernel, from the committed summary."""
+def load_ncu(cfg_name, key):
+    """A per-launch counter of the dominant kernel (ncu), from the committed summary."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
         d = json.loads(p.read_text())
-        return d.get(cfg_name, {}).get("dominant_dram_bytes_per_launch")
+        return d.get(cfg_name, {}).get(key)
     except Exception:
         return None
+
+
+def load_traffic(cfg_name):
+    """ncu dram bytes per launch of the dominant kernel."""
+    return load_ncu(cfg_name, "dominant_dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -316,6 +321,22 @@ def run_our_arm(args):
            "frac_of_measured_peak": (fmp_bytes / (peak * 1e9) * 1e3) / ms_step,
            "note": "BASELINE target: >= 0.60 on 1 B200 (SURVEY 8(d) model, unpruned bytes)"}
     traffic = load_traffic(args.config)
+    # FP64 roofline of the same kernel: its ncu FP64 instruction count per
+    # launch over its average launch time, against the measured DFMA rate
+    fp64 = None
+    try:
+        peak_inst = api.fp64_peak(local)
+        inst = load_ncu(args.config, "dominant_fp64_inst_per_launch")
+        avg_s = (dms / dn) / 1e3 if dn else None
+        fp64 = {"bound": "fp64", "kernel": dom, "peak_inst_per_s": peak_inst,
+                "peak_tflops": 2.0 * peak_inst / 1e12,
+                "peak_source": "measured (skg_fp64_peak: DFMA-only kernel on every SM)",
+                "inst_per_launch": inst,
+                "inst_source": "ncu DADD+DMUL+DFMA thread instructions (profiles/ncu_summary.json)",
+                "achieved_inst_per_s": (inst / avg_s) if (inst and avg_s) else None,
+                "frac": (inst / avg_s / peak_inst) if (inst and avg_s) else None}
+    except Exception as exc:
+        fp64 = {"unavailable": str(exc)}
 
     # ---- e2e through the C ABI with host buffers
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -377,6 +398,7 @@ def run_our_arm(args):
                          "step_algorithmic_GB": step_bytes / 1e9,
                          "step_frac": (step_bytes / (ms_step / 1e3) / 1e9) / peak},
             "fmp_roofline": fmp,
+            "fp64_roofline": fp64,
             "all_to_all": ({"bytes_per_step_per_gpu": stats["exchange"][2] / k_inst,
                             "ms_per_step": stats["exchange"][0] / k_inst,
                             "t_roof_ms_at_900GBps": stats["exchange"][2] / k_inst / 900e9 * 1e3}

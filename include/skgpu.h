@@ -241,6 +241,13 @@ int skg_set_timing(skg_ctx* ctx, int enable);
 int skg_kernel_stats(skg_ctx* ctx, int cls, double* total_ms, long* launches, double* bytes);
 int skg_reset_stats(skg_ctx* ctx);
 
+/* Measurement support (no reference counterpart): the FP64 FMA throughput of
+ * `device` measured with a DFMA-only kernel (8 independent chains per thread,
+ * every SM filled), in DFMA thread-instructions per second (2 flops each).
+ * bench.py's FP64 roofline divides the butterfly kernels' FP64 instruction
+ * counts (ncu) by their launch times against this number. */
+int skg_fp64_peak(int device, double* dfma_per_s);
+
 #ifdef __cplusplus
 }
 #endif

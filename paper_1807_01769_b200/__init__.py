@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     UnsupportedError,
     fft_forward,
     fft_inverse,
+    fp64_peak,
     lib_path,
     load_library,
     nccl_unique_id,

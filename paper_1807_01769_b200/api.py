@@ -35,7 +35,7 @@ EXPORTS = [
     "skg_iteration", "skg_time", "skg_tendency", "skg_fft_forward", "skg_fft_inverse",
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
-    "skg_reset_stats", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
+    "skg_reset_stats", "skg_fp64_peak", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
     "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
     "skg_dist_p2p", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
@@ -96,6 +96,7 @@ def load_library():
     L.skg_create_dist.argtypes = [C.POINTER(vp), C.c_char_p, C.c_int, ip, dp, C.c_double,
                                   C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p]
     L.skg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.skg_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.skg_set_stream.argtypes = [vp, vp]
     for f in ("skg_spect_size", "skg_phys_size", "skg_iteration", "skg_launch_count"):
         getattr(L, f).argtypes = [vp]
@@ -175,6 +176,16 @@ def _check_shape(shape):
         if n % 2:
             raise ShapeError(f"extent {n} is odd")
     return shape
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Measured DFMA thread-instructions per second of `device` (skg_fp64_peak;
+    2 flops each): the FP64 ceiling of bench.py's butterfly roofline."""
+    out = C.c_double(0.0)
+    rc = load_library().skg_fp64_peak(int(device), C.byref(out))
+    if rc:
+        _raise(rc)
+    return out.value
 
 
 def nccl_unique_id() -> bytes:

@@ -277,6 +277,7 @@ cudaError_t launch_count_masked(const cd* f, int dims, const int* n, const int* 
 cudaError_t launch_grid_dump(int dims, const int* n, const int* kc, const double* kscale,
                              int axis, double* d_k, unsigned char* d_mask, cudaStream_t s,
                              long* launches);
+cudaError_t fp64_peak(int device, double* dfma_per_s);  // util.cu (skg_fp64_peak)
 // Return the error of a CUDA call from a cudaError_t function.
 #define SKG_TRY(...)                                \
     do {                                            \

@@ -845,6 +845,16 @@ int skg_set_timing(skg_ctx* c, int enable) {
     return SKG_OK;
 }
 
+int skg_fp64_peak(int device, double* dfma_per_s) {
+    if (!dfma_per_s) return fail(SKG_ECONFIG, "fp64_peak: null output pointer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SKG_ECUDA, "no CUDA device visible (the library has no CPU path)");
+    if (device < 0 || device >= ndev) return fail(SKG_ECONFIG, "device ordinal out of range");
+    CUDA_TRY(skg::fp64_peak(device, dfma_per_s));
+    return SKG_OK;
+}
+
 int skg_reset_stats(skg_ctx* c) {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -6,6 +6,23 @@ namespace skg {
 
 namespace {
 
+// DFMA throughput probe (skg_fp64_peak): 8 independent dependency chains per
+// thread so the FP64 pipe, not latency, bounds the loop.
+__global__ void __launch_bounds__(256) fp64_probe(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-3 + j;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += x[j];
+    if (s == 123.456) out[0] = s;  // keeps the chains live
+}
+
+
 constexpr int TD = 32;
 
 // out[c][r] = in[r][c] (complex), 32x32 tiles through shared memory.
@@ -261,6 +278,36 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
     SKG_TRY(launch_pdl(energy_kernel, 592, 256, 0, s, f, g, nvars, S, d_out, steps));
     ++*launches;
     return cudaGetLastError();
+}
+
+cudaError_t fp64_peak(int device, double* dfma_per_s) {
+    SKG_TRY(cudaSetDevice(device));
+    int sms = 0;
+    SKG_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* d = nullptr;
+    SKG_TRY(cudaMalloc(&d, sizeof(double)));
+    cudaEvent_t e0, e1;
+    SKG_TRY(cudaEventCreate(&e0));
+    SKG_TRY(cudaEventCreate(&e1));
+    const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+    fp64_probe<<<blocks, threads>>>(d, 256, 0.999, 1e-3);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        SKG_TRY(cudaEventRecord(e0));
+        fp64_probe<<<blocks, threads>>>(d, iters, 0.999, 1e-3);
+        SKG_TRY(cudaEventRecord(e1));
+        SKG_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SKG_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        if (ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    if (err != cudaSuccess) return err;
+    *dfma_per_s = (double)blocks * threads * 8.0 * iters / (best * 1e-3);
+    return cudaSuccess;
 }
 
 }  // namespace skg

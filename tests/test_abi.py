@@ -52,6 +52,8 @@ def test_no_cpu_fallback():
         api.Simulation("ns2d", (32, 32), 1e-3, 1e-3)
     with pytest.raises(api.CudaError):
         api.fft_forward(np.zeros((8, 8)))
+    with pytest.raises(api.CudaError):
+        api.fp64_peak(0)
 
 
 def test_argument_validation_before_device():

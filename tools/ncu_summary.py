@@ -36,6 +36,10 @@ METRICS = [
 ]
 
 
+# setup / measurement kernels of a bench run that are not part of the RK step
+NOT_STEP = ("fp64_probe", "count_masked", "transpose_c", "grid_dump")
+
+
 def short(name: str) -> str:
     m = re.search(r"(k\w+?)<([^>]*)>", name)
     return f"{m.group(1)}<{m.group(2)}>" if m else name.split("(")[0][-40:]
@@ -48,6 +52,8 @@ def launches(path: Path, out: Path):
     agg = collections.OrderedDict()
     for r in rows[1:]:
         k = short(r[i_n])
+        if any(x in k for x in NOT_STEP):
+            continue
         agg.setdefault(k, []).append(float(r[i_v].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
     with open(out, "w") as f:
@@ -67,8 +73,14 @@ def report(rep: Path, out: Path):
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     kern = []
+    fp64_ops = [f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"
+                for op in ("dadd", "dmul", "dfma")]
     for r in rows[2:]:
         d = {"kernel": short(r[idx["Kernel Name"]])}
+        if all(m in idx for m in fp64_ops) and "sm__cycles_elapsed.avg" in idx:
+            # FP64 thread-instructions of the launch (DADD + DMUL + DFMA)
+            cyc = float(r[idx["sm__cycles_elapsed.avg"]].replace(",", ""))
+            d["fp64_inst"] = cyc * sum(float(r[idx[m]].replace(",", "")) for m in fp64_ops)
         for m, lab in METRICS:
             if m in idx:
                 d[lab] = (r[idx[m]], units[idx[m]])
@@ -107,13 +119,20 @@ def main():
         for k in kern:
             if "DRAM read" in k and "DRAM write" in k:
                 per.setdefault(k["kernel"], []).append(to_bytes(*k["DRAM read"]) + to_bytes(*k["DRAM write"]))
+        fp = {}
+        for k in kern:
+            if "fp64_inst" in k:
+                fp.setdefault(k["kernel"], []).append(k["fp64_inst"])
         entry = {"tag": a.tag, "kernels_dram_bytes_per_launch":
-                 {k: sum(v) / len(v) for k, v in per.items()}}
+                 {k: sum(v) / len(v) for k, v in per.items()},
+                 "kernels_fp64_inst_per_launch": {k: sum(v) / len(v) for k, v in fp.items()}}
         if a.dominant:
             for k, v in per.items():
                 if k.startswith(a.dominant):
                     entry["dominant"] = k
                     entry["dominant_dram_bytes_per_launch"] = sum(v) / len(v)
+                    if k in fp:
+                        entry["dominant_fp64_inst_per_launch"] = sum(fp[k]) / len(fp[k])
         d[a.config] = entry
         summ.write_text(json.dumps(d, indent=1, sort_keys=True))
 
