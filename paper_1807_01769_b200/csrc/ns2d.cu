@@ -26,6 +26,13 @@
 // Elements per thread of the fast path's x passes below 4096: 8 (twice the
 // threads per column; these grids have too few kept columns to fill the GPU
 // with 16-element lines -- 1024^2: 0.148 -> 0.118 ms/step, 256^2 0.136 -> 0.064).
+// Same for the y pass (1024^2 0.119 -> 0.117, 2048^2 0.448 -> 0.423).
+#ifndef SKG_FAST_Y_EM_SMALL
+#define SKG_FAST_Y_EM_SMALL 8
+#endif
+#ifndef SKG_FAST_Y_EM
+#define SKG_FAST_Y_EM 16
+#endif
 #ifndef SKG_FAST_X_EM_SMALL
 #define SKG_FAST_X_EM_SMALL 8
 #endif
@@ -490,15 +497,17 @@ __global__ void k4_decay(Ns2dArgs a) {
 
 // y pass, one row per group iteration, persistent over rows; the next row's
 // two input lines stream into shared memory (cp.async) during the FFTs.
-template <int NY, bool CFL>
-__global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY>::T > 256 ? 1 : 2)
+template <int NY, bool CFL, int EM = 16>
+__global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false, EM>::T : 256,
+                                  BFFT<NY, false, EM>::T > 256 ? 1 : 2)
     k3b_phys(Ns2dArgs a) {
-    using F = BFFT<NY>;
+    using F = BFFT<NY, false, EM>;
     constexpr int T = F::T, E = F::E;
     constexpr int G = T >= 256 ? 1 : 256 / T;
-    // per-thread zero band: row elements e in [6, 10) (|ky| in [6T, 8T]) are
-    // masked on input and not needed on output (fast_ok: ky_in, ld_o <= 6T)
-    constexpr int ZLO = E == 16 ? 6 : E, ZHI = E == 16 ? 10 : E;
+    // per-thread zero band: row elements e in [6, 10) (E = 16; [3, 5) for
+    // E = 8), |ky| in [3N/8, N/2], are masked on input and not needed on
+    // output (fast_ok: ky_in, ld_o <= 3N/8)
+    constexpr int ZLO = E == 16 ? 6 : E == 8 ? 3 : E, ZHI = E == 16 ? 10 : E == 8 ? 5 : E;
     extern __shared__ cd smem[];
     const int ld = a.ld_i;
     const int slot = F::SMEM + 2 * ld;
@@ -595,11 +604,11 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
         }
         F::template run<-1>(v, sm, t, wb, 0, bar);
         // Hermitian split of the packed spectrum Z = FT(a + i b): output
-        // k = t + T e (e < ZLO) pairs with NY - k = (T - t) + T (15 - e),
-        // element 15 - e of thread T - t (thread 0: its own element 16 - e),
+        // k = t + T e (e < ZLO) pairs with NY - k = (T - t) + T (E - 1 - e),
+        // element E - 1 - e of thread T - t (thread 0: its own element E - e),
         // so each thread publishes its elements [ZHI, E) and reads its
-        // partner's -- one shared-memory round trip of 6 values.
-        static_assert(ZLO == 6 && ZHI == 10 && E == 16, "zero band layout");
+        // partner's -- one shared-memory round trip of E - ZHI values.
+        static_assert(ZLO + ZHI == E, "zero band symmetric about N/2");
 #pragma unroll
         for (int e = ZHI; e < E; ++e) sm[(e - ZHI) * T + t] = v[e];
         line_sync<T>(bar);
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(BFFT<NY>::T > 256 ? BFFT<NY>::T : 256, BFFT<NY
                 const int k = t + T * e;
                 if (k >= a.ld_o) break;
                 const cd zk = v[e];
-                const cd zm = t == 0 ? (e == 0 ? v[0] : v[16 - e]) : sm[(15 - e - ZHI) * T + tp];
+                const cd zm = t == 0 ? (e == 0 ? v[0] : v[E - e]) : sm[(E - 1 - e - ZHI) * T + tp];
                 *ypass_dst(a, 0, x, k) = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
                 *ypass_dst(a, 1, x, k) = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
             }
@@ -890,17 +899,18 @@ cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
 
 template <int NY, bool CFL>
 cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
-    using F = BFFT<NY>;
+    constexpr int EM = NY >= 4096 ? SKG_FAST_Y_EM : SKG_FAST_Y_EM_SMALL;
+    using F = BFFT<NY, false, EM>;
     constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * (F::SMEM + 2 * a.ld_i) * G;
     static size_t init = 0;
     if (init < smem) {
-        cudaFuncSetAttribute(k3b_phys<NY, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k3b_phys<NY, CFL, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         init = smem;
     }
     const int groups = (a.nrl + G - 1) / G;
     const int grid = groups < a.wave ? groups : a.wave;
-    SKG_TRY(launch_pdl(k3b_phys<NY, CFL>, grid, F::T * G, smem, s, a));
+    SKG_TRY(launch_pdl(k3b_phys<NY, CFL, EM>, grid, F::T * G, smem, s, a));
     return cudaGetLastError();
 }
 
