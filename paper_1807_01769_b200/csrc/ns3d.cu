@@ -102,10 +102,23 @@ __device__ __forceinline__ cd stage_input3(const Ns3dArgs& a, int stage, int c, 
     return add(u, scale(a.k3[idx], dt_of(a)));
 }
 
+// Elements per thread of the strided (x, y) passes: 8 for N <= SKG3_EM8_MAX
+// (twice the threads per line; the small grids have too few lines to fill
+// the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3
+// 0.341 -> 0.222, 128^3 0.634 -> 0.630, 256^3 4.19 -> 4.06, 512^3 32.8 -> 36.4
+// (so 16 from 512 on).
+#ifndef SKG3_EM8_MAX
+#define SKG3_EM8_MAX 256
+#endif
+template <int N>
+constexpr int em3() { return N <= SKG3_EM8_MAX && N >= 16 ? 8 : 16; }
+template <int N>
+using BF3 = BFFT<N, false, em3<N>()>;
+
 // Lines per CTA for the strided passes: lanes walk the contiguous kz axis.
 template <int N, int CT = 256>
 struct Strided {
-    using F = BFFT<N>;
+    using F = BF3<N>;
     static constexpr int T = F::T;
     static constexpr int C = T >= CT ? 1 : CT / T;
     static constexpr int MINB = T * C >= 512 ? 1 : 512 / (T * C);  // keeps <= 128 registers
@@ -118,9 +131,10 @@ struct Strided {
 // per-thread elements e in [6, 10) are zero and need no slot.
 template <int NX, bool PZ, int CB = 256>
 __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, int stage) {
-    using F = BFFT<NX>;
+    using F = BF3<NX>;
     constexpr int T = F::T, E = F::E, C = Strided<NX, CB>::C;
-    constexpr int ZLO = PZ ? 6 : E, ZHI = PZ ? 10 : E;
+    // zero band e in [3E/8, 5E/8): kx in [3N/8, 5N/8)
+    constexpr int ZLO = PZ ? 3 * E / 8 : E, ZHI = PZ ? 5 * E / 8 : E;
     constexpr int CT = T * C;  // threads per CTA
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
@@ -247,7 +261,7 @@ __device__ __forceinline__ void line_offsets(const Ns3dArgs& a, int x, int kzs, 
 // ------------------------------------------------------------------ y-inverse
 template <int NY, int CT = 256>
 __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
-    using F = BFFT<NY>;
+    using F = BF3<NY>;
     constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
@@ -320,7 +334,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
 // A3 / A0.
 template <int NY, int CT = 256>
 __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) {
-    using F = BFFT<NY>;
+    using F = BF3<NY>;
     constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
@@ -552,7 +566,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
 // ------------------------------------------------------------------ y-forward
 template <int NY, int CT = 256>
 __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) {
-    using F = BFFT<NY>;
+    using F = BF3<NY>;
     constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
@@ -601,7 +615,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
 // run a leaner one that only stores k_j.
 template <int NX, int CT = 256, bool FIN = false>
 __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, int stage) {
-    using F = BFFT<NX>;
+    using F = BF3<NX>;
     constexpr int T = F::T, E = F::E, C = Strided<NX, CT>::C;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
@@ -770,13 +784,13 @@ void set_smem(K kernel, size_t bytes, size_t& done) {
 template <int NX, int CT>
 cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NX, CT>::C;
-    using F = BFFT<NX>;
+    using F = BF3<NX>;
     if (inverse) {
         const int grid = a.nkyl * ((a.kz_in + C - 1) / C);
-        const bool pz = NX >= 64 && a.pruned && a.kcx <= 6 * F::T - 1;
+        const bool pz = NX >= 64 && a.pruned && a.kcx <= 3 * F::E / 8 * F::T - 1;
         if (pz) {
             if constexpr (NX >= 64) {
-                const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - 4) * F::T * C);
+                const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - F::E / 4) * F::T * C);
                 static size_t done = 0;
                 set_smem(k1_3d<NX, true, CT>, smem, done);
                 SKG_TRY(launch_pdl(k1_3d<NX, true, CT>, grid, F::T * C, smem, s, a, stage));
@@ -822,7 +836,7 @@ cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s
 template <int NY, int CT>
 cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NY, CT>::C;
-    using F = BFFT<NY>;
+    using F = BF3<NY>;
     const size_t smem = sizeof(cd) * F::SMEM * C + 2 * sizeof(int) * NY;  // + line offsets, owners
     if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
