@@ -235,14 +235,32 @@ def run_our_arm(args):
     P = int(np.prod(n))
     S = u0.size  # complex modes over all variables
     slab = ws > 1
+    p2p_used = False
     if slab:
         # slab decomposition over the ranks (strong scaling of
         # one grid), transposes as NCCL all-to-all inside libskgpu
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
-        if args.p2p and solver == "ns2d":
-            sim.enable_p2p()
+        if not args.no_p2p:
+            # fused exchange: the pass epilogues store into the owners'
+            # receive buffers (CUDA IPC over NVLink); every rank must agree,
+            # else all fall back to the NCCL all-to-all
+            import torch
+            ok, why = 1, ""
+            try:
+                sim.enable_p2p()
+            except Exception as exc:  # e.g. CUDA IPC not permitted on this host
+                ok, why = 0, str(exc)
+            flag = torch.tensor([ok], device="cuda", dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            p2p_used = bool(flag.item())
+            if not p2p_used:
+                if ok:
+                    sim.disable_p2p()
+                if rank == 0:
+                    print(f"peer exchange unavailable ({why or 'another rank failed'}); "
+                          "NCCL all-to-all", file=sys.stderr)
     else:
         compact = args.layout == "compact" or (args.layout == "auto" and args.config in COARSE_IC)
         sim = api.Simulation(solver, n, nu, dt, device=local, compact=compact)
@@ -387,7 +405,8 @@ def run_our_arm(args):
                 "workload": f"{args.config}: {solver} {'x'.join(map(str, n))} RK4 step, "
                             f"nu={nu}, dt={dt:.6g} (CFL 0.5)",
                 "solver": solver, "n": list(n), "global_batch": 1 if slab else ws,
-                "parallelism": f"slab{ws} (NCCL all-to-all)" if slab else "single-gpu",
+                "parallelism": (f"slab{ws} ({'peer-memory exchange over NVLink' if p2p_used else 'NCCL all-to-all'})"
+                                if slab else "single-gpu"),
                 "l2": "every field array > 126 MB L2; no flush needed",
                 "dealiased_fast_path": pruned,
             },
@@ -432,8 +451,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--instrumented-steps", type=int, default=20)
-    ap.add_argument("--p2p", action="store_true",
-                    help="ns2d slab under torchrun: peer-memory exchange (CUDA IPC) instead of NCCL copies")
+    ap.add_argument("--no-p2p", action="store_true",
+                    help="slab under torchrun: NCCL all-to-all copies instead of the peer-memory "
+                         "exchange (CUDA IPC stores from the pass epilogues, the default)")
     ap.add_argument("--layout", choices=["auto", "full", "compact"], default="auto",
                     help="ns3d one-GPU layout (auto: compact where the full layout does not fit)")
     args = ap.parse_args()

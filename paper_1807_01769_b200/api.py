@@ -459,6 +459,10 @@ class Simulation:
         blob = b"".join(out)
         self._call("skg_dist_open_peers", C.create_string_buffer(blob, len(blob)))
 
+    def disable_p2p(self) -> None:
+        """Back to the NCCL / device-copy exchange (skg_dist_p2p(0))."""
+        self._call("skg_dist_p2p", C.c_int(0))
+
     def sanitize_state(self) -> None:
         """Solver::sanitize_state on the device (dealias, ns2d mean 0, ns3d
         Leray projection), as the reference applies to initial fields."""
