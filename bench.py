@@ -191,10 +191,11 @@ def run_reference_arm(args):
     ref.set_workers(threads)
     r = ref.RefSimulation(solver, n, nu, dt)
     r.set_state(u0)
-    # warm-up as the reference's own bench protocol: one untimed step
-    # (proj/src/bench.cpp:79-82); then up to K steps within a time budget so
+    # W untimed warm-up steps (the reference's own bench protocol uses one,
+    # proj/src/bench.cpp:79-82); then up to K steps within a time budget so
     # the run stays within a few minutes (each step is a full step_once).
-    t_warm = r.step(1)
+    for _ in range(max(1, args.warmup)):
+        t_warm = r.step(1)
     budget = args.ref_budget_s
     times = []
     while len(times) < args.steps and (sum(times) + (times[-1] if times else t_warm)) <= budget:
@@ -206,14 +207,14 @@ def run_reference_arm(args):
     value = P / sec / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": len(times),
-        "requested_steps": args.steps, "warmup": 1, "ms_per_step": sec * 1e3,
+        "requested_steps": args.steps, "warmup": max(1, args.warmup), "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded spectral Gaussian IC, BASELINE recipe)", "impl": "reference",
         "config": {"workload": f"{args.config} RK4 step (step_once), nu={nu}, dt={dt:.6g}",
                    "solver": solver, "n": list(n), "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{len(times)} step_once calls of {args.config} after "
-                                   f"1 warm-up (budget {budget:.0f} s); reference proj/src compiled "
+                                   f"{max(1, args.warmup)} warm-up (budget {budget:.0f} s); reference proj/src compiled "
                                    f"unmodified, FFT = oracle/fft_shim.c (not FFTW)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
