@@ -130,8 +130,6 @@ int refresh_exp(skg_ctx* c, double dt) {
     // Separable factors: exp(h sigma) = prod_d exp(h (-nu k_d^2)) with
     // sigma = -nu |k|^2 (simulation.cpp:147-157, time_stepping.cpp:49-52).
     const int d = c->dims;
-    std::vector<double> h;
-    int off = 0;
     int ext[3];
     for (int a = 0; a < d; ++a) ext[a] = a == d - 1 ? c->nh : c->n[a];
     std::vector<double> tab;
@@ -145,7 +143,6 @@ int refresh_exp(skg_ctx* c, double dt) {
             }
         }
     }
-    (void)off;
     CUDA_TRY(cudaMemcpyAsync(c->etab, tab.data(), tab.size() * sizeof(double),
                              cudaMemcpyHostToDevice, c->stream));
     c->cached_dt = dt;

@@ -110,33 +110,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 __device__ __forceinline__ bool finite2(cd v) { return isfinite(v.x) && isfinite(v.y); }
 
-// RK stage state at (kx index i, ky index j) from u and the previous k.
-__device__ __forceinline__ cd stage_input(const Ns2dArgs& a, int stage, int ky, int i,
-                                          size_t idx) {
-    cd u = a.u[idx];
-    if (stage <= 1) return u;
-    if (a.has_sigma) {
-        if (stage == 2) {
-            const double e1 = a.e1x[i] * a.e1y[ky];
-            cd k = a.k1[idx];
-            return scale(add(u, scale(k, hdt_of(a))), e1);
-        } else if (stage == 3) {
-            const double e1 = a.e1x[i] * a.e1y[ky];
-            cd k = a.k2[idx];
-            return add(scale(u, e1), scale(k, hdt_of(a)));
-        } else {
-            const double e1 = a.e1x[i] * a.e1y[ky];
-            const double e2 = a.e2x[i] * a.e2y[ky];
-            cd k = a.k3[idx];
-            return add(scale(u, e2), scale(k, dt_of(a) * e1));
-        }
-    } else {
-        if (stage == 2) return add(u, scale(a.k1[idx], hdt_of(a)));
-        if (stage == 3) return add(u, scale(a.k2[idx], hdt_of(a)));
-        return add(u, scale(a.k3[idx], dt_of(a)));
-    }
-}
-
 // RK stage state from already-loaded u and previous k (time_stepping.cpp:128-170).
 __device__ __forceinline__ cd stage_combine(const Ns2dArgs& a, int stage, int ky, int i, cd u, cd k) {
     if (stage <= 1) return u;
@@ -163,7 +136,7 @@ struct XCfg {
     static constexpr int T = F::T;
     static constexpr int LPC = T >= CTW ? 1 : CTW / T;
     static constexpr int CT = T * LPC;
-    static constexpr int MINB = CT >= 256 ? 2 : 512 / CT;  // keeps <= 128 registers
+    static constexpr int MINB = CT >= 256 ? 2 : (512 / CT > 32 ? 32 : 512 / CT);  // keeps <= 128 registers
     static constexpr int ZLO = EM == 16 ? 6 : 3, ZHI = EM == 16 ? 10 : 5;
 };
 

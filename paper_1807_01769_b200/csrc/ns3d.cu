@@ -84,24 +84,6 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
     return ky <= a.kcy ? ky : ky - (a.ny - (2 * a.kcy + 1));
 }
 
-// RK stage state of variable c at mode (i, ky, kz)  (time_stepping.cpp:128-170)
-__device__ __forceinline__ cd stage_input3(const Ns3dArgs& a, int stage, int c, int i, int ky,
-                                           int kz) {
-    const size_t idx = sidx(a, i, ky, kz) + c * a.vstride;
-    const cd u = a.u[idx];
-    if (stage <= 1) return u;
-    if (a.has_sigma) {
-        const double e1 = a.e1x[i] * a.e1y[ky] * a.e1z[kz];
-        if (stage == 2) return scale(add(u, scale(a.k1[idx], hdt_of(a))), e1);
-        if (stage == 3) return add(scale(u, e1), scale(a.k2[idx], hdt_of(a)));
-        const double e2 = a.e2x[i] * a.e2y[ky] * a.e2z[kz];
-        return add(scale(u, e2), scale(a.k3[idx], dt_of(a) * e1));
-    }
-    if (stage == 2) return add(u, scale(a.k1[idx], hdt_of(a)));
-    if (stage == 3) return add(u, scale(a.k2[idx], hdt_of(a)));
-    return add(u, scale(a.k3[idx], dt_of(a)));
-}
-
 // Elements per thread of the strided (x, y) passes: 8 for N <= SKG3_EM8_MAX
 // (twice the threads per line; the small grids have too few lines to fill
 // the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3

@@ -132,9 +132,9 @@ __global__ void energy_kernel(const cd* __restrict__ f, EnGeo g, int nvars, long
         const int il = ix[g.m.dims - 1];
         const double w = (il == 0 || il == g.m.nh - 1) ? 1.0 : 2.0;
         double ksq = 0.0;
-        for (int d = 0; d < g.m.dims; ++d) {
-            const int si = d == g.m.dims - 1 ? ix[d] : signed_index(ix[d], g.m.n[d]);
-            const double k = g.ks[d] * si;
+        for (int ax = 0; ax < g.m.dims; ++ax) {
+            const int si = ax == g.m.dims - 1 ? ix[ax] : signed_index(ix[ax], g.m.n[ax]);
+            const double k = g.ks[ax] * si;
             ksq += k * k;
         }
         for (int v = 0; v < nvars; ++v) {
