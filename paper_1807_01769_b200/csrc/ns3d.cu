@@ -89,6 +89,14 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 // the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3
 // 0.341 -> 0.222, 128^3 0.634 -> 0.630, 256^3 4.19 -> 4.06, 512^3 32.8 -> 36.4
 // (so 16 from 512 on).
+// z pass, dealiased states: the Hermitian split of the forward output from
+// registers (z_store_pair) instead of a shared-memory round trip of all
+// elements.  Measured (ms/step) with the zero band on: 512^3 32.55 vs 32.09
+// without it, 256^3 3.88 vs 3.95, 128^3 0.644 vs 0.632 -- off (512^3 is the
+// BASELINE grid); the zero band alone: 512^3 32.70 -> 32.09, 256^3 4.06 -> 3.95.
+#ifndef SKG3_Z_HERM
+#define SKG3_Z_HERM 0
+#endif
 #ifndef SKG3_EM8_MAX
 #define SKG3_EM8_MAX 256
 #endif
@@ -398,14 +406,27 @@ struct Z3 {
     static constexpr int SLOT = F::SMEM + 5 * NZ / 2;  // exchange + 5 rows of doubles (cd units)
 };
 
+// ZB: kz_in, kz_o <= 3 NZ / 8 (dealiased states), so the row elements
+// e in [3E/8, 5E/8) of every thread (|kz| in [3NZ/8, NZ/2]) are zero on input
+// and not needed on output.
+template <int NZ, bool ZB>
+struct ZBand {
+    static constexpr int E = Z3<NZ>::F::E;
+    static constexpr int LO = ZB ? 3 * E / 8 : E, HI = ZB ? 5 * E / 8 : E;
+};
+
 // Raw inputs of one packed c2r (fields P, Q of a row; kept kz only).
-template <int NZ>
+template <int NZ, bool ZB>
 __device__ __forceinline__ void fetch_pair(const Ns3dArgs& a, const cd* P, const cd* Q, size_t row,
                                            bool active, int t, cd* p, cd* q) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
+        if (e >= ZBand<NZ, ZB>::LO && e < ZBand<NZ, ZB>::HI) {
+            p[e] = q[e] = zero();
+            continue;
+        }
         const int idx = t + T * e;
         const int ki = idx > NZ / 2 ? NZ - idx : idx;
         p[e] = zero();
@@ -418,12 +439,16 @@ __device__ __forceinline__ void fetch_pair(const Ns3dArgs& a, const cd* P, const
 }
 
 // Hermitian-extended P + i Q (two c2r as one complex FFT).
-template <int NZ>
+template <int NZ, bool ZB>
 __device__ __forceinline__ void pack_pair(int t, const cd* p, const cd* q, cd* v) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
+        if (e >= ZBand<NZ, ZB>::LO && e < ZBand<NZ, ZB>::HI) {
+            v[e] = zero();
+            continue;
+        }
         const int idx = t + T * e;
         const bool mirror = idx > NZ / 2;
         const int ki = mirror ? NZ - idx : idx;
@@ -436,9 +461,53 @@ __device__ __forceinline__ void pack_pair(int t, const cd* p, const cd* q, cd* v
     }
 }
 
+// Separate the forward FFT Z = FT(a + i b) of two real rows into their
+// half spectra, x 1/N (h = 1/(2N)), kept kz < kz_o only.  ZB: output
+// k = t + T e (e < LO) pairs with NZ - k = (T - t) + T (E - 1 - e), element
+// E - 1 - e of thread T - t (thread 0: its own element E - e), so each thread
+// publishes its elements [HI, E) and reads its partner's.  Leaves sm free
+// (ends with a barrier).
+template <int NZ, bool ZB>
+__device__ __forceinline__ void z_store_pair(const Ns3dArgs& a, const cd* v, cd* sm, int t, int bar,
+                                             bool active, cd* o0, cd* o1, double h) {
+    using F = typename Z3<NZ>::F;
+    constexpr int T = F::T, E = F::E, LO = ZBand<NZ, ZB>::LO, HI = ZBand<NZ, ZB>::HI;
+    if constexpr (ZB && SKG3_Z_HERM) {
+        static_assert(LO + HI == E, "zero band symmetric about N/2");
+#pragma unroll
+        for (int e = HI; e < E; ++e) sm[(e - HI) * T + t] = v[e];
+        line_sync<T>(bar);
+        if (active) {
+            const int tp = t == 0 ? 0 : T - t;
+#pragma unroll
+            for (int e = 0; e < LO; ++e) {
+                const int k = t + T * e;
+                if (k >= a.kz_o) break;
+                const cd zk = v[e];
+                const cd zm = t == 0 ? (e == 0 ? v[0] : v[E - e]) : sm[(E - 1 - e - HI) * T + tp];
+                o0[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
+        line_sync<T>(bar);
+        if (active) {
+            for (int k = t; k < a.kz_o; k += T) {
+                const cd zk = sm[F::pad(k)];
+                const cd zm = sm[F::pad((NZ - k) & (NZ - 1))];
+                o0[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
+                o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+            }
+        }
+    }
+    line_sync<T>(bar);
+}
+
 // CFL: also reduce max |u_d| (adaptive dt, stage 1 only; a separate
 // instantiation so the common path carries no extra registers).
-template <int NZ, bool CFL>
+template <int NZ, bool CFL, bool ZB>
 __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E, G = Z3<NZ>::G;
@@ -471,8 +540,8 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
         const size_t row = (size_t)(r0 + rr) * a.kz_in;
         cd v[E];
         // w + i wx
-        fetch_pair<NZ>(a, FP[0], FQ[0], row, active, t, p, q);
-        pack_pair<NZ>(t, p, q, v);
+        fetch_pair<NZ, ZB>(a, FP[0], FQ[0], row, active, t, p, q);
+        pack_pair<NZ, ZB>(t, p, q, v);
         F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -480,8 +549,8 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[1 * NZ + t + T * e] = v[e].y;
         }
         // wy + i wz
-        fetch_pair<NZ>(a, FP[1], FQ[1], row, active, t, p, q);
-        pack_pair<NZ>(t, p, q, v);
+        fetch_pair<NZ, ZB>(a, FP[1], FQ[1], row, active, t, p, q);
+        pack_pair<NZ, ZB>(t, p, q, v);
         F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -489,8 +558,8 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[3 * NZ + t + T * e] = v[e].y;
         }
         // u + i v, then the cross product (solvers.cpp:321-325)
-        fetch_pair<NZ>(a, FP[2], FQ[2], row, active, t, p, q);
-        pack_pair<NZ>(t, p, q, v);
+        fetch_pair<NZ, ZB>(a, FP[2], FQ[2], row, active, t, p, q);
+        pack_pair<NZ, ZB>(t, p, q, v);
         F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -510,39 +579,16 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
             st[(rr == 0 ? 4 : 0) * NZ + y] = cz;  // row b reuses the dead w row
         }
         F::template run<-1>(v, sm, t, wb, 0, bar);
-#pragma unroll
-        for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
-        line_sync<T>(bar);
-        if (active) {
-            cd* o0 = a.A + (size_t)(r0 + rr) * a.kz_o;
-            cd* o1 = o0 + fs;
-            for (int k = t; k < a.kz_o; k += T) {
-                const cd zk = sm[F::pad(k)];
-                const cd zm = sm[F::pad((NZ - k) & (NZ - 1))];
-                o0[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-                o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
-            }
-        }
-        line_sync<T>(bar);
+        cd* o0 = a.A + (size_t)(r0 + rr) * a.kz_o;
+        z_store_pair<NZ, ZB>(a, v, sm, t, bar, active, o0, o0 + fs, h);
     }
     if constexpr (cfl) umax_accumulate(a.dyn, 3, mx, my, mz);
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = mk(st[4 * NZ + t + T * e], st[0 * NZ + t + T * e]);
     F::template run<-1>(v, sm, t, wb, 0, bar);
-#pragma unroll
-    for (int e = 0; e < E; ++e) sm[F::pad(t + T * e)] = v[e];
-    line_sync<T>(bar);
-    if (active) {
-        cd* oa = a.A + 2 * fs + (size_t)r0 * a.kz_o;
-        cd* ob = oa + a.kz_o;
-        for (int k = t; k < a.kz_o; k += T) {
-            const cd zk = sm[F::pad(k)];
-            const cd zm = sm[F::pad((NZ - k) & (NZ - 1))];
-            oa[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-            ob[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
-        }
-    }
+    cd* oa = a.A + 2 * fs + (size_t)r0 * a.kz_o;
+    z_store_pair<NZ, ZB>(a, v, sm, t, bar, active, oa, oa + a.kz_o, h);
 }
 
 // ------------------------------------------------------------------ y-forward
@@ -859,12 +905,25 @@ cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
     static size_t done_c = 0;
     const long long pairs = (long long)a.nrl * a.ny / 2;
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
-    if (a.dyn && a.ystage == 1) {
-        set_smem(k3_3d<NZ, true>, smem, done_c);
-        SKG_TRY(launch_pdl(k3_3d<NZ, true>, grid, Z::T * Z::G, smem, s, a));
+    // zero band (dealiased states): kept kz of both directions below 3 NZ / 8
+    const bool zb = NZ >= 16 && 8 * a.kz_in <= 3 * NZ && 8 * a.kz_o <= 3 * NZ;
+    if (zb) {
+        if constexpr (NZ >= 16) {
+            static size_t done_z = 0, done_zc = 0;
+            if (a.dyn && a.ystage == 1) {
+                set_smem(k3_3d<NZ, true, true>, smem, done_zc);
+                SKG_TRY(launch_pdl(k3_3d<NZ, true, true>, grid, Z::T * Z::G, smem, s, a));
+            } else {
+                set_smem(k3_3d<NZ, false, true>, smem, done_z);
+                SKG_TRY(launch_pdl(k3_3d<NZ, false, true>, grid, Z::T * Z::G, smem, s, a));
+            }
+        }
+    } else if (a.dyn && a.ystage == 1) {
+        set_smem(k3_3d<NZ, true, false>, smem, done_c);
+        SKG_TRY(launch_pdl(k3_3d<NZ, true, false>, grid, Z::T * Z::G, smem, s, a));
     } else {
-        set_smem(k3_3d<NZ, false>, smem, done);
-        SKG_TRY(launch_pdl(k3_3d<NZ, false>, grid, Z::T * Z::G, smem, s, a));
+        set_smem(k3_3d<NZ, false, false>, smem, done);
+        SKG_TRY(launch_pdl(k3_3d<NZ, false, false>, grid, Z::T * Z::G, smem, s, a));
     }
     return cudaGetLastError();
 }
