@@ -322,10 +322,12 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
 // vorticity outputs is read directly (recently read by this CTA: L2).
 // Output m: primary / secondary = A0 / -, A1 / -, A2 / -, A2 / A1, A4 / A0,
 // A3 / A0.
-template <int NY, int CT = 256>
+// ZB: kcy < 3 NY / 8, so the inputs e in [3E/8, 5E/8) are masked (zero)
+template <int NY, int CT = 256, bool ZB = false>
 __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) {
     using F = BF3<NY>;
     constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
+    constexpr int ZLO = ZB ? 3 * E / 8 : E, ZHI = ZB ? 5 * E / 8 : E;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_in + C - 1) / C;
@@ -365,6 +367,10 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
         cd v[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
+            if (e >= ZLO && e < ZHI) {
+                v[e] = zero();
+                continue;
+            }
             const int j = t + T * e;
             const int sj = signed_index(j, NY);
             cd r = zero();
@@ -592,10 +598,12 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
 }
 
 // ------------------------------------------------------------------ y-forward
-template <int NY, int CT = 256>
+// ZB: kcy < 3 NY / 8, so the outputs e in [3E/8, 5E/8) are masked (not stored)
+template <int NY, int CT = 256, bool ZB = false>
 __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) {
     using F = BF3<NY>;
     constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
+    constexpr int ZLO = ZB ? 3 * E / 8 : E, ZHI = ZB ? 5 * E / 8 : E;
     extern __shared__ cd smem[];
     const int l = threadIdx.x % C, t = threadIdx.x / C;
     const int nkzb = (a.kz_o + C - 1) / C;
@@ -624,6 +632,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
                              : a.B + m * a.fstride;  // D fields live in B's memory
 #pragma unroll
             for (int e = 0; e < E; ++e) {
+                if (e >= ZLO && e < ZHI) continue;
                 const int lo = loff[t + T * e];
                 if (lo >= 0 && abs(signed_index(t + T * e, NY)) <= a.kcy) {  // masked: never read
                     if (a.p2p) a.peer_D[lown[t + T * e]][m * a.dfs + (size_t)lo + kz] = v[e];
@@ -866,23 +875,36 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NY, CT>::C;
     using F = BF3<NY>;
     const size_t smem = sizeof(cd) * F::SMEM * C + 2 * sizeof(int) * NY;  // + line offsets, owners
+    const bool zb = NY >= 16 && 8 * a.kcy < 3 * NY;  // kept ky clear of the per-thread zero band
     if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
                               sizeof(int) * NY;
-        static size_t done = 0;
-        set_smem(k2s_3d<NY, CT>, smem_s, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
-        SKG_TRY(launch_pdl(k2s_3d<NY, CT>, grid, F::T * C, smem_s, s, a));
+        if (zb) {
+            static size_t done = 0;
+            set_smem(k2s_3d<NY, CT, true>, smem_s, done);
+            SKG_TRY(launch_pdl(k2s_3d<NY, CT, true>, grid, F::T * C, smem_s, s, a));
+        } else {
+            static size_t done = 0;
+            set_smem(k2s_3d<NY, CT, false>, smem_s, done);
+            SKG_TRY(launch_pdl(k2s_3d<NY, CT, false>, grid, F::T * C, smem_s, s, a));
+        }
     } else if (inverse) {
         static size_t done = 0;
         set_smem(k2_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
         SKG_TRY(launch_pdl(k2_3d<NY, CT>, grid, F::T * C, smem, s, a));
     } else {
-        static size_t done = 0;
-        set_smem(k2f_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_o + C - 1) / C);
-        SKG_TRY(launch_pdl(k2f_3d<NY, CT>, grid, F::T * C, smem, s, a));
+        if (zb) {
+            static size_t done = 0;
+            set_smem(k2f_3d<NY, CT, true>, smem, done);
+            SKG_TRY(launch_pdl(k2f_3d<NY, CT, true>, grid, F::T * C, smem, s, a));
+        } else {
+            static size_t done = 0;
+            set_smem(k2f_3d<NY, CT, false>, smem, done);
+            SKG_TRY(launch_pdl(k2f_3d<NY, CT, false>, grid, F::T * C, smem, s, a));
+        }
     }
     return cudaGetLastError();
 }
