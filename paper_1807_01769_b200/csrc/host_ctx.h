@@ -191,6 +191,7 @@ struct skg_ctx {
     double g_dt = 0.0;
     long g_launches = 0;
     bool g_pruned = false;
+    bool g_p2p = false;  // exchange mode the graph was captured with
     cudaStream_t g_stream = nullptr;
 };
 

@@ -382,7 +382,7 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     // middle steps: replay of a captured step; the last step eagerly
     if (nsteps - s >= 3 && !c->timing && c->stream != nullptr) {
         if (c->gexec && (c->g_dt != dt || c->g_pruned != c->pruned || c->g_stream != c->stream ||
-                         c->g_diag != c->diag)) {
+                         c->g_diag != c->diag || c->g_p2p != c->p2p)) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
         }
@@ -400,6 +400,7 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
             c->g_dt = dt;
             c->g_diag = c->diag;
             c->g_pruned = c->pruned;
+            c->g_p2p = c->p2p;
             c->g_stream = c->stream;
         }
         for (; s < nsteps - 1; ++s) {

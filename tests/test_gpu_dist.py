@@ -207,3 +207,24 @@ def test_slab3d_peer_exchange_matches(n, world):
     b.set_state(u0)
     b.step(3)
     assert np.array_equal(a.get_state(), b.get_state())
+
+
+@pytest.mark.gpu
+def test_exchange_mode_switch_between_calls():
+    """Toggling the peer exchange between skg_step calls re-captures the
+    per-step CUDA graph (its key includes the exchange mode): the trajectory
+    equals the copy-path one step for step."""
+    n, world = (256, 256), 4
+    u0 = ic.ns2d_ic(n, seed=5)
+    dt = ic.cfl_dt("ns2d", n, u0)
+    a = api.Simulation("ns2d", n, 1e-4, dt, world=world)
+    a.set_state(u0)
+    a.step(15)
+    b = api.Simulation("ns2d", n, 1e-4, dt, world=world)
+    b.set_state(u0)
+    b.step(5)
+    b.enable_p2p()
+    b.step(5)
+    b.disable_p2p()
+    b.step(5)
+    assert np.array_equal(a.get_state(), b.get_state())
