@@ -358,9 +358,15 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
         }
         cp_async_commit();
     };
+    // Processing order 0, 5, 4, 1, 3, 2: each secondary field (A0 for
+    // outputs 5 and 4, A1 for 3) was this CTA's previous primary (still in
+    // L2), and outputs 3 and 2 share the primary A2, staged once.
+    auto order = [](int i) { return i == 0 ? 0 : i == 1 ? 5 : i == 2 ? 4 : i == 3 ? 1 : i == 4 ? 3 : 2; };
+    auto primary = [](int m) { return m == 3 ? 2 : m == 4 ? 4 : m == 5 ? 3 : m; };
     issue(0);
 #pragma unroll 1
-    for (int m = 0; m < 6; ++m) {
+    for (int i = 0; i < 6; ++i) {
+        const int m = order(i);
         cp_async_wait_all();
         __syncthreads();
         const cd* sec = Ab + (size_t)(m == 3 ? 1 : 0) * afs;
@@ -389,8 +395,10 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
             }
             v[e] = r;
         }
-        __syncthreads();  // stage consumed
-        if (m < 5) issue(m == 2 ? 2 : m == 3 ? 4 : m == 4 ? 3 : m + 1);  // primary of m + 1
+        if (i < 5 && primary(order(i + 1)) != primary(m)) {
+            __syncthreads();  // stage consumed
+            issue(primary(order(i + 1)));
+        }
         F::template run<+1>(v, sm, t, wb, salt);
         if (active) {
             cd* out = a.B + m * a.fstride;
