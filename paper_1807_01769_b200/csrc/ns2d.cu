@@ -30,6 +30,9 @@
 #ifndef SKG_FAST_Y_EM_SMALL
 #define SKG_FAST_Y_EM_SMALL 8
 #endif
+#ifndef SKG_Y8_MINB
+#define SKG_Y8_MINB 2
+#endif
 #ifndef SKG_FAST_Y_EM
 #define SKG_FAST_Y_EM 16
 #endif
@@ -470,9 +473,16 @@ __global__ void k4_decay(Ns2dArgs a) {
 
 // y pass, one row per group iteration, persistent over rows; the next row's
 // two input lines stream into shared memory (cp.async) during the FFTs.
+// Resident CTAs per SM of the fast y pass (256-thread CTAs): 2 with
+// 16-element rows (128 registers); SKG_Y8_MINB with 8-element rows -- 3 or 4
+// (85 / 64 registers, one wave of rows at 1024^2) spill and measured slower
+// (1024^2: 0.147 / 0.140 vs 0.117 ms/step), so 2.
+template <int NY, int EM>
+constexpr int y_minb() { return BFFT<NY, false, EM>::T > 256 ? 1 : EM == 16 ? 2 : SKG_Y8_MINB; }
+
 template <int NY, bool CFL, int EM = 16>
 __global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false, EM>::T : 256,
-                                  BFFT<NY, false, EM>::T > 256 ? 1 : 2)
+                                  y_minb<NY, EM>())
     k3b_phys(Ns2dArgs a) {
     using F = BFFT<NY, false, EM>;
     constexpr int T = F::T, E = F::E;
@@ -882,7 +892,8 @@ cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
         init = smem;
     }
     const int groups = (a.nrl + G - 1) / G;
-    const int grid = groups < a.wave ? groups : a.wave;
+    const int wave = a.wave / 2 * y_minb<NY, EM>();  // a.wave = 2 CTAs per SM
+    const int grid = groups < wave ? groups : wave;
     SKG_TRY(launch_pdl(k3b_phys<NY, CFL, EM>, grid, F::T * G, smem, s, a));
     return cudaGetLastError();
 }
