@@ -360,12 +360,15 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
     };
     // Processing order 0, 5, 4, 1, 3, 2: each secondary field (A0 for
     // outputs 5 and 4, A1 for 3) was this CTA's previous primary (still in
-    // L2), and outputs 3 and 2 share the primary A2, staged once.
+    // L2), and outputs 3 and 2 share the primary A2, staged once.  With
+    // gridDim.y == 2 the two halves {0, 5, 4} and {1, 3, 2} (each closed
+    // under its secondary) run in separate CTAs.
     auto order = [](int i) { return i == 0 ? 0 : i == 1 ? 5 : i == 2 ? 4 : i == 3 ? 1 : i == 4 ? 3 : 2; };
     auto primary = [](int m) { return m == 3 ? 2 : m == 4 ? 4 : m == 5 ? 3 : m; };
-    issue(0);
+    const int i0 = gridDim.y == 2 ? 3 * blockIdx.y : 0, i1 = gridDim.y == 2 ? i0 + 3 : 6;
+    issue(primary(order(i0)));
 #pragma unroll 1
-    for (int i = 0; i < 6; ++i) {
+    for (int i = i0; i < i1; ++i) {
         const int m = order(i);
         cp_async_wait_all();
         __syncthreads();
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
             }
             v[e] = r;
         }
-        if (i < 5 && primary(order(i + 1)) != primary(m)) {
+        if (i + 1 < i1 && primary(order(i + 1)) != primary(m)) {
             __syncthreads();  // stage consumed
             issue(primary(order(i + 1)));
         }
@@ -887,7 +890,9 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
                               sizeof(int) * NY;
-        const int grid = a.nrl * ((a.kz_in + C - 1) / C);
+        // the two output halves in separate CTAs (ms/step: 64^3 0.218 -> 0.202,
+        // 128^3 0.621 -> 0.600, 512^3 31.27 -> 31.20, 256^3 3.868 -> 3.888)
+        const dim3 grid(a.nrl * ((a.kz_in + C - 1) / C), 2);
         if (zb) {
             static size_t done = 0;
             set_smem(k2s_3d<NY, CT, true>, smem_s, done);
