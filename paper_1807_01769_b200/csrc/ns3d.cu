@@ -94,6 +94,11 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 // elements.  Measured (ms/step) with the zero band on: 512^3 32.55 vs 32.09
 // without it, 256^3 3.88 vs 3.95, 128^3 0.644 vs 0.632 -- off (512^3 is the
 // BASELINE grid); the zero band alone: 512^3 32.70 -> 32.09, 256^3 4.06 -> 3.95.
+// x-inverse and y-forward: one component / field per CTA (gridDim.y = 3)
+// instead of three in sequence -- shorter dependent chains per CTA (ms/step:
+// 64^3 0.201 -> 0.184, 128^3 0.601 -> 0.588, 512^3 31.10 -> 30.94,
+// 256^3 3.889 -> 3.914).
+constexpr int kSplit3 = 3;
 #ifndef SKG3_Z_HERM
 #define SKG3_Z_HERM 0
 #endif
@@ -134,7 +139,8 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
     const bool active = kz < a.kz_in;
     pdl_wait();
     if (a.flags->diverged) return;
-    if (stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
+    if (stage == 1 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.lead)
+        atomicAdd(&a.flags->steps, 1);
     const int ky = ky_of(a, kyi);
     const int ys = a.slab ? kyi - a.kys : ky;
     cd* sm = smem + l * F::SMEM;
@@ -143,8 +149,10 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twx);
     const cd* kprev = stage == 2 ? a.k1 : stage == 3 ? a.k2 : a.k3;
+    // gridDim.y == 3: one velocity component per CTA
+    const int c0 = gridDim.y == 3 ? blockIdx.y : 0, c1 = gridDim.y == 3 ? c0 + 1 : 3;
 #pragma unroll 1
-    for (int c = 0; c < 3; ++c) {
+    for (int c = c0; c < c1; ++c) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             if (e >= ZLO && e < ZHI) continue;
@@ -630,8 +638,10 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
     int* lown = loff + NY;
     if (a.p2p) line_offsets_p2p<NY>(a, x, a.kz_o, loff, lown);
     else line_offsets<NY>(a, x, a.kz_o, loff);
+    // gridDim.y == 3: one field per CTA
+    const int m0 = gridDim.y == 3 ? blockIdx.y : 0, m1 = gridDim.y == 3 ? m0 + 1 : 3;
 #pragma unroll 1
-    for (int m = 0; m < 3; ++m) {
+    for (int m = m0; m < m1; ++m) {
         const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
         cd v[E];
 #pragma unroll
@@ -834,7 +844,7 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
     constexpr int C = Strided<NX, CT>::C;
     using F = BF3<NX>;
     if (inverse) {
-        const int grid = a.nkyl * ((a.kz_in + C - 1) / C);
+        const dim3 grid(a.nkyl * ((a.kz_in + C - 1) / C), kSplit3);
         const bool pz = NX >= 64 && a.pruned && a.kcx <= 3 * F::E / 8 * F::T - 1;
         if (pz) {
             if constexpr (NX >= 64) {
@@ -908,7 +918,7 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
         SKG_TRY(launch_pdl(k2_3d<NY, CT>, grid, F::T * C, smem, s, a));
     } else {
-        const int grid = a.nrl * ((a.kz_o + C - 1) / C);
+        const dim3 grid(a.nrl * ((a.kz_o + C - 1) / C), kSplit3);
         if (zb) {
             static size_t done = 0;
             set_smem(k2f_3d<NY, CT, true>, smem, done);
