@@ -84,24 +84,26 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
     return ky <= a.kcy ? ky : ky - (a.ny - (2 * a.kcy + 1));
 }
 
-// Elements per thread of the strided (x, y) passes: 8 for N <= SKG3_EM8_MAX
-// (twice the threads per line; the small grids have too few lines to fill
-// the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3
-// 0.341 -> 0.222, 128^3 0.634 -> 0.630, 256^3 4.19 -> 4.06, 512^3 32.8 -> 36.4
-// (so 16 from 512 on).
-// z pass, dealiased states: the Hermitian split of the forward output from
-// registers (z_store_pair) instead of a shared-memory round trip of all
-// elements.  Measured (ms/step) with the zero band on: 512^3 32.55 vs 32.09
-// without it, 256^3 3.88 vs 3.95, 128^3 0.644 vs 0.632 -- off (512^3 is the
-// BASELINE grid); the zero band alone: 512^3 32.70 -> 32.09, 256^3 4.06 -> 3.95.
 // x-inverse and y-forward: one component / field per CTA (gridDim.y = 3)
 // instead of three in sequence -- shorter dependent chains per CTA (ms/step:
 // 64^3 0.201 -> 0.184, 128^3 0.601 -> 0.588, 512^3 31.10 -> 30.94,
 // 256^3 3.889 -> 3.914).
 constexpr int kSplit3 = 3;
+
+// z pass, dealiased states: the Hermitian split of the forward output from
+// registers (z_store_pair) instead of a shared-memory round trip of all
+// elements.  Measured (ms/step) with the zero band on: 512^3 32.55 vs 32.09
+// without it, 256^3 3.88 vs 3.95, 128^3 0.644 vs 0.632 -- off (512^3 is the
+// BASELINE grid); the zero band alone: 512^3 32.70 -> 32.09, 256^3 4.06 -> 3.95.
 #ifndef SKG3_Z_HERM
 #define SKG3_Z_HERM 0
 #endif
+
+// Elements per thread of the strided (x, y) passes: 8 for N <= SKG3_EM8_MAX
+// (twice the threads per line; the small grids have too few lines to fill
+// the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3
+// 0.341 -> 0.222, 128^3 0.634 -> 0.630, 256^3 4.19 -> 4.06, 512^3 32.8 -> 36.4
+// (so 16 from 512 on).
 #ifndef SKG3_EM8_MAX
 #define SKG3_EM8_MAX 256
 #endif
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
 // index) while the current FFT runs; the secondary field of the three
 // vorticity outputs is read directly (recently read by this CTA: L2).
 // Output m: primary / secondary = A0 / -, A1 / -, A2 / -, A2 / A1, A4 / A0,
-// A3 / A0.
+// A3 / A0 (processed as two halves, see the order below).
 // ZB: kcy < 3 NY / 8, so the inputs e in [3E/8, 5E/8) are masked (zero)
 template <int NY, int CT = 256, bool ZB = false>
 __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) {
