@@ -104,6 +104,13 @@ constexpr int kSplit3 = 3;
 // the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3
 // 0.341 -> 0.222, 128^3 0.634 -> 0.630, 256^3 4.19 -> 4.06, 512^3 32.8 -> 36.4
 // (so 16 from 512 on).
+// z pass at NZ = 128: 14 row-pair groups per CTA (224 threads) instead of
+// 16: two CTAs per SM then hold 148 * 28 = 4144 groups, and the 8192 row
+// pairs of 128^3 take 1.98 waves instead of 1.73 (a 73%-full second wave).
+// 128^3: 0.584 -> 0.568 ms/step (10 groups: 0.604, 8: 0.597).
+#ifndef SKG3_ZG128
+#define SKG3_ZG128 14
+#endif
 #ifndef SKG3_EM8_MAX
 #define SKG3_EM8_MAX 256
 #endif
@@ -429,7 +436,7 @@ template <int NZ>
 struct Z3 {
     using F = BFFT<NZ, false, 8>;
     static constexpr int T = F::T;
-    static constexpr int G = T >= 256 ? 1 : 256 / T;
+    static constexpr int G = NZ == 128 ? SKG3_ZG128 : T >= 256 ? 1 : 256 / T;
     static constexpr int SLOT = F::SMEM + 5 * NZ / 2;  // exchange + 5 rows of doubles (cd units)
 };
 
