@@ -139,7 +139,9 @@ struct XCfg {
     static constexpr int T = F::T;
     static constexpr int LPC = T >= CTW ? 1 : CTW / T;
     static constexpr int CT = T * LPC;
-    static constexpr int MINB = CT >= 256 ? 2 : (512 / CT > 32 ? 32 : 512 / CT);  // keeps <= 128 registers
+    // resident CTAs the register budget is sized for: <= 128 registers per
+    // thread (512-thread lines of 8192: one CTA, its shared memory is ~224 KB)
+    static constexpr int MINB = CT >= 512 ? 1 : CT >= 256 ? 2 : (512 / CT > 32 ? 32 : 512 / CT);
     static constexpr int ZLO = EM == 16 ? 6 : 3, ZHI = EM == 16 ? 10 : 5;
 };
 
