@@ -7,8 +7,13 @@
 A "step" is one RK4 time step (Simulation::step_once, reference
 proj/src/simulation.cpp:535-555) of the BASELINE config on synthetic seeded
 input (paper_1807_01769_b200/ic.py), state resident in HBM.  Default workload:
-BASELINE.json configs[1], ns2d 4096^2, nu 1e-4, dt from CFL 0.5 on the IC
-(the largest single-GPU config the metric is quoted on).
+BASELINE.json configs[3], ns3d 512^3, nu 2e-4, dt from CFL 0.5 on the IC --
+the largest BASELINE config that fits one GPU in the reference layout and the
+one the north-star target (>= 60% of the HBM roofline on 1 B200) names.
+
+--gpus N: one process per GPU.  Under torchrun (WORLD_SIZE set) the ranks
+come from the environment and must number N; without it, bench.py relaunches
+itself through torch.distributed.run with N processes (127.0.0.1 rendezvous).
 
 Our arm: W untimed steps, then K steps timed with CUDA events on the launch
 stream (bracketed by barrier + synchronize, max over ranks), per-kernel-class
@@ -21,7 +26,8 @@ skg_get_state (D2H).  `cpu_baseline` times the reference's own CPU step
 sample on this host.
 
 --impl reference: the reference CPU implementation alone (rank 0), same
-config/metric, K steps after W warm-up steps.
+config/metric: one untimed warm-up step (the reference's own bench protocol,
+proj/src/bench.cpp:79-82), then up to K step_once calls within a time budget.
 """
 from __future__ import annotations
 
@@ -60,6 +66,40 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# 1-thread CPU row: a grid of the same solver whose single-threaded step takes
+# seconds (the BASELINE configs' own single-thread steps take minutes at 512^3)
+SINGLE_THREAD_CFG = {"ns2d": "ns2d_1024", "ns3d": "ns3d_128"}
+
+
+def single_thread_row(solver):
+    """The reference step on ONE host thread (the 1-thread
+    row), on the small config of the same solver, as Gpts*steps/s."""
+    from oracle import ref
+    cfg = SINGLE_THREAD_CFG[solver]
+    _, n, nu, dt, u0 = make_input(cfg)
+    ref.set_workers(1)
+    r = ref.RefSimulation(solver, n, nu, dt)
+    r.set_state(u0)
+    r.step(1)  # warm-up (plans)
+    times = []
+    while len(times) < 3 and sum(times) < 20.0:
+        times.append(r.step(1))
+    r.close()
+    sec = sum(times) / len(times)
+    return {"value": int(np.prod(n)) / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{len(times)} step_once of {cfg} on 1 thread after 1 warm-up ({sec:.3f} s/step)"}
 
 
 def load_peaks():
@@ -171,8 +211,12 @@ def cpu_reference_rate(solver, n, nu, dt, u0, steps, warmup, threads):
         times.append(r.step(1))
     if not times:
         times.append(t_warm)  # the warm-up step itself is the sample
+    # Simulation::run() per iteration: the step plus the per-step means
+    # (E, Z, eps) and check_finite the reference writes every step
+    # (simulation.cpp:565-590, output.cpp:204-214) -- one iteration
+    t_run = r.run(1)
     r.close()
-    return times
+    return times, t_run
 
 
 def run_reference_arm(args):
@@ -191,11 +235,10 @@ def run_reference_arm(args):
     ref.set_workers(threads)
     r = ref.RefSimulation(solver, n, nu, dt)
     r.set_state(u0)
-    # W untimed warm-up steps (the reference's own bench protocol uses one,
+    # one untimed warm-up step (the reference's own bench protocol,
     # proj/src/bench.cpp:79-82); then up to K steps within a time budget so
     # the run stays within a few minutes (each step is a full step_once).
-    for _ in range(max(1, args.warmup)):
-        t_warm = r.step(1)
+    t_warm = r.step(1)
     budget = args.ref_budget_s
     times = []
     while len(times) < args.steps and (sum(times) + (times[-1] if times else t_warm)) <= budget:
@@ -207,15 +250,16 @@ def run_reference_arm(args):
     value = P / sec / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": len(times),
-        "requested_steps": args.steps, "warmup": max(1, args.warmup), "ms_per_step": sec * 1e3,
+        "requested_steps": args.steps, "warmup": 1, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded spectral Gaussian IC, BASELINE recipe)", "impl": "reference",
         "config": {"workload": f"{args.config} RK4 step (step_once), nu={nu}, dt={dt:.6g}",
                    "solver": solver, "n": list(n), "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{len(times)} step_once calls of {args.config} after "
-                                   f"{max(1, args.warmup)} warm-up (budget {budget:.0f} s); reference proj/src compiled "
-                                   f"unmodified, FFT = oracle/fft_shim.c (not FFTW)"},
+                                   f"1 warm-up (budget {budget:.0f} s); reference proj/src compiled "
+                                   f"unmodified, FFT = oracle/fft_shim.c (batched Stockham, not FFTW)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -386,12 +430,20 @@ def run_our_arm(args):
     elif ws == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            times = cpu_reference_rate(solver, n, nu, dt, u0, args.cpu_steps, 1, threads)
+            times, t_run = cpu_reference_rate(solver, n, nu, dt, u0, args.cpu_steps, 1, threads)
             sec = sum(times) / len(times)
             cpu = {"value": P / sec / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "cpu_model": cpu_model(),
                    "sample": f"{len(times)} step_once of {args.config} after 1 warm-up "
                              f"({sec:.2f} s/step); reference proj/src compiled unmodified, "
-                             f"FFT = oracle/fft_shim.c (FFTW absent), {threads} threads"}
+                             f"FFT = oracle/fft_shim.c (batched Stockham; FFTW absent), {threads} threads",
+                   "run_s_per_iter": t_run,
+                   "run_note": "Simulation::run() per iteration (step + per-step E/Z/eps means + "
+                               "check_finite, simulation.cpp:565-590), one iteration"}
+            try:
+                cpu["single_thread"] = single_thread_row(solver)
+            except Exception as exc:
+                cpu["single_thread"] = {"value": None, "sample": f"unavailable: {exc}"}
         except Exception as exc:  # the oracle .so may be missing on a foreign box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -446,11 +498,11 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="ns2d_4096")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="ns3d_512")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--ref-budget-s", type=float, default=120.0)
     ap.add_argument("--instrumented-steps", type=int, default=20)
     ap.add_argument("--no-p2p", action="store_true",
                     help="slab under torchrun: NCCL all-to-all copies instead of the peer-memory "
@@ -460,6 +512,21 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: relaunch through torchrun (127.0.0.1 rendezvous)
+        import socket
+        import subprocess
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+        return subprocess.call(cmd)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_our_arm(args)

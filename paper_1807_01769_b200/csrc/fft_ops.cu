@@ -295,14 +295,8 @@ cudaError_t launch_blue_m(const BlueTab& tb, int si, cd* data, long long lines, 
                           int mode, const double* ur, double* uo, cudaStream_t s) {
     using F = BFFT<M>;
     const size_t smem = sizeof(cd) * F::SMEM;
-    static bool init[2] = {false, false};
-    if (!init[si]) {
-        if (si == 0)
-            cudaFuncSetAttribute(bluestein_line<M, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        else
-            cudaFuncSetAttribute(bluestein_line<M, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init[si] = true;
-    }
+    SKG_TRY(si == 0 ? ensure_smem(reinterpret_cast<const void*>(bluestein_line<M, -1>), smem)
+                    : ensure_smem(reinterpret_cast<const void*>(bluestein_line<M, 1>), smem));
     if (si == 0)
         bluestein_line<M, -1><<<(unsigned)lines, F::T, smem, s>>>(data, inner, n, mode, ur, uo,
                                                                   tb.chirp[0], tb.bhat[0], tb.twm);
@@ -339,11 +333,7 @@ cudaError_t launch_c2c(cd* data, long long outer, long long inner, const cd* tw,
     using F = BFFT<N>;
     constexpr int LPC = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * F::SMEM * LPC;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(c2c_axis_tw<N, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = true;
-    }
+    SKG_TRY(ensure_smem(reinterpret_cast<const void*>(c2c_axis_tw<N, S>), smem));
     const long long lines = outer * inner;
     c2c_axis_tw<N, S><<<(unsigned)((lines + LPC - 1) / LPC), F::T * LPC, smem, s>>>(data, outer, inner, tw);
     return cudaGetLastError();
@@ -354,11 +344,7 @@ cudaError_t launch_r2c(const double* u, cd* out, long long rows, const cd* tw, c
     using F = BFFT<N>;
     constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * F::SMEM * G;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(r2c_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = true;
-    }
+    SKG_TRY(ensure_smem(reinterpret_cast<const void*>(r2c_rows<N>), smem));
     const long long pairs = (rows + 1) / 2;
     r2c_rows<N><<<(unsigned)((pairs + G - 1) / G), F::T * G, smem, s>>>(u, out, rows, tw);
     return cudaGetLastError();
@@ -369,11 +355,7 @@ cudaError_t launch_c2r(const cd* in, double* u, long long rows, const cd* tw, cu
     using F = BFFT<N>;
     constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * F::SMEM * G;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(c2r_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = true;
-    }
+    SKG_TRY(ensure_smem(reinterpret_cast<const void*>(c2r_rows<N>), smem));
     const long long pairs = (rows + 1) / 2;
     c2r_rows<N><<<(unsigned)((pairs + G - 1) / G), F::T * G, smem, s>>>(in, u, rows, tw);
     return cudaGetLastError();
@@ -392,6 +374,7 @@ cudaError_t c2c(cd* data, long long outer, int n, long long inner, int sign, con
             const long long lines = outer * inner;
             cudaError_t e = cudaSuccess;
             if (bluestein(n, sign, data, lines, inner, 0, nullptr, nullptr, s, &e)) return e;
+            SKG_TRY(ensure_smem(reinterpret_cast<const void*>(dft_axis_generic), sizeof(cd) * n));
             dft_axis_generic<<<(unsigned)lines, 128, sizeof(cd) * n, s>>>(data, outer, n, inner, sign, tw);
             return cudaGetLastError();
         }
@@ -407,6 +390,7 @@ cudaError_t r2c(const double* u, cd* out, long long rows, int n, const cd* tw, c
         default: {
             cudaError_t e = cudaSuccess;
             if (bluestein(n, -1, out, rows, 1, 1, u, nullptr, s, &e)) return e;
+            SKG_TRY(ensure_smem(reinterpret_cast<const void*>(dft_r2c_generic), sizeof(double) * n));
             dft_r2c_generic<<<(unsigned)rows, 128, sizeof(double) * n, s>>>(u, out, n, tw);
             return cudaGetLastError();
         }
@@ -422,6 +406,7 @@ cudaError_t c2r(const cd* in, double* u, long long rows, int n, const cd* tw, cu
         default: {
             cudaError_t e = cudaSuccess;
             if (bluestein(n, 1, const_cast<cd*>(in), rows, 1, 2, nullptr, u, s, &e)) return e;
+            SKG_TRY(ensure_smem(reinterpret_cast<const void*>(dft_c2r_generic), sizeof(cd) * (n / 2 + 1)));
             dft_c2r_generic<<<(unsigned)rows, 128, sizeof(cd) * (n / 2 + 1), s>>>(in, u, n, tw);
             return cudaGetLastError();
         }

@@ -147,7 +147,8 @@ struct XCfg {
 
 template <int NX, bool PZ, int NM, int EM = 16, int CTW = 256>
 __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
-                                  (PZ || EM == 8) ? XCfg<NX, EM, CTW>::MINB : XCfg<NX, EM, CTW>::MINB / 2)
+                                  (PZ || EM == 8 || XCfg<NX, EM, CTW>::MINB < 2) ? XCfg<NX, EM, CTW>::MINB
+                                                                       : XCfg<NX, EM, CTW>::MINB / 2)
     k1_xinv(Ns2dArgs a, int stage) {
     using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
     const int ky = (NM == 2 ? a.c0 : 0) + kyl;
     const bool active = kyl < (NM == 2 ? a.ncols : a.ky_in);
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     // step counter: here on the general path, in the stage-1 y pass on the
     // fast path (whose x-inverse usually runs fused into the previous step)
     if (NM == 4 && stage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead)
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(BFFT<NY, true, EM>::T >= 256 ? BFFT<NY, true, 
     const int xa = 2 * (blockIdx.x * G + g);
     const bool active = xa < a.nx;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     cd* sm = smem + g * slot;
     double* prow = reinterpret_cast<double*>(sm + F::SMEM);
     cd* st = sm + F::SMEM + NY / 2;
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(BFFT<NX>::T > 256 ? BFFT<NX>::T : 256, BFFT<NX
     const int ky = blockIdx.x * LPC + l;
     const bool active = ky < a.ld_o;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     cd* sm = smem + l * F::SMEM;
     cd v[E];
 #pragma unroll
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(BFFT<NX>::T > 256 ? BFFT<NX>::T : 256, BFFT<NX
 // there, so u <- E2 u (time_stepping.cpp:186-192 with k = 0).
 __global__ void k4_decay(Ns2dArgs a) {
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     const size_t cols = (size_t)(a.nh - (a.kcy + 1));
     const size_t total = cols * a.nx;
     bool bad = false;
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false,
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const int bar = G > 1 ? g + 1 : 0;  // the groups' own barriers (line_sync)
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     if (a.ystage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     cd* sm = smem + g * slot;
     cd* st = sm + F::SMEM;
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
     const int ky = a.c0 + kyl;
     const bool active = kyl < a.ncols;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     cd* sm = smem + l * (F::SMEM + NS * T);
     cd* sv = sm + F::SMEM;
     const typename F::Bases wb = F::bases(t, a.twx);
@@ -827,11 +828,6 @@ cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
     const size_t smem = sizeof(cd) * (F::SMEM + NS * T) * LPC;
     const int grid = ((NM == 2 ? a.ncols : a.ky_in) + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(k1_xinv<NX, PZ, NM, EM, CTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = true;
-    }
     SKG_TRY(launch_pdl(k1_xinv<NX, PZ, NM, EM, CTW>, grid, T * LPC, smem, s, a, stage));
     return cudaGetLastError();
 }
@@ -850,11 +846,6 @@ cudaError_t launch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s)
     const size_t smem = sizeof(cd) * F::SMEM * LPC;
     const int grid = (a.ld_o + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(k4_xfwd<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = true;
-    }
     SKG_TRY(launch_pdl(k4_xfwd<NX>, grid, T * LPC, smem, s, a, stage));
     return cudaGetLastError();
 }
@@ -868,11 +859,6 @@ cudaError_t launch_y_v(const Ns2dArgs& a, cudaStream_t s) {
     const size_t smem = sizeof(cd) * (F::SMEM + NY / 2 + 2 * a.ld_i) * G;
     const int pairs = a.nx / 2;
     const int grid = (pairs + G - 1) / G;
-    static size_t init = 0;
-    if (init < smem) {
-        cudaFuncSetAttribute(k3_phys<NY, EM, CFL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = smem;
-    }
     SKG_TRY(launch_pdl(k3_phys<NY, EM, CFL>, grid, T * G, smem, s, a));
     return cudaGetLastError();
 }
@@ -888,11 +874,6 @@ cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
     using F = BFFT<NY, false, EM>;
     constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * (F::SMEM + 2 * a.ld_i) * G;
-    static size_t init = 0;
-    if (init < smem) {
-        cudaFuncSetAttribute(k3b_phys<NY, CFL, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        init = smem;
-    }
     const int groups = (a.nrl + G - 1) / G;
     const int wave = a.wave / 2 * y_minb<NY, EM>();  // a.wave = 2 CTAs per SM
     const int grid = groups < wave ? groups : wave;
@@ -919,12 +900,6 @@ cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     constexpr int T = F::T;
     constexpr int LPC = C::LPC;
     const size_t smem = sizeof(cd) * (F::SMEM + (F::E - (C::ZHI - C::ZLO)) * T) * LPC;
-    static bool init = false;
-    if (!init) {
-        cudaFuncSetAttribute(k4b_xfwd<NX, EM, CTW, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        init = true;
-    }
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
     SKG_TRY(launch_pdl(k4b_xfwd<NX, EM, CTW, FUSE>, grid, T * LPC, smem, s,
@@ -952,8 +927,8 @@ cudaError_t launch_fast_x(const Ns2dArgs& a, int stage, int mode, cudaStream_t s
     return launch_fast_x_w<NX, 256>(a, stage, mode, s);
 }
 
-#define SKG_POW2_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
-#define SKG_FAST_CASES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
+#define SKG_POW2_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+#define SKG_FAST_CASES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
 
 cudaError_t dispatch_x(const Ns2dArgs& a, int stage, bool inverse, cudaStream_t s) {
     switch (a.nx) {
@@ -1007,8 +982,11 @@ bool fast_ok(const Ns2dArgs& a) {
 
 }  // namespace
 
+// The general (non-dealiased) passes hold a whole line plus its stage in
+// shared memory: 4096 is the largest extent that fits 227 KB for every
+// state, so larger grids run the generic step (generic.cu) instead.
 bool ns2d_supported(int nx, int ny) {
-    auto ok = [](int n) { return n >= 4 && n <= 8192 && (n & (n - 1)) == 0; };
+    auto ok = [](int n) { return n >= 4 && n <= 4096 && (n & (n - 1)) == 0; };
     return ok(nx) && ok(ny);
 }
 

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_in;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     if (stage == 1 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && a.lead)
         atomicAdd(&a.flags->steps, 1);
     const int ky = ky_of(a, kyi);
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_in;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
     const int kz = kz0 + l;
     const bool active = kz < a.kz_in;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     const int K = 2 * a.kcy + 1;  // kept lines
     cd* sm = smem + l * F::SMEM;
     cd* stg = smem + C * F::SMEM;                       // [kyi][l]
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     const long long r0 = 2ll * ((long long)blockIdx.x * G + g);
     const bool active = r0 < (long long)a.nrl * a.ny;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     cd* sm = smem + g * Z3<NZ>::SLOT;
     const int bar = G > 1 ? g + 1 : 0;  // the groups' own barriers (line_sync)
     double* st = reinterpret_cast<double*>(sm + F::SMEM);  // w, wx, wy, wz, cz_a rows
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_o;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     const int kz = (blockIdx.x % nkzb) * C + l;
     const bool active = kz < a.kz_o;
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     const int ky = ky_of(a, kyi);
     const int ys = a.slab ? kyi - a.kys : ky;
     const int sky = signed_index(ky, a.ny);
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
 // Unpruned final update of the kz planes above the cut (tendency zero there).
 __global__ void k4_3d_decay(Ns3dArgs a) {
     pdl_wait();
-    if (a.flags->diverged) return;
+    if (cta_diverged(a.flags)) return;
     const int nk = a.nh - a.kz_o;
     const size_t total = (size_t)a.nx * a.ny * nk;
     int bad = 3;
@@ -840,14 +840,6 @@ __global__ void k4_3d_decay(Ns3dArgs a) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <typename K>
-void set_smem(K kernel, size_t bytes, size_t& done) {
-    if (done < bytes) {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        done = bytes;
-    }
-}
-
 template <int NX, int CT>
 cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NX, CT>::C;
@@ -858,15 +850,11 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
         if (pz) {
             if constexpr (NX >= 64) {
                 const size_t smem = sizeof(cd) * (F::SMEM * C + (F::E - F::E / 4) * F::T * C);
-                static size_t done = 0;
-                set_smem(k1_3d<NX, true, CT>, smem, done);
                 SKG_TRY(launch_pdl(k1_3d<NX, true, CT>, grid, F::T * C, smem, s, a, stage));
             }
         } else {
             if constexpr (CT == 256) {
                 const size_t smem = sizeof(cd) * (F::SMEM * C + F::E * F::T * C);
-                static size_t done = 0;
-                set_smem(k1_3d<NX, false>, smem, done);
                 SKG_TRY(launch_pdl(k1_3d<NX, false>, grid, F::T * C, smem, s, a, stage));
             } else {
                 return launch_x3_v<NX, 256>(a, stage, inverse, s);
@@ -874,14 +862,10 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
         }
     } else {
         const size_t smem = sizeof(cd) * F::SMEM * C;
-        static size_t done = 0;
         const int grid = a.nkyl * ((a.kz_o + C - 1) / C);
         if (a.rk2 ? stage == 2 : stage == 4) {
-            static size_t done_f = 0;
-            set_smem(k4_3d<NX, CT, true>, smem, done_f);
             SKG_TRY(launch_pdl(k4_3d<NX, CT, true>, grid, F::T * C, smem, s, a, stage));
         } else {
-            set_smem(k4_3d<NX, CT, false>, smem, done);
             SKG_TRY(launch_pdl(k4_3d<NX, CT, false>, grid, F::T * C, smem, s, a, stage));
         }
     }
@@ -913,28 +897,18 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
         // 128^3 0.621 -> 0.600, 512^3 31.27 -> 31.20, 256^3 3.868 -> 3.888)
         const dim3 grid(a.nrl * ((a.kz_in + C - 1) / C), 2);
         if (zb) {
-            static size_t done = 0;
-            set_smem(k2s_3d<NY, CT, true>, smem_s, done);
             SKG_TRY(launch_pdl(k2s_3d<NY, CT, true>, grid, F::T * C, smem_s, s, a));
         } else {
-            static size_t done = 0;
-            set_smem(k2s_3d<NY, CT, false>, smem_s, done);
             SKG_TRY(launch_pdl(k2s_3d<NY, CT, false>, grid, F::T * C, smem_s, s, a));
         }
     } else if (inverse) {
-        static size_t done = 0;
-        set_smem(k2_3d<NY, CT>, smem, done);
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
         SKG_TRY(launch_pdl(k2_3d<NY, CT>, grid, F::T * C, smem, s, a));
     } else {
         const dim3 grid(a.nrl * ((a.kz_o + C - 1) / C), kSplit3);
         if (zb) {
-            static size_t done = 0;
-            set_smem(k2f_3d<NY, CT, true>, smem, done);
             SKG_TRY(launch_pdl(k2f_3d<NY, CT, true>, grid, F::T * C, smem, s, a));
         } else {
-            static size_t done = 0;
-            set_smem(k2f_3d<NY, CT, false>, smem, done);
             SKG_TRY(launch_pdl(k2f_3d<NY, CT, false>, grid, F::T * C, smem, s, a));
         }
     }
@@ -955,28 +929,21 @@ template <int NZ>
 cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
     using Z = Z3<NZ>;
     const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
-    static size_t done = 0;
-    static size_t done_c = 0;
     const long long pairs = (long long)a.nrl * a.ny / 2;
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
     // zero band (dealiased states): kept kz of both directions below 3 NZ / 8
     const bool zb = NZ >= 16 && 8 * a.kz_in <= 3 * NZ && 8 * a.kz_o <= 3 * NZ;
     if (zb) {
         if constexpr (NZ >= 16) {
-            static size_t done_z = 0, done_zc = 0;
             if (a.dyn && a.ystage == 1) {
-                set_smem(k3_3d<NZ, true, true>, smem, done_zc);
                 SKG_TRY(launch_pdl(k3_3d<NZ, true, true>, grid, Z::T * Z::G, smem, s, a));
             } else {
-                set_smem(k3_3d<NZ, false, true>, smem, done_z);
                 SKG_TRY(launch_pdl(k3_3d<NZ, false, true>, grid, Z::T * Z::G, smem, s, a));
             }
         }
     } else if (a.dyn && a.ystage == 1) {
-        set_smem(k3_3d<NZ, true, false>, smem, done_c);
         SKG_TRY(launch_pdl(k3_3d<NZ, true, false>, grid, Z::T * Z::G, smem, s, a));
     } else {
-        set_smem(k3_3d<NZ, false, false>, smem, done);
         SKG_TRY(launch_pdl(k3_3d<NZ, false, false>, grid, Z::T * Z::G, smem, s, a));
     }
     return cudaGetLastError();

@@ -20,6 +20,14 @@ struct DevFlags {
     int bad_dt;     // adaptive dt: nonpositive dt (past t_end) at step div_step
 };
 
+// The divergence flag as one value per CTA: CTAs of the grid that sets it
+// (the final RK update) may see it change while they start, and a kernel
+// whose threads disagree would leave some of them waiting at a barrier.
+// All threads of the CTA must call it (kernel entry, before any return).
+__device__ __forceinline__ bool cta_diverged(const DevFlags* f) {
+    return __syncthreads_or(*reinterpret_cast<const volatile int*>(&f->diverged)) != 0;
+}
+
 // Adaptive (CFL) time step, device-resident so replayed graphs follow it
 // (Simulation::compute_dt + compute_cfl_dt, simulation.cpp:463-476,
 // time_stepping.cpp:15-26).  The stage-1 physical pass of every step reduces
@@ -333,10 +341,17 @@ cudaError_t sanitize_dev(const ForceGeo& g, cd* f, cudaStream_t s, long* launche
 cudaError_t forcing_finish(const ForceGeo& g, const cd* u, cd* f, double rate, double* red,
                            cudaStream_t s, long* launches);
 
+// Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device
+// (cudaFuncSetAttribute is per device): recorded per (kernel, device) under a
+// mutex, so a second device or a second thread gets its own attribute call;
+// a no-op up to the 48 KB default.  Returns the attribute call's error.
+cudaError_t ensure_smem(const void* kernel, size_t bytes);
+
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <typename... KP, typename... A>
 inline cudaError_t launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               A... args) {
+    SKG_TRY(ensure_smem(reinterpret_cast<const void*>(k), smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;

@@ -363,6 +363,13 @@ int skg_get_state_device(skg_ctx* c, double* d_out) {
 }
 
 int skg_step_async(skg_ctx* c, double dt, long nsteps) {
+    // one batch in flight: every batch resets the device flags and (CFL) the
+    // device time, and sync_and_check accounts one dt per batch, so an
+    // earlier batch is checked first (as skg_step does)
+    if (c->pending_steps) {
+        int rc = skg_sync(c);
+        if (rc) return rc;
+    }
     int rc = enqueue_steps(c, dt, nsteps);
     if (rc) return rc;
     c->pending_steps += nsteps;

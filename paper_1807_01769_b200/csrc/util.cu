@@ -2,6 +2,10 @@
 // diagnostic reductions.
 #include "skg_internal.h"
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace skg {
 
 namespace {
@@ -278,6 +282,20 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
     SKG_TRY(launch_pdl(energy_kernel, 592, 256, 0, s, f, g, nvars, S, d_out, steps));
     ++*launches;
     return cudaGetLastError();
+}
+
+cudaError_t ensure_smem(const void* kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    SKG_TRY(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& d = done[{kernel, dev}];
+    if (d >= bytes) return cudaSuccess;
+    SKG_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    d = bytes;
+    return cudaSuccess;
 }
 
 cudaError_t fp64_peak(int device, double* dfma_per_s) {

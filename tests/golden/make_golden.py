@@ -27,12 +27,18 @@ CASES = [
     ("ns2d_64_rk2", "ns2d", (64, 64), 1e-3, 5, "RK2", 14),
     ("ns3d_16", "ns3d", (16, 16, 16), 1e-3, 5, "RK4", 15),
     ("ns3d_16x8x32", "ns3d", (16, 8, 32), 2e-3, 3, "RK4", 16),
+    # viscous RK4 at grids on the dealiased fast kernels' path (smoke())
+    ("ns2d_128", "ns2d", (128, 128), 1e-3, 10, "RK4", 17),
+    ("ns3d_32", "ns3d", (32, 32, 32), 1e-3, 5, "RK4", 18),
 ]
 
 
-def main():
+def main(only=None):
+    """only: fixture names to (re)generate; None = all."""
     out = Path(__file__).resolve().parent
     for name, solver, n, nu, steps, scheme, seed in CASES:
+        if only and name not in only:
+            continue
         u0 = ic.initial_state(solver, n, seed)
         dt = ic.cfl_dt(solver, n, u0)
         r = ref.RefSimulation(solver, n, nu, dt, scheme=scheme)
@@ -43,6 +49,8 @@ def main():
                             n=np.array(n), nu=nu, dt=dt, steps=steps, scheme=scheme,
                             solver=solver, seed=seed, energy=r.energy)
         print(name, "dt", dt, "E", r.energy)
+    if only:
+        return
     # FFT known answers on the reference's own test shapes (test_fft.cpp:111-124)
     fx = {}
     rng = np.random.default_rng(11)
@@ -55,4 +63,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

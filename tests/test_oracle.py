@@ -44,7 +44,8 @@ def test_shim_matches_direct_summation(ref_lib, shape):
     assert err < 1e-13  # test_fft.cpp:122
 
 
-@pytest.mark.parametrize("shape", [(64,), (64, 64), (32, 32, 32), (16, 12, 8), (96, 10), (30, 18)])
+@pytest.mark.parametrize("shape", [(64,), (64, 64), (32, 32, 32), (16, 12, 8), (96, 10), (30, 18),
+                                   (4,), (4, 4), (20, 8), (10, 6, 16), (128, 4, 512), (8, 2048)])
 def test_shim_matches_numpy(ref_lib, shape):
     rng = np.random.default_rng(3)
     u = rng.uniform(-1, 1, size=shape)
