@@ -403,9 +403,14 @@ def run_our_arm(args):
 
     # ---- e2e through the C ABI with host buffers
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    host_in = torch.empty(u0.shape, dtype=torch.complex128, pin_memory=True).numpy()
-    host_in[...] = u0
-    host_out = torch.empty(u0.shape, dtype=torch.complex128, pin_memory=True).numpy()
+    if S * 16 <= (8 << 30):
+        host_in = torch.empty(u0.shape, dtype=torch.complex128, pin_memory=True).numpy()
+        host_in[...] = u0
+        host_out = torch.empty(u0.shape, dtype=torch.complex128, pin_memory=True).numpy()
+    else:  # 1024^3: 25.8 GB states, pageable (pinning two more copies per rank is not affordable)
+        e2e_steps = 1
+        host_in = u0
+        host_out = np.empty_like(u0)
     sim.set_stream(None)  # C-ABI default stream of the context
     barrier()
     torch.cuda.synchronize()

@@ -95,6 +95,15 @@ int skg_destroy(skg_ctx* ctx);
  *   256 bytes); the NCCL communicator then carries only a 1-double barrier.
  */
 int skg_dist_p2p(skg_ctx* ctx, int enable);
+/*
+ * Copy / NCCL exchange of the ns3d slab: with overlap on (the default) the
+ * x-inverse runs one velocity component and the y-forward one field per
+ * launch, and each one's all-to-all runs on a second stream while the next
+ * one computes (events fork and join the streams; CUDA-graph capturable).
+ * Off: one all-to-all per exchange on the context stream.  No effect on the
+ * peer-memory exchange (it overlaps by construction) or on ns2d.
+ */
+int skg_dist_overlap(skg_ctx* ctx, int enable);
 int skg_dist_ipc_handle(skg_ctx* ctx, char* out256);
 int skg_dist_open_peers(skg_ctx* ctx, const char* all_handles);
 int skg_nccl_unique_id(char* out128);

@@ -55,6 +55,11 @@ def lib(path=None):
         L.skref_create_forced.argtypes = [C.POINTER(C.c_void_p), C.c_char_p, C.c_int, ip,
                                           C.c_double, C.c_double, C.c_int, C.c_double,
                                           C.c_double, C.c_double, C.c_double, C.c_long]
+        L.skref_create_files.argtypes = [C.POINTER(C.c_void_p), C.c_char_p, C.c_int, ip,
+                                         C.c_double, C.c_double, C.c_int, C.c_double,
+                                         C.c_char_p, C.c_double]
+        L.skref_output_dir.argtypes = [C.c_void_p, C.c_char_p, C.c_long]
+        L.skref_restart.argtypes = [C.POINTER(C.c_void_p), C.c_char_p, C.c_double]
         L.skref_last_injection.argtypes = [C.c_void_p]
         L.skref_last_injection.restype = C.c_double
         for f in ("skref_spect_size", "skref_phys_size", "skref_iteration"):
@@ -114,15 +119,25 @@ class RefSimulation:
     and forcing off, fixed dt and an injected spectral state."""
 
     def __init__(self, solver: str, n, nu: float, dt: float, scheme: str = "RK4",
-                 dealias_coef: float = 2.0 / 3.0, forcing=None, library=None):
-        """forcing: None, or (k_lo, k_hi, rate, seed) for forcing.enable = true."""
+                 dealias_coef: float = 2.0 / 3.0, forcing=None, library=None, files=None,
+                 _handle=None):
+        """forcing: None, or (k_lo, k_hi, rate, seed) for forcing.enable = true.
+        files: None, or (root_dir, period_save): output.enable_files = true
+        (the OutputManager writes the run directory, output.cpp:105-300)."""
         self.solver = solver
         self.n = tuple(int(x) for x in n)
         self._L = lib(library)
         h = C.c_void_p()
         cn = (C.c_int * len(self.n))(*self.n)
         rk2 = 1 if scheme.upper() == "RK2" else 0
-        if forcing is None:
+        if _handle is not None:
+            h = _handle
+        elif files is not None:
+            root, period = files
+            _check(self._L.skref_create_files(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
+                                            float(dt), rk2, float(dealias_coef),
+                                            str(root).encode(), float(period)))
+        elif forcing is None:
             _check(self._L.skref_create(C.byref(h), solver.encode(), len(self.n), cn, float(nu),
                                       float(dt), rk2, float(dealias_coef)))
         else:
@@ -133,6 +148,22 @@ class RefSimulation:
         self._h = h
         self.nvars = self._L.skref_nvars(h)
         self.spect_shape = self.n[:-1] + (self.n[-1] // 2 + 1,)
+
+    @classmethod
+    def restart(cls, run_dir, solver: str, n, time: float = -1.0, library=None):
+        """load_state_phys_file(run_dir, time) (proj/src/simulation.cpp:705-732):
+        a Simulation from run_dir/params.txt and the snapshot nearest `time`
+        (time < 0: the latest), whose digest must match the params."""
+        L = lib(library)
+        h = C.c_void_p()
+        _check(L.skref_restart(C.byref(h), str(run_dir).encode(), float(time)))
+        return cls(solver, n, 0.0, 0.0, library=library, _handle=h)
+
+    @property
+    def output_dir(self) -> str:
+        buf = C.create_string_buffer(4096)
+        _check(self._L.skref_output_dir(self._h, buf, 4096))
+        return buf.value.decode()
 
     def close(self):
         if self._h:

@@ -18,6 +18,10 @@
 //   tendency    -> Simulation::compute_tendency (simulation.cpp:478-480)
 //   fft_*       -> plan_fft()->forward/inverse (proj/src/fft.cpp:92-137)
 //   grid        -> SpectralGrid k_axis / dealias_mask (proj/src/grid.cpp:20-110)
+//   create_files-> the same Simulation with output.enable_files on (its
+//                  OutputManager writes params.txt, snapshots/*.fld and the
+//                  spectra / budget records, proj/src/output.cpp:105-300)
+//   restart     -> load_state_phys_file (proj/src/simulation.cpp:705-732)
 // Errors are caught and mapped to the same status codes as include/skgpu.h.
 #include <chrono>
 #include <complex>
@@ -30,6 +34,7 @@
 #include "spectralkit/errors.hpp"
 #include "spectralkit/fft.hpp"
 #include "spectralkit/grid.hpp"
+#include "spectralkit/output.hpp"
 #include "spectralkit/simulation.hpp"
 
 using namespace spectralkit;
@@ -88,7 +93,8 @@ void skref_set_workers(int n) { set_fft_workers(n); }
 
 static int create_impl(RefSim** out, const char* solver, int dims, const int* n, double nu,
                        double fixed_dt, int scheme_rk2, double dealias_coef, int forcing,
-                       double k_lo, double k_hi, double rate, long seed);
+                       double k_lo, double k_hi, double rate, long seed,
+                       const char* root_dir = nullptr, double period_save = 0.0);
 
 int skref_create(RefSim** out, const char* solver, int dims, const int* n, double nu,
                  double fixed_dt, int scheme_rk2, double dealias_coef) {
@@ -105,11 +111,45 @@ int skref_create_forced(RefSim** out, const char* solver, int dims, const int* n
                        rate, seed);
 }
 
+// Files on: the run directory goes under root_dir (output.root_dir), records
+// and a snapshot every period_save of simulated time (output.period_save),
+// plus at run start and end (OutputManager on_run_start / on_run_end).
+int skref_create_files(RefSim** out, const char* solver, int dims, const int* n, double nu,
+                       double fixed_dt, int scheme_rk2, double dealias_coef, const char* root_dir,
+                       double period_save) {
+    return create_impl(out, solver, dims, n, nu, fixed_dt, scheme_rk2, dealias_coef, 0, 2.0, 4.0,
+                       1.0, 1234, root_dir, period_save);
+}
+
+// The run directory of a files-on simulation (OutputManager::dir, output.hpp:49).
+int skref_output_dir(RefSim* rs, char* buf, long len) {
+    return guard([&] {
+        const std::string& d = rs->sim->output().dir();
+        if (static_cast<long>(d.size()) + 1 > len) throw ConfigError("buffer too small");
+        std::memcpy(buf, d.c_str(), d.size() + 1);
+    });
+}
+
+// Restart from a run directory's snapshot (time < 0: the latest):
+// load_state_phys_file checks the snapshot's digest against params.txt
+// (simulation.cpp:705-732).
+int skref_restart(RefSim** out, const char* dir, double time) {
+    *out = nullptr;
+    return guard([&] {
+        ensure_builtin_solvers();
+        auto rs = std::make_unique<RefSim>();
+        rs->sim = load_state_phys_file(dir, time);
+        rs->sim->set_quiet(true);
+        *out = rs.release();
+    });
+}
+
 double skref_last_injection(RefSim* rs) { return rs->sim->last_injection(); }
 
 static int create_impl(RefSim** out, const char* solver, int dims, const int* n, double nu,
                        double fixed_dt, int scheme_rk2, double dealias_coef, int forcing,
-                       double k_lo, double k_hi, double rate, long seed) {
+                       double k_lo, double k_hi, double rate, long seed, const char* root_dir,
+                       double period_save) {
     *out = nullptr;
     return guard([&] {
         ensure_builtin_solvers();
@@ -119,7 +159,11 @@ static int create_impl(RefSim** out, const char* solver, int dims, const int* n,
             p.set(std::string("oper.") + ns[d], static_cast<std::int64_t>(n[d]));
         if (dealias_coef > 0) p.set("oper.dealias_coef", dealias_coef);
         p.set("nu_2", nu);
-        p.set("output.enable_files", false);
+        p.set("output.enable_files", root_dir != nullptr);
+        if (root_dir) {
+            p.set("output.root_dir", std::string(root_dir));
+            p.set("output.period_save", period_save);
+        }
         p.set("forcing.enable", forcing != 0);
         if (forcing) {
             p.set("forcing.k_lo", k_lo);

@@ -38,7 +38,7 @@ EXPORTS = [
     "skg_reset_stats", "skg_fp64_peak", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
     "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
-    "skg_dist_p2p", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
+    "skg_dist_p2p", "skg_dist_overlap", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
 ]
 
 
@@ -133,6 +133,7 @@ def load_library():
     L.skg_last_injection.restype = C.c_double
     L.skg_sanitize_state.argtypes = [vp]
     L.skg_dist_p2p.argtypes = [vp, C.c_int]
+    L.skg_dist_overlap.argtypes = [vp, C.c_int]
     L.skg_dist_ipc_handle.argtypes = [vp, C.c_char_p]
     L.skg_dist_open_peers.argtypes = [vp, C.c_char_p]
     L.skg_spectra.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -458,6 +459,11 @@ class Simulation:
             out = all_gather(mine.raw)
         blob = b"".join(out)
         self._call("skg_dist_open_peers", C.create_string_buffer(blob, len(blob)))
+
+    def set_overlap(self, on: bool) -> None:
+        """ns3d slab, copy / NCCL exchange: all-to-all chunked per field on a
+        second stream, overlapping the next field's pass (skg_dist_overlap)."""
+        self._call("skg_dist_overlap", C.c_int(1 if on else 0))
 
     def disable_p2p(self) -> None:
         """Back to the NCCL / device-copy exchange (skg_dist_p2p(0))."""

@@ -148,6 +148,11 @@ struct skg_ctx {
     size_t dfs3 = 0;                   // ns3d: their field stride (uniform)
     std::vector<void*> ipc_opened;  // cudaIpcOpenMemHandle mappings to close
     double* d_barrier = nullptr;    // one double all-reduced as the cross-rank barrier
+    // ns3d copy / NCCL exchange chunked per field on a second stream
+    // (enqueue_dist_step3_chunked); no_overlap keeps it on the context stream
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t xev[7] = {};
+    bool no_overlap = false;
 
     // per-kernel-class event timing (skg_set_timing)
     struct Pending {

@@ -87,7 +87,7 @@ int sync_and_check(skg_ctx* c, long nsteps, double dt) {
 // (rows(q) x cols(r) from r to q), 1: product spectra (cols(q) x rows(r)).
 // Single-process mode: device-to-device copies; otherwise NCCL send/recv
 // on the context stream (grouped, one block per peer).
-int exchange3(skg_ctx* c, int which);
+int exchange3(skg_ctx* c, int which, unsigned fmask = 0xffu, cudaStream_t st = nullptr);
 
 int exchange(skg_ctx* c, int which) {
     if (c->solver == 3) return exchange3(c, which);
@@ -169,8 +169,10 @@ int exchange(skg_ctx* c, int which) {
 
 // ns3d all-to-alls.  which = 0: x-inverse outputs, 5 fields, block r -> q =
 // rows(q) x lines(r) ([xl][kyl_r][kz_in]); 1: y-forward outputs, 3 fields,
-// block r -> q = rows(r) x lines(q) ([xl][kyl_q][kz_o]).
-int exchange3(skg_ctx* c, int which) {
+// block r -> q = rows(r) x lines(q) ([xl][kyl_q][kz_o]).  fmask: the fields
+// to exchange (bit f); st: the stream (default: the context stream).
+int exchange3(skg_ctx* c, int which, unsigned fmask, cudaStream_t st) {
+    if (!st) st = c->stream;
     const int G = c->G;
     if (G == 1) return SKG_OK;  // one partition: receive buffers alias the send buffers
     if (c->p2p) {  // producers stored into the receive buffers: a barrier remains
@@ -203,9 +205,9 @@ int exchange3(skg_ctx* c, int which) {
             for (const Part& dst : c->parts)
                 for (int f = 0; f < nf; ++f) {
                     const size_t cnt = count(src.r, dst.r);
-                    if (!cnt) continue;
+                    if (!cnt || !(fmask >> f & 1u)) continue;
                     CUDA_TRY(cudaMemcpyAsync(dst_ptr(dst, src.r, f), src_ptr(src, dst.r, f),
-                                             cnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                                             cnt * sizeof(cd), cudaMemcpyDeviceToDevice, st));
                     if (src.r != dst.r) bytes += cnt * sizeof(cd);
                 }
     } else {
@@ -214,15 +216,16 @@ int exchange3(skg_ctx* c, int which) {
         ncclResult_t nr = nccl().GroupStart();
         for (int q = 0; q < G && nr == ncclSuccess; ++q) {
             for (int f = 0; f < nf && nr == ncclSuccess; ++f) {
+                if (!(fmask >> f & 1u)) continue;
                 const size_t scnt = count(r, q), rcnt = count(q, r);
                 cd* sptr = src_ptr(me, q, f);
                 cd* rptr = dst_ptr(me, q, f);
                 if (q == r) {
-                    if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, c->stream));
+                    if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, st));
                     continue;
                 }
-                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, c->stream);
-                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, c->stream);
+                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, st);
+                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, st);
                 bytes += scnt * sizeof(cd);
             }
         }
@@ -249,10 +252,62 @@ int dist_dt_update(skg_ctx* c, long* counter) {
 // One step of a slab-decomposed context.  ns2d: the x-forward of every stage
 // runs fused with the next stage's x-inverse (first: the step opens the
 // batch and runs its own stage-1 x-inverse; last: no next stage).
+// ns3d slab step with the all-to-alls chunked per field on a second stream
+// (copy / NCCL exchange): the x-inverse runs one velocity component per
+// launch and the y-forward one field per launch, each followed by the
+// exchange of the fields it produced on c->cstream, so the transfer of one
+// overlaps the next one's pass; the compute stream joins the exchange stream
+// before the consumers (y-inverse, x-forward) start.
+int enqueue_dist_step3_chunked(skg_ctx* c, double dt, long* counter) {
+    const int nst = c->scheme == SKG_RK2 ? 2 : 4;
+    const skg::LaunchHook hook = hook_of(c);
+    int rc;
+    if (!c->cstream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : c->xev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    auto run = [&](int pass, int st, int comp0, int ncomp) -> int {
+        for (const Part& p : c->parts) {
+            skg::Ns3dArgs a = args3d_part(c, dt, p);
+            a.comp0 = comp0;
+            a.ncomp = ncomp;
+            CUDA_TRY(skg::ns3d_pass(a, pass, st, c->stream, counter, hook));
+        }
+        return SKG_OK;
+    };
+    auto fork = [&](int k, int which, unsigned fmask) -> int {
+        CUDA_TRY(cudaEventRecord(c->xev[k], c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->xev[k], 0));
+        int r2 = exchange3(c, which, fmask, c->cstream);
+        ++*counter;
+        return r2;
+    };
+    auto join = [&]() -> int {
+        CUDA_TRY(cudaEventRecord(c->xev[6], c->cstream));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->xev[6], 0));
+        return SKG_OK;
+    };
+    // fields of x-inverse component c: X[v_0]; X[v_1], X[kx v_1]; X[v_2], X[kx v_2]
+    static const unsigned xfields[3] = {1u, 2u | 8u, 4u | 16u};
+    for (int st = 1; st <= nst; ++st) {
+        for (int comp = 0; comp < 3; ++comp)
+            if ((rc = run(0, st, comp, 1)) || (rc = fork(comp, 0, xfields[comp]))) return rc;
+        if ((rc = join()) || (rc = run(3, st, 0, 3))) return rc;
+        for (int m = 0; m < 3; ++m)
+            if ((rc = run(4, st, m, 1)) || (rc = fork(3 + m, 1, 1u << m))) return rc;
+        if ((rc = join())) return rc;
+        if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;
+        if ((rc = run(2, st, 0, 3))) return rc;
+    }
+    return SKG_OK;
+}
+
 int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool last) {
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
     int rc;
+    if (c->solver == 3 && !c->p2p && c->G > 1 && !c->timing && !c->no_overlap)
+        return enqueue_dist_step3_chunked(c, dt, counter);
     if (c->solver == 3) {
         for (int st = 1; st <= nst; ++st) {
             for (int pass = 0; pass < 3; ++pass) {
@@ -311,8 +366,45 @@ int enqueue_steps(skg_ctx* c, double dt, long nsteps) {
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
     if (c->dist) {
-        for (long s = 0; s < nsteps; ++s) {
-            int rc2 = enqueue_dist_step(c, dt, &c->launches, s == 0, s == nsteps - 1);
+        // first step eagerly, middle steps by replay of a captured step (the
+        // NCCL calls and the exchange stream's fork/join are captured too),
+        // the last step eagerly (ns2d: it closes the fused x-pass chain)
+        long s = 0;
+        if (nsteps > 0) {
+            int rc2 = enqueue_dist_step(c, dt, &c->launches, true, nsteps == 1);
+            if (rc2) return rc2;
+            s = 1;
+        }
+        if (nsteps - s >= 3 && !c->timing && c->stream != nullptr) {
+            if (c->gexec && (c->g_dt != dt || c->g_stream != c->stream || c->g_diag != c->diag ||
+                             c->g_p2p != c->p2p)) {
+                cudaGraphExecDestroy(c->gexec);
+                c->gexec = nullptr;
+            }
+            if (!c->gexec) {
+                cudaGraph_t graph;
+                long dummy = 0;
+                CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+                const int rc2 = enqueue_dist_step(c, dt, &dummy, false, false);
+                cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
+                if (rc2) return rc2;
+                CUDA_TRY(e2);
+                CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
+                cudaGraphDestroy(graph);
+                c->g_launches = dummy;
+                c->g_dt = dt;
+                c->g_diag = c->diag;
+                c->g_pruned = c->pruned;
+                c->g_p2p = c->p2p;
+                c->g_stream = c->stream;
+            }
+            for (; s < nsteps - 1; ++s) {
+                CUDA_TRY(cudaGraphLaunch(c->gexec, c->stream));
+                c->launches += c->g_launches;
+            }
+        }
+        for (; s < nsteps; ++s) {
+            int rc2 = enqueue_dist_step(c, dt, &c->launches, false, s == nsteps - 1);
             if (rc2) return rc2;
         }
         return SKG_OK;

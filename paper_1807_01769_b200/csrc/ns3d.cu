@@ -84,11 +84,12 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
     return ky <= a.kcy ? ky : ky - (a.ny - (2 * a.kcy + 1));
 }
 
-// x-inverse and y-forward: one component / field per CTA (gridDim.y = 3)
-// instead of three in sequence -- shorter dependent chains per CTA (ms/step:
+// x-inverse and y-forward: one component / field per CTA (blockIdx.y; a
+// launch covers components [comp0, comp0 + ncomp), normally all three; the
+// NCCL slab path launches them one at a time so the all-to-all of one
+// overlaps the next one's pass) instead of three in sequence -- shorter dependent chains per CTA (ms/step:
 // 64^3 0.201 -> 0.184, 128^3 0.601 -> 0.588, 512^3 31.10 -> 30.94,
 // 256^3 3.889 -> 3.914).
-constexpr int kSplit3 = 3;
 
 // z pass, dealiased states: the Hermitian split of the forward output from
 // registers (z_store_pair) instead of a shared-memory round trip of all
@@ -158,8 +159,8 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twx);
     const cd* kprev = stage == 2 ? a.k1 : stage == 3 ? a.k2 : a.k3;
-    // gridDim.y == 3: one velocity component per CTA
-    const int c0 = gridDim.y == 3 ? blockIdx.y : 0, c1 = gridDim.y == 3 ? c0 + 1 : 3;
+    // one velocity component per CTA
+    const int c0 = a.comp0 + blockIdx.y, c1 = c0 + 1;
 #pragma unroll 1
     for (int c = c0; c < c1; ++c) {
 #pragma unroll
@@ -647,8 +648,8 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
     int* lown = loff + NY;
     if (a.p2p) line_offsets_p2p<NY>(a, x, a.kz_o, loff, lown);
     else line_offsets<NY>(a, x, a.kz_o, loff);
-    // gridDim.y == 3: one field per CTA
-    const int m0 = gridDim.y == 3 ? blockIdx.y : 0, m1 = gridDim.y == 3 ? m0 + 1 : 3;
+    // one field per CTA
+    const int m0 = a.comp0 + blockIdx.y, m1 = m0 + 1;
 #pragma unroll 1
     for (int m = m0; m < m1; ++m) {
         const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
@@ -845,7 +846,7 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
     constexpr int C = Strided<NX, CT>::C;
     using F = BF3<NX>;
     if (inverse) {
-        const dim3 grid(a.nkyl * ((a.kz_in + C - 1) / C), kSplit3);
+        const dim3 grid(a.nkyl * ((a.kz_in + C - 1) / C), a.ncomp);
         const bool pz = NX >= 64 && a.pruned && a.kcx <= 3 * F::E / 8 * F::T - 1;
         if (pz) {
             if constexpr (NX >= 64) {
@@ -905,7 +906,7 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
         const int grid = a.nrl * ((a.kz_in + C - 1) / C);
         SKG_TRY(launch_pdl(k2_3d<NY, CT>, grid, F::T * C, smem, s, a));
     } else {
-        const dim3 grid(a.nrl * ((a.kz_o + C - 1) / C), kSplit3);
+        const dim3 grid(a.nrl * ((a.kz_o + C - 1) / C), a.ncomp);
         if (zb) {
             SKG_TRY(launch_pdl(k2f_3d<NY, CT, true>, grid, F::T * C, smem, s, a));
         } else {
@@ -1002,23 +1003,31 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
     const double plane_in = (double)a.nrl * a.ny * a.kz_in;
     const double plane_o = (double)a.nrl * a.ny * a.kz_o;
     if (pass == 0) {
+        // component c reads v_c (and k_c) and writes X[v_c] (+ X[kx v_c] for c > 0)
+        const double nin = a.ncomp, nout = a.ncomp == 3 ? 5.0 : (a.comp0 == 0 ? 1.0 : 2.0) * a.ncomp;
         hook.begin(0);
         if ((err = dispatch_x3(a, stage, true, s)) != cudaSuccess) return err;
-        hook.end(0, B * (3.0 * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + 5.0 * a.nx * lines_in));
+        hook.end(0, B * (nin * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + nout * a.nx * lines_in));
         *launches += 1;
-    } else if (pass == 1) {
+    } else if (pass == 1 || pass == 3 || pass == 4) {
         Ns3dArgs b = a;  // the z pass of stage 1 feeds the CFL max
         b.ystage = stage;
-        hook.begin(3);
-        if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
-        hook.end(3, B * (5.0 * a.nrl * kyk * a.kz_in + 6.0 * plane_in));
-        hook.begin(1);
-        if ((err = dispatch_z3(b, s)) != cudaSuccess) return err;
-        hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
-        hook.begin(5);
-        if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;
-        hook.end(5, B * (3.0 * plane_o + 3.0 * a.nrl * kyk * a.kz_o));
-        *launches += 3;
+        if (pass != 4) {
+            hook.begin(3);
+            if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
+            hook.end(3, B * (5.0 * a.nrl * kyk * a.kz_in + 6.0 * plane_in));
+            hook.begin(1);
+            if ((err = dispatch_z3(b, s)) != cudaSuccess) return err;
+            hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
+            *launches += 2;
+        }
+        if (pass != 3) {
+            const double nf = pass == 4 ? a.ncomp : 3.0;
+            hook.begin(5);
+            if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;
+            hook.end(5, B * nf * (plane_o + a.nrl * kyk * a.kz_o));
+            *launches += 1;
+        }
     } else {
         hook.begin(2);
         if ((err = dispatch_x3(a, stage, false, s)) != cudaSuccess) return err;

@@ -194,6 +194,8 @@ struct Ns3dArgs {
     double dt, hdt, sdt;
     DynStep* dyn;       // adaptive dt (nullptr: the fixed dt above)
     int ystage;         // RK stage of the physical pass (stage 1 feeds the CFL max)
+    int comp0 = 0;      // x-inverse / y-forward launches: components [comp0, comp0 + ncomp)
+    int ncomp = 3;
     const cd* force;    // forcing addend in the state layout (nullptr: off)
     const double *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
     cd* u;               // 3 variables, each nx*ny*nh (reference layout)
@@ -271,7 +273,9 @@ __device__ __forceinline__ void diag_accumulate(double* slot, double e, double z
 }
 cudaError_t ns3d_launch_stage(const Ns3dArgs& a, int stage, cudaStream_t s, long* launches,
                               const LaunchHook& hook);
-// Slab pieces: pass 0 x-inverse, 1 y-inverse + z + y-forward, 2 x-forward + RK.
+// Slab pieces: pass 0 x-inverse, 1 y-inverse + z + y-forward, 2 x-forward + RK;
+// pass 3 = y-inverse + z alone, 4 = y-forward alone (a.comp0 / a.ncomp pick
+// the fields of passes 0 and 4).
 cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, long* launches,
                       const LaunchHook& hook);
 bool ns3d_supported(int nx, int ny, int nz);

@@ -288,6 +288,9 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->gs.work);
     harvest(c);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (cudaEvent_t e : c->xev)
+        if (e) cudaEventDestroy(e);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     for (Part& p : c->parts) {
         cudaFree(p.u);
         for (auto q : p.k) cudaFree(q);
@@ -820,6 +823,12 @@ int skg_dist_open_peers(skg_ctx* c, const char* all) {
     }
     if (!c->d_barrier) CUDA_TRY(cudaMalloc(&c->d_barrier, sizeof(double)));
     c->p2p = true;
+    return SKG_OK;
+}
+
+int skg_dist_overlap(skg_ctx* c, int enable) {
+    if (!c->dist) return fail(SKG_EUNSUPPORTED, "exchange overlap: slab-decomposed contexts");
+    c->no_overlap = !enable;
     return SKG_OK;
 }
 

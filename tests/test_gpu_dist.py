@@ -230,3 +230,112 @@ def test_exchange_mode_switch_between_calls():
     b.disable_p2p()
     b.step(5)
     assert np.array_equal(a.get_state(), b.get_state())
+
+
+@pytest.mark.parametrize("n,world", [((64, 64, 64), 4), ((128, 64, 32), 8)])
+def test_slab3d_overlapped_exchange_matches_serial(n, world):
+    """ns3d copy exchange chunked per field on a second stream (the
+    NCCL path's overlap, skg_dist_overlap: per-component x-inverse and
+    per-field y-forward launches, fork/join events) equals the serial
+    exchange bit for bit, with the middle steps replayed from the captured
+    CUDA graph of the dist step; and both equal one partition."""
+    u0 = ic.ns3d_ic(n, seed=6)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    a = api.Simulation("ns3d", n, 1e-3, dt, world=world)
+    a.set_overlap(False)
+    a.set_state(u0)
+    a.step(6)
+    b = api.Simulation("ns3d", n, 1e-3, dt, world=world)
+    b.set_state(u0)
+    b.step(6)
+    assert np.array_equal(a.get_state(), b.get_state())
+    one = api.Simulation("ns3d", n, 1e-3, dt)
+    one.set_state(u0)
+    one.step(6)
+    s, r = b.get_state(), one.get_state()
+    for v in range(3):
+        assert O.rel_l2(s[v], r[v]) < 1e-14
+    # CFL steps through the overlapped path (all-reduced max |u_d| per step)
+    b.set_cfl(0.5, 0.1)
+    one.set_cfl(0.5, 0.1)
+    b.step(5)
+    one.step(5)
+    assert abs(b.t - one.t) <= 1e-15 * one.t
+    s, r = b.get_state(), one.get_state()
+    for v in range(3):
+        assert O.rel_l2(s[v], r[v]) < 1e-13
+
+
+def a2a_bytes_per_gpu_step(sim, world, nsteps=2):
+    """Measured all-to-all bytes per GPU per RK4 step (exchange class of the
+    per-kernel stats: bytes that cross partitions)."""
+    sim.reset_stats()
+    sim.set_timing(True)
+    sim.step(nsteps)
+    sim.set_timing(False)
+    return sim.kernel_stats()["exchange"][2] / world / nsteps
+
+
+@pytest.mark.slow
+def test_real_split_ns2d_4096_world8():
+    """BASELINE configs[1]'s grid at its 8-GPU split (8 slab partitions on one
+    GPU): copy and peer-memory exchanges equal one partition; the measured
+    all-to-all volume per GPU is the kept-column model
+    4 stages x 2 exchanges x 2 fields x nx Kc 16 B (G-1)/G^2 (SURVEY 8(d)'s
+    unpruned 4-inverse+1-forward model: 20 F (G-1)/G^2)."""
+    n, world = (4096, 4096), 8
+    u0 = ic.ns2d_ic(n, seed=1234)
+    dt = ic.cfl_dt("ns2d", n, u0)
+    one = api.Simulation("ns2d", n, 1e-4, dt)
+    one.set_state(u0)
+    one.step(5)
+    ref = one.get_state()
+    one.close()
+    for p2p in (False, True):
+        d = api.Simulation("ns2d", n, 1e-4, dt, world=world)
+        if p2p:
+            d.enable_p2p()
+        d.set_state(u0)
+        d.step(5)
+        assert O.rel_l2(d.get_state(), ref) < 1e-14
+        if not p2p:
+            kc = 1365 + 1
+            model = 4 * 2 * 2 * n[0] * kc * 16 * (world - 1) / world ** 2
+            got = a2a_bytes_per_gpu_step(d, world)
+            assert abs(got - model) <= 1e-9 * model
+            F = 16 * n[0] * (n[1] // 2 + 1)
+            assert got < 20 * F * (world - 1) / world ** 2
+        d.close()
+
+
+@pytest.mark.slow
+def test_real_split_ns3d_512_world8():
+    """BASELINE configs[3]'s grid at its 8-GPU split: the overlapped copy
+    exchange and the peer-memory exchange equal one partition; measured
+    all-to-all volume per GPU = 4 stages x 8 fields x nx K kz 16 B (G-1)/G^2
+    (K = 341 kept ky lines, kz = 171 kept kz; SURVEY 8(d) unpruned 32 F (G-1)/G^2)."""
+    n, world = (512, 512, 512), 8
+    u0 = ic.ns3d_ic(n, seed=1234)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    one = api.Simulation("ns3d", n, 2e-4, dt)
+    one.set_state(u0)
+    one.step(4)
+    ref = one.get_state()
+    one.close()
+    for p2p in (False, True):
+        d = api.Simulation("ns3d", n, 2e-4, dt, world=world)
+        if p2p:
+            d.enable_p2p()
+        d.set_state(u0)
+        d.step(4)
+        s = d.get_state()
+        for v in range(3):
+            assert O.rel_l2(s[v], ref[v]) < 1e-14
+        del s
+        if not p2p:
+            model = 4 * 8 * n[0] * 341 * 171 * 16 * (world - 1) / world ** 2
+            got = a2a_bytes_per_gpu_step(d, world, 1)
+            assert abs(got - model) <= 1e-9 * model
+            F = 16 * n[0] * n[1] * (n[2] // 2 + 1)
+            assert got < 32 * F * (world - 1) / world ** 2
+        d.close()
