@@ -229,6 +229,8 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         else c->inter_elems = 11 * (size_t)n[0] * n[1] * c->nh;  // A[5] (C aliases) + B[6] (D aliases)
         if (c->generic) c->inter_elems = 1;
         ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
+        // counters of the chained y/z/y pass (zeroed; self-resetting)
+        if (sid == 3 && !c->generic) ok = ok && alloc((void**)&c->chain, sizeof(int) * (2 + 2 * (size_t)n[0]));
         if (c->generic) {
             const size_t P = (size_t)c->P;
             ok = ok && alloc((void**)&c->gs.w, sizeof(cd) * S * c->nvars);
@@ -272,6 +274,7 @@ int skg_destroy(skg_ctx* c) {
     cudaFree(c->work);
     cudaFree(c->etab);
     cudaFree(c->flags);
+    cudaFree(c->chain);
     cudaFree(c->d_count);
     cudaFree(c->d_red);
     cudaFree(c->d_dyn);
