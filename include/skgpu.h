@@ -104,6 +104,13 @@ int skg_dist_p2p(skg_ctx* ctx, int enable);
  * peer-memory exchange (it overlaps by construction) or on ns2d.
  */
 int skg_dist_overlap(skg_ctx* ctx, int enable);
+
+/* Debug aid (no compute-sanitizer on the target pool): with SKG_GUARD=1 in
+ * the environment every device allocation of the library is surrounded by
+ * 64 KB guard zones holding a byte pattern; this returns how many guard
+ * bytes of the live allocations changed (out-of-bounds writes), 0 when the
+ * mode is off, -1 on a copy error. */
+long skg_guard_violations(void);
 int skg_dist_ipc_handle(skg_ctx* ctx, char* out256);
 int skg_dist_open_peers(skg_ctx* ctx, const char* all_handles);
 int skg_nccl_unique_id(char* out128);

@@ -38,7 +38,7 @@ EXPORTS = [
     "skg_reset_stats", "skg_fp64_peak", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
     "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
-    "skg_dist_p2p", "skg_dist_overlap", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
+    "skg_dist_p2p", "skg_dist_overlap", "skg_guard_violations", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
 ]
 
 
@@ -134,6 +134,8 @@ def load_library():
     L.skg_sanitize_state.argtypes = [vp]
     L.skg_dist_p2p.argtypes = [vp, C.c_int]
     L.skg_dist_overlap.argtypes = [vp, C.c_int]
+    L.skg_guard_violations.argtypes = []
+    L.skg_guard_violations.restype = C.c_long
     L.skg_dist_ipc_handle.argtypes = [vp, C.c_char_p]
     L.skg_dist_open_peers.argtypes = [vp, C.c_char_p]
     L.skg_spectra.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -187,6 +189,12 @@ def fp64_peak(device: int = 0) -> float:
     if rc:
         _raise(rc)
     return out.value
+
+
+def guard_violations() -> int:
+    """Changed guard bytes around the library's device allocations
+    (SKG_GUARD=1 debug mode, skg_guard_violations); 0 when the mode is off."""
+    return int(load_library().skg_guard_violations())
 
 
 def nccl_unique_id() -> bytes:

@@ -280,12 +280,12 @@ const BlueTab* blue_tab(int n) {
             }
             bh[q] = make_double2((double)acc.real(), (double)acc.imag());
         }
-        cudaMalloc(&tb.chirp[si], sizeof(cd) * n);
-        cudaMalloc(&tb.bhat[si], sizeof(cd) * M);
+        skg::dmalloc(&tb.chirp[si], sizeof(cd) * n);
+        skg::dmalloc(&tb.bhat[si], sizeof(cd) * M);
         cudaMemcpy(tb.chirp[si], ch.data(), sizeof(cd) * n, cudaMemcpyHostToDevice);
         cudaMemcpy(tb.bhat[si], bh.data(), sizeof(cd) * M, cudaMemcpyHostToDevice);
     }
-    cudaMalloc(&tb.twm, sizeof(cd) * M);
+    skg::dmalloc(&tb.twm, sizeof(cd) * M);
     cudaMemcpy(tb.twm, wm.data(), sizeof(cd) * M, cudaMemcpyHostToDevice);
     return &(g_blue[key] = tb);
 }

@@ -531,8 +531,8 @@ int store_state_to_io(skg_ctx* c, const cd* src) {
 // grid dump, allocated on first use (the step itself never needs them)
 int ensure_fft_bufs(skg_ctx* c) {
     if (c->phys && c->work) return SKG_OK;
-    CUDA_TRY(cudaMalloc(&c->phys, sizeof(double) * (size_t)c->P));
-    CUDA_TRY(cudaMalloc(&c->work, sizeof(cd) * (size_t)c->S));
+    CUDA_TRY(skg::dmalloc(&c->phys, sizeof(double) * (size_t)c->P));
+    CUDA_TRY(skg::dmalloc(&c->work, sizeof(cd) * (size_t)c->S));
     return SKG_OK;
 }
 
@@ -543,7 +543,7 @@ int ensure_p2p_bufs(skg_ctx* c) {
     for (int q = 0; q < c->G; ++q) maxcols = std::max(maxcols, (size_t)(c->cstart[q + 1] - c->cstart[q]));
     c->dfs3 = (size_t)c->n[0] * maxcols * ((size_t)c->kc[2] + 1);
     for (Part& p : c->parts)
-        if (!p.rD3) CUDA_TRY(cudaMalloc(&p.rD3, sizeof(cd) * 3 * c->dfs3));
+        if (!p.rD3) CUDA_TRY(skg::dmalloc(&p.rD3, sizeof(cd) * 3 * c->dfs3));
     return SKG_OK;
 }
 
@@ -559,7 +559,7 @@ cd* twiddle_table(int device, int n) {
     if (it != g_tw.tabs.end()) return it->second;
     std::vector<cd> w = twiddles(n);
     cd* d = nullptr;
-    if (cudaMalloc(&d, sizeof(cd) * n) != cudaSuccess) return nullptr;
+    if (skg::dmalloc(&d, sizeof(cd) * n) != cudaSuccess) return nullptr;
     cudaMemcpy(d, w.data(), sizeof(cd) * n, cudaMemcpyHostToDevice);
     g_tw.tabs[key] = d;
     return d;

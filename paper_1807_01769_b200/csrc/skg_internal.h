@@ -349,6 +349,20 @@ cudaError_t sanitize_dev(const ForceGeo& g, cd* f, cudaStream_t s, long* launche
 cudaError_t forcing_finish(const ForceGeo& g, const cd* u, cd* f, double rate, double* red,
                            cudaStream_t s, long* launches);
 
+// Device allocations of the library.  With SKG_GUARD=1 in the environment
+// every allocation gets 64 KB guard zones before and after it, filled with a
+// byte pattern; guard_violations() counts the guard bytes that changed (an
+// out-of-bounds write by any kernel or copy).  Debug aid where
+// compute-sanitizer is unavailable; IPC export is refused in this mode.
+cudaError_t dmalloc_raw(void** p, size_t bytes);
+void dfree(void* p);
+long guard_violations();
+bool guards_enabled();
+template <class T>
+inline cudaError_t dmalloc(T** p, size_t bytes) {
+    return dmalloc_raw(reinterpret_cast<void**>(p), bytes);
+}
+
 // Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device
 // (cudaFuncSetAttribute is per device): recorded per (kernel, device) under a
 // mutex, so a second device or a second thread gets its own attribute call;

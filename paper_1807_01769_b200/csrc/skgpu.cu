@@ -109,7 +109,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     c->stream = c->own;
     const size_t S = (size_t)c->S;
     auto alloc = [&](void** p, size_t bytes) {
-        if (cudaMalloc(p, bytes < 16 ? 16 : bytes) != cudaSuccess) return false;
+        if (skg::dmalloc(p, bytes < 16 ? 16 : bytes) != cudaSuccess) return false;
         return cudaMemset(*p, 0, bytes < 16 ? 16 : bytes) == cudaSuccess;
     };
     bool ok = true;
@@ -266,52 +266,52 @@ int skg_destroy(skg_ctx* c) {
     if (!c) return SKG_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->u);
-    for (auto p : c->k) cudaFree(p);
-    cudaFree(c->inter);
-    cudaFree(c->io);
-    cudaFree(c->phys);
-    cudaFree(c->work);
-    cudaFree(c->etab);
-    cudaFree(c->flags);
-    cudaFree(c->chain);
-    cudaFree(c->d_count);
-    cudaFree(c->d_red);
-    cudaFree(c->d_dyn);
+    skg::dfree(c->u);
+    for (auto p : c->k) skg::dfree(p);
+    skg::dfree(c->inter);
+    skg::dfree(c->io);
+    skg::dfree(c->phys);
+    skg::dfree(c->work);
+    skg::dfree(c->etab);
+    skg::dfree(c->flags);
+    skg::dfree(c->chain);
+    skg::dfree(c->d_count);
+    skg::dfree(c->d_red);
+    skg::dfree(c->d_dyn);
     for (void* d : c->ipc_opened) cudaIpcCloseMemHandle(d);
-    cudaFree(c->d_barrier);
-    cudaFree(c->f_ref);
-    cudaFree(c->f_cm);
-    cudaFree(c->f_red);
+    skg::dfree(c->d_barrier);
+    skg::dfree(c->f_ref);
+    skg::dfree(c->f_cm);
+    skg::dfree(c->f_red);
     if (c->f_noise) cudaFreeHost(c->f_noise);
-    cudaFree(c->gs.w);
-    cudaFree(c->gs.spec);
-    cudaFree(c->gs.nl);
-    cudaFree(c->gs.phys);
-    cudaFree(c->gs.work);
+    skg::dfree(c->gs.w);
+    skg::dfree(c->gs.spec);
+    skg::dfree(c->gs.nl);
+    skg::dfree(c->gs.phys);
+    skg::dfree(c->gs.work);
     harvest(c);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (cudaEvent_t e : c->xev)
         if (e) cudaEventDestroy(e);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     for (Part& p : c->parts) {
-        cudaFree(p.u);
-        for (auto q : p.k) cudaFree(q);
+        skg::dfree(p.u);
+        for (auto q : p.k) skg::dfree(q);
         for (int f = 0; f < 2; ++f) {
-            cudaFree(p.sI[f]);
-            cudaFree(p.rI[f]);
-            cudaFree(p.sA[f]);
-            cudaFree(p.rA[f]);
+            skg::dfree(p.sI[f]);
+            skg::dfree(p.rI[f]);
+            skg::dfree(p.sA[f]);
+            skg::dfree(p.rA[f]);
         }
-        cudaFree(p.rD3);
-        if (p.rA3 != p.A3) cudaFree(p.rA3);
-        if (p.sD3 != p.B3) cudaFree(p.sD3);
-        cudaFree(p.A3);
-        cudaFree(p.B3);
+        skg::dfree(p.rD3);
+        if (p.rA3 != p.A3) skg::dfree(p.rA3);
+        if (p.sD3 != p.B3) skg::dfree(p.sD3);
+        skg::dfree(p.A3);
+        skg::dfree(p.B3);
     }
-    cudaFree(c->cmfull);
-    cudaFree(c->d_kowner);
-    cudaFree(c->d_cstart);
+    skg::dfree(c->cmfull);
+    skg::dfree(c->d_kowner);
+    skg::dfree(c->d_cstart);
     if (c->comm) nccl().CommDestroy(c->comm);
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
@@ -410,7 +410,7 @@ int skg_run(skg_ctx* c, double dt, long nsteps, double* series) {
         if (rc) return rc;
     }
     double* d = nullptr;
-    CUDA_TRY(cudaMalloc(&d, sizeof(double) * 3 * nsteps));
+    CUDA_TRY(skg::dmalloc(&d, sizeof(double) * 3 * nsteps));
     CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(double) * 3 * nsteps, c->stream));
     c->diag = d;
     int rc = enqueue_steps(c, dt, nsteps);
@@ -422,7 +422,7 @@ int skg_run(skg_ctx* c, double dt, long nsteps, double* series) {
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
     }
-    cudaFree(d);
+    skg::dfree(d);
     return rc;
 }
 
@@ -537,8 +537,8 @@ int skg_spectra(skg_ctx* c, int cap, double* k, double* E, double* T, double* D,
     if (int rc = ensure_fft_bufs(c)) return rc;
     cd* st = nullptr;
     double* d3 = nullptr;
-    CUDA_TRY(cudaMalloc(&st, sizeof(cd) * c->S * c->nvars));
-    CUDA_TRY(cudaMalloc(&d3, sizeof(double) * 3 * nsh));
+    CUDA_TRY(skg::dmalloc(&st, sizeof(cd) * c->S * c->nvars));
+    CUDA_TRY(skg::dmalloc(&d3, sizeof(double) * 3 * nsh));
     int rc = store_state_to_io(c, c->u);
     if (!rc) {
         cudaMemcpyAsync(st, c->io, sizeof(cd) * c->S * c->nvars, cudaMemcpyDeviceToDevice, c->stream);
@@ -561,8 +561,8 @@ int skg_spectra(skg_ctx* c, int cap, double* k, double* E, double* T, double* D,
             }
         }
     }
-    cudaFree(st);
-    cudaFree(d3);
+    skg::dfree(st);
+    skg::dfree(d3);
     return rc;
 }
 
@@ -622,13 +622,13 @@ static int plan_run(int rank, const int* shape, const double* in, double* out, i
     std::lock_guard<std::mutex> lk(g_plan_mu);
     PlanBufs& b = g_plan_bufs[device];
     if (b.P < P || b.S < S) {
-        cudaFree(b.u);
-        cudaFree(b.h);
-        cudaFree(b.w);
+        skg::dfree(b.u);
+        skg::dfree(b.h);
+        skg::dfree(b.w);
         b = PlanBufs{};
-        CUDA_TRY(cudaMalloc(&b.u, sizeof(double) * P));
-        CUDA_TRY(cudaMalloc(&b.h, sizeof(cd) * S));
-        CUDA_TRY(cudaMalloc(&b.w, sizeof(cd) * S));
+        CUDA_TRY(skg::dmalloc(&b.u, sizeof(double) * P));
+        CUDA_TRY(skg::dmalloc(&b.h, sizeof(cd) * S));
+        CUDA_TRY(skg::dmalloc(&b.w, sizeof(cd) * S));
         b.P = P;
         b.S = S;
     }
@@ -730,10 +730,10 @@ int skg_set_forcing(skg_ctx* c, int enable, double k_lo, double k_hi, double rat
     CUDA_TRY(cudaSetDevice(c->device));
     if (int rc = ensure_fft_bufs(c)) return rc;
     if (!c->f_ref) {
-        CUDA_TRY(cudaMalloc(&c->f_ref, sizeof(cd) * c->S * c->nvars));
-        CUDA_TRY(cudaMalloc(&c->f_red, 8 * sizeof(double)));
+        CUDA_TRY(skg::dmalloc(&c->f_ref, sizeof(cd) * c->S * c->nvars));
+        CUDA_TRY(skg::dmalloc(&c->f_red, 8 * sizeof(double)));
         CUDA_TRY(cudaMallocHost(&c->f_noise, sizeof(double) * c->P * c->nvars));
-        if (c->solver == 2 && !c->generic) CUDA_TRY(cudaMalloc(&c->f_cm, sizeof(cd) * c->S));
+        if (c->solver == 2 && !c->generic) CUDA_TRY(skg::dmalloc(&c->f_cm, sizeof(cd) * c->S));
     }
     c->forcing = true;
     c->f_klo = k_lo;
@@ -772,6 +772,7 @@ static const int kIpcBytes = 4 * (int)sizeof(cudaIpcMemHandle_t);
 int skg_dist_ipc_handle(skg_ctx* c, char* out) {
     if (!c->dist || c->G < 2 || c->parts.size() != 1)
         return fail(SKG_EUNSUPPORTED, "IPC handles: one slab partition per process");
+    if (skg::guards_enabled()) return fail(SKG_EUNSUPPORTED, "IPC handles: not with SKG_GUARD=1 (offset allocations)");
     CUDA_TRY(cudaSetDevice(c->device));
     if (int rc = ensure_p2p_bufs(c)) return rc;
     const Part& p = c->parts[0];
@@ -824,10 +825,12 @@ int skg_dist_open_peers(skg_ctx* c, const char* all) {
         c->peer_rA[q][0] = ptr[2];
         c->peer_rA[q][1] = ptr[3];
     }
-    if (!c->d_barrier) CUDA_TRY(cudaMalloc(&c->d_barrier, sizeof(double)));
+    if (!c->d_barrier) CUDA_TRY(skg::dmalloc(&c->d_barrier, sizeof(double)));
     c->p2p = true;
     return SKG_OK;
 }
+
+long skg_guard_violations(void) { return skg::guard_violations(); }
 
 int skg_dist_overlap(skg_ctx* c, int enable) {
     if (!c->dist) return fail(SKG_EUNSUPPORTED, "exchange overlap: slab-decomposed contexts");

@@ -2,7 +2,9 @@
 // diagnostic reductions.
 #include "skg_internal.h"
 
+#include <cstdlib>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <utility>
 
@@ -284,6 +286,70 @@ cudaError_t launch_energy(const cd* f, int dims, const int* n, const double* ksc
     return cudaGetLastError();
 }
 
+namespace {
+constexpr size_t kGuard = 65536;
+constexpr unsigned char kGuardByte = 0xA5;
+std::mutex g_guard_mu;
+std::map<void*, std::pair<void*, size_t>> g_guarded;  // user pointer -> (base, bytes)
+}  // namespace
+
+bool guards_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SKG_GUARD");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+cudaError_t dmalloc_raw(void** p, size_t bytes) {
+    if (!guards_enabled()) return cudaMalloc(p, bytes);
+    void* base = nullptr;
+    SKG_TRY(cudaMalloc(&base, bytes + 2 * kGuard));
+    char* b = static_cast<char*>(base);
+    SKG_TRY(cudaMemset(b, kGuardByte, kGuard));
+    SKG_TRY(cudaMemset(b + kGuard + bytes, kGuardByte, kGuard));
+    SKG_TRY(cudaDeviceSynchronize());
+    *p = b + kGuard;
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    g_guarded[*p] = {base, bytes};
+    return cudaSuccess;
+}
+
+void dfree(void* p) {
+    if (!p) return;
+    if (guards_enabled()) {
+        std::lock_guard<std::mutex> lock(g_guard_mu);
+        auto it = g_guarded.find(p);
+        if (it != g_guarded.end()) {
+            cudaFree(it->second.first);
+            g_guarded.erase(it);
+            return;
+        }
+    }
+    cudaFree(p);
+}
+
+long guard_violations() {
+    if (!guards_enabled()) return 0;
+    std::lock_guard<std::mutex> lock(g_guard_mu);
+    std::vector<unsigned char> h(kGuard);
+    long bad = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (const auto& kv : g_guarded) {
+        const char* b = static_cast<const char*>(kv.second.first);
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, b) == cudaSuccess) cudaSetDevice(at.device);
+        for (int side = 0; side < 2; ++side) {
+            const char* g = side == 0 ? b : b + kGuard + kv.second.second;
+            if (cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+            for (unsigned char v : h) bad += v != kGuardByte;
+        }
+    }
+    cudaSetDevice(cur);
+    return bad;
+}
+
 cudaError_t ensure_smem(const void* kernel, size_t bytes) {
     if (bytes <= 48 * 1024) return cudaSuccess;
     int dev = 0;
@@ -303,7 +369,7 @@ cudaError_t fp64_peak(int device, double* dfma_per_s) {
     int sms = 0;
     SKG_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     double* d = nullptr;
-    SKG_TRY(cudaMalloc(&d, sizeof(double)));
+    SKG_TRY(dmalloc(&d, sizeof(double)));
     cudaEvent_t e0, e1;
     SKG_TRY(cudaEventCreate(&e0));
     SKG_TRY(cudaEventCreate(&e1));
@@ -322,7 +388,7 @@ cudaError_t fp64_peak(int device, double* dfma_per_s) {
     cudaError_t err = cudaGetLastError();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaFree(d);
+    dfree(d);
     if (err != cudaSuccess) return err;
     *dfma_per_s = (double)blocks * threads * 8.0 * iters / (best * 1e-3);
     return cudaSuccess;
