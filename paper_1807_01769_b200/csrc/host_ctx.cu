@@ -168,16 +168,6 @@ int env_opt() {
     return v;
 }
 
-// SKG_CHAIN=0 runs the y-inverse, z and y-forward of ns3d as three launches
-// instead of the chained persistent pass (A/B timing).
-bool chain_enabled() {
-    static const bool v = [] {
-        const char* e = std::getenv("SKG_CHAIN");
-        return !(e && e[0] == '0');
-    }();
-    return v;
-}
-
 int sm_count(int device) {
     int n = 148;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
@@ -327,7 +317,6 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.kstart = c->d_cstart;
     a.slab = 0;
     a.sz = c->nh;
-    a.chain = chain_enabled() ? c->chain : nullptr;
     return a;
 }
 

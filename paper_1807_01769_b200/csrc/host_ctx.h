@@ -115,7 +115,6 @@ struct skg_ctx {
     double* etab = nullptr;  // e1[axis], e2[axis] tables
     cd* tw[3] = {nullptr, nullptr, nullptr};
     skg::DevFlags* flags = nullptr;
-    int* chain = nullptr;  // ns3d chained y/z/y pass counters (Ns3dArgs::chain)
     unsigned long long* d_count = nullptr;
     double* d_red = nullptr;
 

@@ -460,7 +460,7 @@ struct ZBand {
 };
 
 // Raw inputs of one packed c2r (fields P, Q of a row; kept kz only).
-template <int NZ, bool ZB, bool CG = false>
+template <int NZ, bool ZB>
 __device__ __forceinline__ void fetch_pair(const Ns3dArgs& a, const cd* P, const cd* Q, size_t row,
                                            bool active, int t, cd* p, cd* q) {
     using F = typename Z3<NZ>::F;
@@ -476,13 +476,8 @@ __device__ __forceinline__ void fetch_pair(const Ns3dArgs& a, const cd* P, const
         p[e] = zero();
         q[e] = zero();
         if (active && ki < a.kz_in) {
-            if constexpr (CG) {
-                p[e] = __ldcg(P + row + ki);
-                q[e] = __ldcg(Q + row + ki);
-            } else {
-                p[e] = P[row + ki];
-                q[e] = Q[row + ki];
-            }
+            p[e] = P[row + ki];
+            q[e] = Q[row + ki];
         }
     }
 }
@@ -556,10 +551,8 @@ __device__ __forceinline__ void z_store_pair(const Ns3dArgs& a, const cd* v, cd*
 
 // CFL: also reduce max |u_d| (adaptive dt, stage 1 only; a separate
 // instantiation so the common path carries no extra registers).
-// One tile of the z pass (G row pairs from bx).  CHAIN: the inputs were
-// written by other CTAs of the same (chained) launch, so they are read
-// through L2 (ld.global.cg) and the tile is already L2-resident (no prefetch).
-template <int NZ, bool CFL, bool ZB, bool CHAIN>
+// One tile of the z pass (G row pairs from bx).
+template <int NZ, bool CFL, bool ZB>
 __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E, G = Z3<NZ>::G;
@@ -576,7 +569,7 @@ __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx
     // input field pairs of the three packed inverse FFTs of a row
     const cd* FP[3] = {B + 2 * fs, B + 4 * fs, B + 0 * fs};
     const cd* FQ[3] = {B + 3 * fs, B + 5 * fs, B + 1 * fs};
-    if (active && !CHAIN) {  // the row pair of all six fields into L2 up front
+    if (active) {  // the row pair of all six fields into L2 up front
         const size_t bytes = sizeof(cd) * 2 * a.kz_in;
         for (int f = 0; f < 6; ++f)
             l2_prefetch(B + f * fs + (size_t)r0 * a.kz_in, bytes, t, T);
@@ -589,7 +582,7 @@ __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx
         const size_t row = (size_t)(r0 + rr) * a.kz_in;
         cd v[E];
         // w + i wx
-        fetch_pair<NZ, ZB, CHAIN>(a, FP[0], FQ[0], row, active, t, p, q);
+        fetch_pair<NZ, ZB>(a, FP[0], FQ[0], row, active, t, p, q);
         pack_pair<NZ, ZB>(t, p, q, v);
         F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
@@ -598,7 +591,7 @@ __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx
             st[1 * NZ + t + T * e] = v[e].y;
         }
         // wy + i wz
-        fetch_pair<NZ, ZB, CHAIN>(a, FP[1], FQ[1], row, active, t, p, q);
+        fetch_pair<NZ, ZB>(a, FP[1], FQ[1], row, active, t, p, q);
         pack_pair<NZ, ZB>(t, p, q, v);
         F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
@@ -607,7 +600,7 @@ __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx
             st[3 * NZ + t + T * e] = v[e].y;
         }
         // u + i v, then the cross product (solvers.cpp:321-325)
-        fetch_pair<NZ, ZB, CHAIN>(a, FP[2], FQ[2], row, active, t, p, q);
+        fetch_pair<NZ, ZB>(a, FP[2], FQ[2], row, active, t, p, q);
         pack_pair<NZ, ZB>(t, p, q, v);
         F::template run<+1>(v, sm, t, wb, 0, bar);
 #pragma unroll
@@ -638,7 +631,6 @@ __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx
     F::template run<-1>(v, sm, t, wb, 0, bar);
     cd* oa = a.A + 2 * fs + (size_t)r0 * a.kz_o;
     z_store_pair<NZ, ZB>(a, v, sm, t, bar, active, oa, oa + a.kz_o, h);
-    if constexpr (CHAIN) __syncthreads();  // smem free for the next tile
 }
 
 template <int NZ, bool CFL, bool ZB>
@@ -646,14 +638,13 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
     extern __shared__ cd smem[];
     pdl_wait();
     if (cta_diverged(a.flags)) return;
-    z_tile<NZ, CFL, ZB, false>(a, smem, blockIdx.x);
+    z_tile<NZ, CFL, ZB>(a, smem, blockIdx.x);
 }
 
 // ------------------------------------------------------------------ y-forward
 // ZB: kcy < 3 NY / 8, so the outputs e in [3E/8, 5E/8) are masked (not stored)
 // One tile of the y-forward: x row and kz block from bx, fields m0..m1.
-// CHAIN: inputs written by the same launch, read through L2.
-template <int NY, int CT, bool ZB, bool CHAIN>
+template <int NY, int CT, bool ZB>
 __device__ __forceinline__ void yf_tile(const Ns3dArgs& a, cd* smem, int bx, int m0, int m1) {
     using F = BF3<NY>;
     constexpr int T = F::T, E = F::E, C = Strided<NY, CT>::C;
@@ -675,10 +666,8 @@ __device__ __forceinline__ void yf_tile(const Ns3dArgs& a, cd* smem, int bx, int
         const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
         cd v[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const cd* src = in + ((size_t)x * a.ny + (t + T * e)) * a.kz_o + kz;
-            v[e] = active ? (CHAIN ? __ldcg(src) : *src) : zero();
-        }
+        for (int e = 0; e < E; ++e)
+            v[e] = active ? in[((size_t)x * a.ny + (t + T * e)) * a.kz_o + kz] : zero();
         F::template run<-1>(v, sm, t, wb, salt);
         if (active) {
             cd* out = a.slab ? a.sD + m * a.rfs
@@ -695,7 +684,6 @@ __device__ __forceinline__ void yf_tile(const Ns3dArgs& a, cd* smem, int bx, int
         }
     }
     if (a.p2p) __threadfence_system();
-    if constexpr (CHAIN) __syncthreads();  // smem free for the next tile
 }
 
 template <int NY, int CT = 256, bool ZB = false>
@@ -705,7 +693,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
     if (cta_diverged(a.flags)) return;
     // one field per CTA
     const int m0 = a.comp0 + blockIdx.y;
-    yf_tile<NY, CT, ZB, false>(a, smem, blockIdx.x, m0, m0 + 1);
+    yf_tile<NY, CT, ZB>(a, smem, blockIdx.x, m0, m0 + 1);
 }
 
 // ------------------------------------------------------------------ x-forward + RK
@@ -984,137 +972,6 @@ cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
 }
 
 
-// ------------------------------------------------------------------ chained y/z/y
-// The y-inverse, z pass and y-forward of one RK stage as ONE persistent
-// launch.  Work items are the three kernels' tiles, ordered by x plane with a
-// lookahead: slot s holds the y-inverse tiles of plane s, the z tiles of
-// plane s - L and the y-forward tiles of plane s - 2L.  CTAs take items in
-// order from an atomic counter; a z tile of plane p first waits until every
-// y-inverse tile of p has completed (per-plane counter), a y-forward tile
-// until every z tile of p has.  A waited-on item always has a smaller index,
-// so it was taken by a running CTA and the wait cannot deadlock.  The plane's
-// intermediates (6 + 3 fields, 12.6 MB per 512^3 plane) are consumed while
-// L2-resident, and y-inverse (load-latency bound) and z (shared-memory / FP64
-// bound) tiles share each SM.  The last CTA to exit zeroes the counters for
-// the next launch.  Full (unpartitioned) layout, ny == nz, dealiased state.
-constexpr int kChainLookahead = 4;
-
-template <int N>
-struct Chain {
-    using SY = Strided<N, 256>;
-    using FZ = Z3<N>;
-    static_assert(SY::T * SY::C == 256 && FZ::T * FZ::G == 256, "256-thread tiles");
-    static constexpr size_t smem_y(int K) {
-        return sizeof(cd) * ((size_t)BF3<N>::SMEM * SY::C + (size_t)K * SY::C) + sizeof(int) * N;
-    }
-    static constexpr size_t smem_z() { return sizeof(cd) * FZ::SLOT * FZ::G; }
-    static constexpr size_t smem_f() { return sizeof(cd) * BF3<N>::SMEM * SY::C + 2 * sizeof(int) * N; }
-};
-
-__device__ __forceinline__ void chain_wait(const int* ctr, int target) {
-    if (threadIdx.x == 0) {
-        int v;
-        for (;;) {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (v >= target) break;
-            __nanosleep(200);
-        }
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ void chain_done(int* ctr) {
-    __threadfence();  // this thread's tile stores, device-wide
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(ctr, 1);
-}
-
-template <int N, bool CFL>
-__global__ void __launch_bounds__(256, 2) k_yzy_chain(Ns3dArgs a) {
-    extern __shared__ cd smem[];
-    __shared__ int s_item;
-    pdl_wait();
-    int* next = a.chain;
-    int* exited = a.chain + 1;
-    int* doneY = a.chain + 2;
-    int* doneZ = a.chain + 2 + a.nx;
-    const int nkzb_i = (a.kz_in + Chain<N>::SY::C - 1) / Chain<N>::SY::C;
-    const int nkzb_o = (a.kz_o + Chain<N>::SY::C - 1) / Chain<N>::SY::C;
-    const int nY = 2 * nkzb_i, nZ = (a.ny / 2) / Chain<N>::FZ::G, nF = 3 * nkzb_o;
-    const int Q = nY + nZ + nF;
-    const int total = (a.nx + 2 * kChainLookahead) * Q;
-    if (!cta_diverged(a.flags)) {
-        for (;;) {
-            if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
-            __syncthreads();
-            const int item = s_item;
-            __syncthreads();
-            if (item >= total) break;
-            const int slot = item / Q, r = item % Q;
-            if (r < nY) {
-                const int p = slot;
-                if (p >= a.nx) continue;
-                const int half = r / nkzb_i;
-                y_inv_tile<N, 256, true>(a, smem, p * nkzb_i + r % nkzb_i, 3 * half, 3 * half + 3);
-                chain_done(doneY + p);
-            } else if (r < nY + nZ) {
-                const int p = slot - kChainLookahead;
-                if (p < 0 || p >= a.nx) continue;
-                chain_wait(doneY + p, nY);
-                z_tile<N, CFL, true, true>(a, smem, (long long)p * nZ + (r - nY));
-                chain_done(doneZ + p);
-            } else {
-                const int p = slot - 2 * kChainLookahead;
-                if (p < 0 || p >= a.nx) continue;
-                chain_wait(doneZ + p, nZ);
-                const int q = r - nY - nZ, m = q / nkzb_o;
-                yf_tile<N, 256, true, true>(a, smem, p * nkzb_o + q % nkzb_o, m, m + 1);
-            }
-        }
-    }
-    // the last CTA out resets the counters for the next launch
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(exited, 1) == (int)gridDim.x - 1) {
-            for (int i = 0; i < 2 * a.nx; ++i) doneY[i] = 0;
-            *next = 0;
-            __threadfence();
-            *exited = 0;
-        }
-    }
-}
-
-template <int N>
-cudaError_t launch_chain_n(const Ns3dArgs& a, cudaStream_t s) {
-    const int K = 2 * a.kcy + 1;
-    size_t smem = Chain<N>::smem_y(K);
-    if (Chain<N>::smem_z() > smem) smem = Chain<N>::smem_z();
-    if (Chain<N>::smem_f() > smem) smem = Chain<N>::smem_f();
-    const int grid = a.wave;  // resident CTAs: 2 per SM
-    if (a.dyn && a.ystage == 1) SKG_TRY(launch_pdl(k_yzy_chain<N, true>, grid, 256, smem, s, a));
-    else SKG_TRY(launch_pdl(k_yzy_chain<N, false>, grid, 256, smem, s, a));
-    return cudaGetLastError();
-}
-
-// The chained pass applies to the full-layout dealiased path of cubic-in-(y,z)
-// grids with 256-thread tiles of every kind (N = 256, 512).
-bool chain_ok(const Ns3dArgs& a) {
-    if (!a.chain || a.slab || a.p2p || !a.pruned || a.ny != a.nz) return false;
-    if (a.ny != 256 && a.ny != 512) return false;
-    const bool zby = 8 * a.kcy < 3 * a.ny;
-    const bool zbz = 8 * a.kz_in <= 3 * a.nz && 8 * a.kz_o <= 3 * a.nz;
-    return zby && zbz;
-}
-
-cudaError_t launch_chain(const Ns3dArgs& a, cudaStream_t s) {
-    switch (a.ny) {
-        case 256: return launch_chain_n<256>(a, s);
-        case 512: return launch_chain_n<512>(a, s);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
 #define SKG3_CASES(X) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
 cudaError_t dispatch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
@@ -1177,13 +1034,6 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
     } else if (pass == 1 || pass == 3 || pass == 4) {
         Ns3dArgs b = a;  // the z pass of stage 1 feeds the CFL max
         b.ystage = stage;
-        if (pass == 1 && chain_ok(a)) {
-            hook.begin(1);
-            if ((err = launch_chain(b, s)) != cudaSuccess) return err;
-            hook.end(1, B * (5.0 * a.nrl * kyk * a.kz_in + 3.0 * a.nrl * kyk * a.kz_o));
-            *launches += 1;
-            return cudaSuccess;
-        }
         if (pass != 4) {
             hook.begin(3);
             if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;

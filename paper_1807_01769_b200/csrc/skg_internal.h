@@ -196,10 +196,6 @@ struct Ns3dArgs {
     int ystage;         // RK stage of the physical pass (stage 1 feeds the CFL max)
     int comp0 = 0;      // x-inverse / y-forward launches: components [comp0, comp0 + ncomp)
     int ncomp = 3;
-    // chained y-inverse -> z -> y-forward (one persistent launch, dataflow
-    // over x planes): 2 + 2 nx ints (next item, exited CTAs, per-plane
-    // y-inverse and z completion counts), zero between launches; nullptr: off
-    int* chain = nullptr;
     const cd* force;    // forcing addend in the state layout (nullptr: off)
     const double *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
     cd* u;               // 3 variables, each nx*ny*nh (reference layout)

@@ -229,8 +229,6 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
         else c->inter_elems = 11 * (size_t)n[0] * n[1] * c->nh;  // A[5] (C aliases) + B[6] (D aliases)
         if (c->generic) c->inter_elems = 1;
         ok = ok && alloc((void**)&c->inter, sizeof(cd) * c->inter_elems);
-        // counters of the chained y/z/y pass (zeroed; self-resetting)
-        if (sid == 3 && !c->generic) ok = ok && alloc((void**)&c->chain, sizeof(int) * (2 + 2 * (size_t)n[0]));
         if (c->generic) {
             const size_t P = (size_t)c->P;
             ok = ok && alloc((void**)&c->gs.w, sizeof(cd) * S * c->nvars);
@@ -274,7 +272,6 @@ int skg_destroy(skg_ctx* c) {
     skg::dfree(c->work);
     skg::dfree(c->etab);
     skg::dfree(c->flags);
-    skg::dfree(c->chain);
     skg::dfree(c->d_count);
     skg::dfree(c->d_red);
     skg::dfree(c->d_dyn);

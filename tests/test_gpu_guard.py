@@ -1,7 +1,7 @@
 """Out-of-bounds write check of every kernel class (compute-sanitizer is
 refused on the GPU pool): the small step cases of tools/sanitize_case.py --
 general and fast ns2d kernels, ns3d passes, slab emulation with the copy,
-overlapped-copy and peer-memory exchanges, the chained ns3d pass -- run in a
+overlapped-copy and peer-memory exchanges -- run in a
 subprocess with SKG_GUARD=1, where every device allocation has 64 KB guard
 zones; no guard byte may change."""
 import os
@@ -21,7 +21,6 @@ def test_no_guard_zone_writes():
         "import sanitize_case as sc\n"
         "from paper_1807_01769_b200 import api\n"
         "for c in sorted(sc.CASES): sc.main(c)\n"
-        "sc.main_chain()\n"
         "print('violations', api.guard_violations())\n"
         "assert api.guard_violations() == 0\n" % (str(ROOT), str(ROOT / "tools")))
     env = dict(os.environ, SKG_GUARD="1")

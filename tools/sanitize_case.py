@@ -48,18 +48,6 @@ def main(name):
     print(name, "ok")
 
 
-def main_chain():
-    """The chained ns3d y/z/y pass (256^3, 3 steps incl. graph replay)."""
-    n = (256, 256, 256)
-    u0 = ic.ns3d_ic(n, seed=3)
-    s = api.Simulation("ns3d", n, 1e-3, ic.cfl_dt("ns3d", n, u0))
-    s.set_state(u0)
-    s.step(5)
-    assert np.all(np.isfinite(s.get_state().view(np.float64)))
-    s.close()
-    print("chain ok")
-
-
 if __name__ == "__main__":
     for c in sys.argv[1:] or sorted(CASES):
         main(c)

@@ -3,7 +3,7 @@
 cfg=$1; rounds=$2; shift 2
 for r in $(seq $rounds); do
 for v in "$@"; do
-  SKG_LIB_VARIANT=$v timeout 300 python bench.py --config $cfg --steps ${STEPS:-100} --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/var_${cfg}_$v.log 2>&1
+  SKG_LIB_VARIANT=$([ "$v" = base ] && echo "" || echo $v) timeout 300 python bench.py --config $cfg --steps ${STEPS:-100} --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/var_${cfg}_$v.log 2>&1
   python - "$v" gpurun_out/var_${cfg}_$v.log <<'PY'
 import json,sys
 try:
