@@ -69,7 +69,22 @@ def report(rep: Path, out: Path):
     else:
         txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
                              text=True).stdout
-    rows = list(csv.reader(txt.splitlines()))
+    # drop ncu's ==PROF== / ==WARNING== banner lines of --log-file captures
+    rows = [r for r in csv.reader(l for l in txt.splitlines() if not l.startswith("=="))]
+    if "Metric Name" in rows[0]:  # `ncu --metrics ... --csv` launch-per-metric rows: pivot
+        h = rows[0]
+        i_id, i_k, i_m, i_u, i_v = (h.index(x) for x in ("ID", "Kernel Name", "Metric Name",
+                                                          "Metric Unit", "Metric Value"))
+        launch = collections.OrderedDict()
+        unit = {}
+        for r in rows[1:]:
+            if len(r) <= i_v:
+                continue
+            launch.setdefault(r[i_id], {"Kernel Name": r[i_k]})[r[i_m]] = r[i_v]
+            unit[r[i_m]] = r[i_u]
+        names = ["Kernel Name"] + sorted(unit)
+        rows = [names, [""] + [unit[n] for n in names[1:]]] + [
+            [d.get(n, "") for n in names] for d in launch.values()]
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     kern = []
