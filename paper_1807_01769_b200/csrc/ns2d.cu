@@ -143,6 +143,8 @@ struct XCfg {
     // thread (512-thread lines of 8192: one CTA, its shared memory is ~224 KB)
     static constexpr int MINB = CT >= 512 ? 1 : CT >= 256 ? 2 : (512 / CT > 32 ? 32 : 512 / CT);
     static constexpr int ZLO = EM == 16 ? 6 : 3, ZHI = EM == 16 ? 10 : 5;
+    static constexpr int NSL = EM == 16 ? 12 : 6;  // kept slots per thread
+    static constexpr int XF_SLOT = F::SMEM + NSL * T;  // fused x-forward: cd per line
 };
 
 template <int NX, bool PZ, int NM, int EM = 16, int CTW = 256>
@@ -499,12 +501,11 @@ __global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false,
     const int slot = F::SMEM + 2 * ld;
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const int bar = G > 1 ? g + 1 : 0;  // the groups' own barriers (line_sync)
+    const typename F::Bases wb = F::bases(t, a.twy);  // constant table: before the wait
     pdl_wait();
-    if (cta_diverged(a.flags)) return;
-    if (a.ystage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
+    const int dflag = *reinterpret_cast<const volatile int*>(&a.flags->diverged);
     cd* sm = smem + g * slot;
     cd* st = sm + F::SMEM;
-    const typename F::Bases wb = F::bases(t, a.twy);
     const int stride = gridDim.x * G;
     const cd* P = a.rI[0];  // X[psi]
     const cd* Q = a.rI[1];  // X[kx psi]
@@ -538,6 +539,13 @@ __global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false,
     int x = blockIdx.x * G + g;
     issue(x);
     cp_async_commit();
+    // divergence flag, one value per CTA (cta_diverged), checked with the
+    // first row's loads in flight
+    if (__syncthreads_or(dflag) != 0) {
+        cp_async_wait_all();
+        return;
+    }
+    if (a.ystage == 1 && blockIdx.x == 0 && threadIdx.x == 0 && a.lead) atomicAdd(&a.flags->steps, 1);
     const double h = 0.5 * a.inv_n;
     constexpr bool cfl = CFL;  // max |u_d| of the step's initial state (adaptive dt)
     double mx = 0.0, my = 0.0;
@@ -713,11 +721,9 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
     const int kyl = blockIdx.x * LPC + l;  // local column
     const int ky = a.c0 + kyl;
     const bool active = kyl < a.ncols;
-    pdl_wait();
-    if (cta_diverged(a.flags)) return;
-    cd* sm = smem + l * (F::SMEM + NS * T);
+    const typename F::Bases wb = F::bases(t, a.twx);  // constant table: before the wait
+    cd* sm = smem + l * XCfg<NX, EM, CTW>::XF_SLOT;
     cd* sv = sm + F::SMEM;
-    const typename F::Bases wb = F::bases(t, a.twx);
     const double kyv = a.ky_scale * (double)ky;
     const size_t blk = (size_t)2 * ((a.ncols + 1) >> 1) * a.nrl;  // receive block per source
     auto ridx = [&](int x) {
@@ -725,10 +731,16 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
         return ro * blk + ((size_t)(kyl >> 1) * a.nrl + xl) * 2 + (kyl & 1);
     };
     const bool final = a.rk2 ? stage == 2 : stage == 4;
+    const bool fuse = FUSE && next;
+    pdl_wait();
+    const int dflag = *reinterpret_cast<const volatile int*>(&a.flags->diverged);
     cd v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e)
         v[e] = active ? a.rA[0][ridx(t + T * e)] : zero();
+    // divergence flag, one value per CTA (cta_diverged), checked after the
+    // input loads are in flight
+    if (__syncthreads_or(dflag) != 0) return;
     F::template run<-1>(v, sm, t, wb);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -750,7 +762,6 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
         const cd u0 = a.u[(size_t)kyl * NX];  // mean mode: untouched, enstrophy only
         sZ += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
     }
-    const bool fuse = FUSE && next;
     const double e1y = a.has_sigma ? a.e1y[ky] : 1.0, e2y = a.has_sigma ? a.e2y[ky] : 1.0;
     // chunks of CH kept modes: the chunk's operand loads, then its arithmetic
     // (CH = 2 spills at 4096 and measured 262 vs 212 us)
@@ -899,7 +910,7 @@ cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     using F = typename C::F;
     constexpr int T = F::T;
     constexpr int LPC = C::LPC;
-    const size_t smem = sizeof(cd) * (F::SMEM + (F::E - (C::ZHI - C::ZLO)) * T) * LPC;
+    const size_t smem = sizeof(cd) * C::XF_SLOT * LPC;
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
     SKG_TRY(launch_pdl(k4b_xfwd<NX, EM, CTW, FUSE>, grid, T * LPC, smem, s,

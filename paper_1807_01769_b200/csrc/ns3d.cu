@@ -100,6 +100,31 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 #define SKG3_Z_HERM 0
 #endif
 
+// z pass inputs staged in shared memory by bulk (TMA 1D) copies on an
+// mbarrier, one packed pair ahead, so the loads of the next pair land while
+// the current FFT runs (the register-fetch variant waits on them: long
+// scoreboard was the z pass's top stall); the second inverse FFT's output
+// (wy + i wz) stays in registers instead of two shared-memory rows.
+// Measured (ms/step, B200): 512^3 31.52 -> 30.74 with 3 row-pair groups per
+// CTA (168 registers, no spills; two CTAs per SM) and the second inverse
+// output in shared memory, 30.50 with 2 groups (3 CTAs per SM), 30.38 with
+// one group per CTA (64 threads, 6 CTAs per SM: independent scheduling);
+// 256^3 3.82 -> 3.79 with 8 groups and that output in registers; 128^3
+// slower (0.574 -> 0.617) -- so 256 and 512 (1024: SKG3_ZSTAGE1024).
+#ifndef SKG3_ZSTAGE
+#define SKG3_ZSTAGE 1
+#endif
+#ifndef SKG3_ZG512
+#define SKG3_ZG512 1
+#endif
+#ifndef SKG3_ZSTAGE1024
+#define SKG3_ZSTAGE1024 0
+#endif
+template <int NZ>
+constexpr bool zstage() { return SKG3_ZSTAGE && (NZ == 256 || NZ == 512 || (NZ == 1024 && SKG3_ZSTAGE1024)); }
+template <int NZ>
+constexpr bool zreg() { return NZ == 256; }
+
 // Elements per thread of the strided (x, y) passes: 8 for N <= SKG3_EM8_MAX
 // (twice the threads per line; the small grids have too few lines to fill
 // the GPU with 16-element lines), else 16.  Measured (ms/step): 64^3
@@ -446,8 +471,21 @@ template <int NZ>
 struct Z3 {
     using F = BFFT<NZ, false, 8>;
     static constexpr int T = F::T;
-    static constexpr int G = NZ == 128 ? SKG3_ZG128 : T >= 256 ? 1 : 256 / T;
-    static constexpr int SLOT = F::SMEM + 5 * NZ / 2;  // exchange + 5 rows of doubles (cd units)
+    static constexpr int G = NZ == 128                      ? SKG3_ZG128
+                             : (NZ == 512 && zstage<NZ>())  ? SKG3_ZG512
+                             : (NZ == 1024 && zstage<NZ>()) ? 1
+                             : T >= 256                     ? 1
+                                                            : 256 / T;
+    static constexpr bool STG = zstage<NZ>(), REG = zreg<NZ>();
+    // resident CTAs: 2, or 6 groups per SM at 512 (168 registers)
+    static constexpr int MINB = (NZ == 512 && STG) ? 6 / G : (NZ == 1024 && STG) ? 3 : 2;
+    // exchange + 5 rows of doubles (cd units); staged: 3 rows when the
+    // second inverse output stays in registers, + the bulk-copy stage of
+    // one packed pair
+    static constexpr int KZS = NZ / 2 + 1;
+    static constexpr int SLOT = STG ? F::SMEM + (REG ? 3 : 5) * NZ / 2 + 2 * KZS : F::SMEM + 5 * NZ / 2;
+    // + one mbarrier per group (staged variant)
+    static constexpr size_t BYTES = sizeof(cd) * SLOT * G + (STG ? 16 * ((G + 1) / 2) : 0);
 };
 
 // ZB: kz_in, kz_o <= 3 NZ / 8 (dealiased states), so the row elements
@@ -633,12 +671,136 @@ __device__ __forceinline__ void z_tile(const Ns3dArgs& a, cd* smem, long long bx
     z_store_pair<NZ, ZB>(a, v, sm, t, bar, active, oa, oa + a.kz_o, h);
 }
 
+// Staged z tile: same arithmetic as z_tile, inputs through shared memory.
 template <int NZ, bool CFL, bool ZB>
-__global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, 2) k3_3d(Ns3dArgs a) {
+__device__ __forceinline__ void z_tile_s(const Ns3dArgs& a, cd* smem, long long bx) {
+    using Z = Z3<NZ>;
+    using F = typename Z::F;
+    constexpr int T = F::T, E = F::E, G = Z::G, KZS = Z::KZS;
+    constexpr int LO = ZBand<NZ, ZB>::LO, HI = ZBand<NZ, ZB>::HI;
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const long long r0 = 2ll * (bx * G + g);
+    const bool active = r0 < (long long)a.nrl * a.ny;
+    cd* sm = smem + g * Z::SLOT;
+    const int bar = G > 1 ? g + 1 : 0;
+    double* st = reinterpret_cast<double*>(sm + F::SMEM);  // rows: w, wx, cz_a (cz_b reuses w)
+    cd* stg = sm + F::SMEM + (Z::REG ? 3 : 5) * NZ / 2;  // P row, Q row of the next pair
+    unsigned long long* mb = reinterpret_cast<unsigned long long*>(smem + G * Z::SLOT) + g;
+    const typename F::Bases wb = F::bases(t, a.twz);
+    const cd* B = a.B;
+    const size_t fs = a.fstride;
+    const double h = 0.5 * a.inv_n;
+    const cd* FP[3] = {B + 2 * fs, B + 4 * fs, B + 0 * fs};
+    const cd* FQ[3] = {B + 3 * fs, B + 5 * fs, B + 1 * fs};
+    const unsigned bytes = 16u * (unsigned)a.kz_in;
+    auto issue = [&](int k) {  // packed pair k = 3 rr + pr (one thread)
+        const size_t row = (size_t)(r0 + k / 3) * a.kz_in;
+        mbar_expect_tx(mb, 2 * bytes);
+        bulk_g2s(stg, FP[k % 3] + row, bytes, mb);
+        bulk_g2s(stg + KZS, FQ[k % 3] + row, bytes, mb);
+    };
+    if (t == 0) mbar_init(mb, 1);
+    line_sync<T>(bar);
+    if (active && t == 0) {
+        const size_t rb = sizeof(cd) * 2 * a.kz_in;  // the rest of the row pair into L2
+        for (int f = 0; f < 6; ++f)
+            if (f != 2 && f != 3) l2_prefetch(B + f * fs + (size_t)r0 * a.kz_in, rb, 0, 1);
+        issue(0);
+    }
+    unsigned phase = 0;
+    // packed spectrum of pair k from the stage; then the stage is released
+    // and pair k + 1 requested
+    auto fetch = [&](int k, cd* v) {
+        if (active) mbar_wait(mb, phase);
+        phase ^= 1u;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (e >= LO && e < HI) {
+                v[e] = zero();
+                continue;
+            }
+            const int idx = t + T * e;
+            const bool mirror = idx > NZ / 2;
+            const int ki = mirror ? NZ - idx : idx;
+            cd pp = zero(), qq = zero();
+            if (active && ki < a.kz_in) {
+                pp = stg[ki];
+                qq = stg[KZS + ki];
+                if (ki == 0 || 2 * ki == NZ) {  // c2r ignores these imaginary parts
+                    pp.y = 0.0;
+                    qq.y = 0.0;
+                }
+            }
+            v[e] = mirror ? mk(pp.x + qq.y, qq.x - pp.y) : mk(pp.x - qq.y, pp.y + qq.x);
+        }
+        line_sync<T>(bar);
+        if (active && t == 0 && k < 5) issue(k + 1);
+    };
+    constexpr bool cfl = CFL;
+    double mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll 1
+    for (int rr = 0; rr < 2; ++rr) {
+        cd v[E];
+        fetch(3 * rr, v);  // w + i wx
+        F::template run<+1>(v, sm, t, wb, 0, bar);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            st[0 * NZ + t + T * e] = v[e].x;
+            st[1 * NZ + t + T * e] = v[e].y;
+        }
+        cd w2[Z::REG ? E : 1];
+        if constexpr (Z::REG) {
+            fetch(3 * rr + 1, w2);  // wy + i wz, kept in registers
+            F::template run<+1>(w2, sm, t, wb, 0, bar);
+        } else {
+            fetch(3 * rr + 1, v);  // wy + i wz
+            F::template run<+1>(v, sm, t, wb, 0, bar);
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                st[3 * NZ + t + T * e] = v[e].x;
+                st[4 * NZ + t + T * e] = v[e].y;
+            }
+        }
+        fetch(3 * rr + 2, v);  // u + i v, then the cross product (solvers.cpp:321-325)
+        F::template run<+1>(v, sm, t, wb, 0, bar);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int y = t + T * e;
+            const double ux = v[e].x, uy = v[e].y;
+            const double uz = st[0 * NZ + y], ox = st[1 * NZ + y];
+            if constexpr (cfl) {
+                mx = fmax(mx, fabs(ux));
+                my = fmax(my, fabs(uy));
+                mz = fmax(mz, fabs(uz));
+            }
+            const double oy = Z::REG ? w2[Z::REG ? e : 0].x : st[3 * NZ + y];
+            const double oz = Z::REG ? w2[Z::REG ? e : 0].y : st[4 * NZ + y];
+            const double cx = uy * oz - uz * oy;
+            const double cy = uz * ox - ux * oz;
+            const double cz = ux * oy - uy * ox;
+            v[e] = mk(cx, cy);
+            st[(rr == 0 ? 2 : 0) * NZ + y] = cz;  // row b reuses the dead w row
+        }
+        F::template run<-1>(v, sm, t, wb, 0, bar);
+        cd* o0 = a.A + (size_t)(r0 + rr) * a.kz_o;
+        z_store_pair<NZ, ZB>(a, v, sm, t, bar, active, o0, o0 + fs, h);
+    }
+    if constexpr (cfl) umax_accumulate(a.dyn, 3, mx, my, mz);
+    cd v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = mk(st[2 * NZ + t + T * e], st[0 * NZ + t + T * e]);
+    F::template run<-1>(v, sm, t, wb, 0, bar);
+    cd* oa = a.A + 2 * fs + (size_t)r0 * a.kz_o;
+    z_store_pair<NZ, ZB>(a, v, sm, t, bar, active, oa, oa + a.kz_o, h);
+}
+
+template <int NZ, bool CFL, bool ZB>
+__global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, Z3<NZ>::MINB) k3_3d(Ns3dArgs a) {
     extern __shared__ cd smem[];
     pdl_wait();
     if (cta_diverged(a.flags)) return;
-    z_tile<NZ, CFL, ZB>(a, smem, blockIdx.x);
+    if constexpr (Z3<NZ>::STG) z_tile_s<NZ, CFL, ZB>(a, smem, blockIdx.x);
+    else z_tile<NZ, CFL, ZB>(a, smem, blockIdx.x);
 }
 
 // ------------------------------------------------------------------ y-forward
@@ -950,7 +1112,7 @@ cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
 template <int NZ>
 cudaError_t launch_z3(const Ns3dArgs& a, cudaStream_t s) {
     using Z = Z3<NZ>;
-    const size_t smem = sizeof(cd) * Z::SLOT * Z::G;
+    const size_t smem = Z::BYTES;
     const long long pairs = (long long)a.nrl * a.ny / 2;
     const int grid = (int)((pairs + Z::G - 1) / Z::G);
     // zero band (dealiased states): kept kz of both directions below 3 NZ / 8

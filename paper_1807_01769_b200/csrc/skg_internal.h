@@ -258,6 +258,37 @@ __device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes, int t, 
     }
 }
 
+// Bulk (TMA 1D) global -> shared copies completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(bytes)
+                 : "memory");
+}
+// dst, src 16-byte aligned; bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mb))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W;\n"
+        "}\n" ::"r"(smem_u32(mb)),
+        "r"(parity)
+        : "memory");
+}
+
 // Warp-sum three doubles and add them to slot[0..2] (all 32 lanes must call).
 __device__ __forceinline__ void diag_accumulate(double* slot, double e, double z, double d) {
     for (int o = 16; o > 0; o >>= 1) {
