@@ -236,7 +236,7 @@ __device__ __forceinline__ void line_sync(int bar) {
 template <int N, bool SPLIT = false, int EMAX = 16>
 struct BFFT {
     static_assert((N & (N - 1)) == 0 && N >= 2, "power-of-two length");
-    static_assert(EMAX == 8 || EMAX == 16, "8 or 16 elements per thread");
+    static_assert(EMAX == 4 || EMAX == 8 || EMAX == 16, "4, 8 or 16 elements per thread");
     static constexpr int E = N < EMAX ? N : EMAX;  // elements per thread
     static constexpr int T = N / E;            // threads per line
     static constexpr int SH = ilog2c(E);
@@ -245,7 +245,7 @@ struct BFFT {
     // unit-stride reads are both conflict-free (no padding).
     static constexpr int SMEM = SPLIT ? (N + 1) / 2 : N;  // in cd (16-byte) units
     __device__ __forceinline__ static int pad(int i) {
-        if constexpr (E >= 8) return i ^ ((i >> SH) & 7);
+        if constexpr (E >= 4) return i ^ ((i >> SH) & 7);
         else return i;
     }
     // 8-byte slots: XOR the slot within each 128-byte line.

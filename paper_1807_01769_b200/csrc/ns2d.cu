@@ -42,6 +42,34 @@
 #ifndef SKG_FAST_X_EM
 #define SKG_FAST_X_EM 16
 #endif
+// 4 elements per thread (four times the threads per line) for the smallest
+// grids, 128 registers: x passes up to 512 (ms/step 256^2 0.0599 -> 0.0455,
+// 512^2 0.0589 -> 0.0525; 1024^2 slower, 0.1175 -> 0.1334), the y pass up to
+// 256 (256^2 -> 0.0432; 512^2 slower).  64 registers spill (slower).
+// Paired x-forward (k4p_xfwd) for NX in [SKG_PAIRED_X_MIN, SKG_PAIRED_X_MAX],
+// SKG_PAIRED_REGS registers per thread (80: three 256-thread CTAs per SM, no
+// spills).  Measured (ms/step): 1024^2 0.1173 -> 0.1119, 512^2 0.0524 ->
+// 0.0483; 2048^2 slower (0.420 -> 0.442: 683 columns, more than one wave);
+// 128 registers 0.1230 at 1024^2 (two CTAs per SM: two waves).
+#ifndef SKG_PAIRED_X_MIN
+#define SKG_PAIRED_X_MIN 512
+#endif
+#ifndef SKG_PAIRED_X_MAX
+#define SKG_PAIRED_X_MAX 1024
+#endif
+#ifndef SKG_PAIRED_REGS
+#define SKG_PAIRED_REGS 80
+#endif
+
+#ifndef SKG_EM4_REGS
+#define SKG_EM4_REGS 128
+#endif
+#ifndef SKG_X_EM4_MAX
+#define SKG_X_EM4_MAX 512
+#endif
+#ifndef SKG_Y_EM4_MAX
+#define SKG_Y_EM4_MAX 256
+#endif
 
 namespace skg {
 
@@ -141,11 +169,17 @@ struct XCfg {
     static constexpr int CT = T * LPC;
     // resident CTAs the register budget is sized for: <= 128 registers per
     // thread (512-thread lines of 8192: one CTA, its shared memory is ~224 KB)
-    static constexpr int MINB = CT >= 512 ? 1 : CT >= 256 ? 2 : (512 / CT > 32 ? 32 : 512 / CT);
-    static constexpr int ZLO = EM == 16 ? 6 : 3, ZHI = EM == 16 ? 10 : 5;
-    static constexpr int NSL = EM == 16 ? 12 : 6;  // kept slots per thread
-    static constexpr int XF_SLOT = F::SMEM + NSL * T;  // fused x-forward: cd per line
+    static constexpr int MINB = EM == 4 ? (CT >= 65536 / SKG_EM4_REGS ? 1 : 65536 / SKG_EM4_REGS / CT > 32 ? 32 : 65536 / SKG_EM4_REGS / CT)
+                               : CT >= 512 ? 1 : CT >= 256 ? 2 : (512 / CT > 32 ? 32 : 512 / CT);
+    // zero band of the dealiased kx (none with 4-element lines)
+    static constexpr int ZLO = EM == 16 ? 6 : EM == 8 ? 3 : F::E / 2, ZHI = EM == 16 ? 10 : EM == 8 ? 5 : F::E / 2;
 };
+// fused x-forward: shared memory per line (exchange + kept slots), cd units
+template <int N, int EM, int CTW>
+constexpr int xf_slot() {
+    using C = XCfg<N, EM, CTW>;
+    return C::F::SMEM + (C::F::E - (C::ZHI - C::ZLO)) * C::T;
+}
 
 template <int NX, bool PZ, int NM, int EM = 16, int CTW = 256>
 __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT,
@@ -483,7 +517,9 @@ __global__ void k4_decay(Ns2dArgs a) {
 // (85 / 64 registers, one wave of rows at 1024^2) spill and measured slower
 // (1024^2: 0.147 / 0.140 vs 0.117 ms/step), so 2.
 template <int NY, int EM>
-constexpr int y_minb() { return BFFT<NY, false, EM>::T > 256 ? 1 : EM == 16 ? 2 : SKG_Y8_MINB; }
+constexpr int y_minb() {
+    return BFFT<NY, false, EM>::T > 256 ? 1 : EM == 16 ? 2 : EM == 4 ? 256 / SKG_EM4_REGS : SKG_Y8_MINB;
+}
 
 template <int NY, bool CFL, int EM = 16>
 __global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false, EM>::T : 256,
@@ -495,7 +531,7 @@ __global__ void __launch_bounds__(BFFT<NY, false, EM>::T > 256 ? BFFT<NY, false,
     // per-thread zero band: row elements e in [6, 10) (E = 16; [3, 5) for
     // E = 8), |ky| in [3N/8, N/2], are masked on input and not needed on
     // output (fast_ok: ky_in, ld_o <= 3N/8)
-    constexpr int ZLO = E == 16 ? 6 : E == 8 ? 3 : E, ZHI = E == 16 ? 10 : E == 8 ? 5 : E;
+    constexpr int ZLO = E == 16 ? 6 : E == 8 ? 3 : E / 2, ZHI = E == 16 ? 10 : E == 8 ? 5 : E / 2;
     extern __shared__ cd smem[];
     const int ld = a.ld_i;
     const int slot = F::SMEM + 2 * ld;
@@ -715,14 +751,14 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
     using F = BFFT<NX, false, EM>;
     constexpr int T = F::T, E = F::E;
     constexpr int LPC = XCfg<NX, EM, CTW>::LPC;
-    constexpr int ZLO = XCfg<NX, EM>::ZLO, ZHI = XCfg<NX, EM>::ZHI, NS = E - (ZHI - ZLO);
+    constexpr int ZLO = XCfg<NX, EM>::ZLO, ZHI = XCfg<NX, EM>::ZHI;
     extern __shared__ cd smem[];
     const int l = threadIdx.x / T, t = threadIdx.x % T;
     const int kyl = blockIdx.x * LPC + l;  // local column
     const int ky = a.c0 + kyl;
     const bool active = kyl < a.ncols;
     const typename F::Bases wb = F::bases(t, a.twx);  // constant table: before the wait
-    cd* sm = smem + l * XCfg<NX, EM, CTW>::XF_SLOT;
+    cd* sm = smem + l * xf_slot<NX, EM, CTW>();
     cd* sv = sm + F::SMEM;
     const double kyv = a.ky_scale * (double)ky;
     const size_t blk = (size_t)2 * ((a.ncols + 1) >> 1) * a.nrl;  // receive block per source
@@ -829,6 +865,119 @@ __global__ void __launch_bounds__(XCfg<NX, EM, CTW>::CT, XCfg<NX, EM, CTW>::MINB
     }
 }
 
+// Paired x-forward for grids with few kept columns (one wave of columns):
+// one column per CTA and two line groups of T threads, group 0 on the
+// product spectrum A, group 1 on B, so the column's two forward FFTs run
+// side by side, and then (FUSE) the next stage's two x-inverse FFTs (psi and
+// kx psi) too: the column's critical path holds 2 FFTs instead of 4.  The
+// RK epilogue is split between the groups (kept slots [0, NS/2) in group 0,
+// the rest in group 1).  Same arithmetic per mode as k4b_xfwd (xf_point).
+template <int NX, int EM>
+struct XPCfg {
+    using C = XCfg<NX, EM, 1>;
+    using F = typename C::F;
+    static constexpr int T = F::T, CT = 2 * T;
+    static constexpr int NS = F::E - (C::ZHI - C::ZLO);  // kept slots per thread
+    static constexpr int MINB = 65536 / (CT * SKG_PAIRED_REGS) > 16 ? 16 : 65536 / (CT * SKG_PAIRED_REGS);
+    static constexpr size_t SMEM = sizeof(cd) * (2 * F::SMEM + 2 * NS * T);
+};
+
+template <int NX, int EM, bool FUSE>
+__global__ void __launch_bounds__(XPCfg<NX, EM>::CT, XPCfg<NX, EM>::MINB)
+    k4p_xfwd(Ns2dArgs a, int stage, int next) {
+    using P = XPCfg<NX, EM>;
+    using F = typename P::F;
+    constexpr int T = F::T, E = F::E, NS = P::NS;
+    constexpr int ZLO = P::C::ZLO, ZHI = P::C::ZHI;
+    extern __shared__ cd smem[];
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const int kyl = blockIdx.x;  // local column (grid = ncols)
+    const int ky = a.c0 + kyl;
+    const typename F::Bases wb = F::bases(t, a.twx);  // constant table: before the wait
+    cd* ex = smem + g * F::SMEM;  // the group's exchange buffer
+    cd* sa = smem + 2 * F::SMEM;  // kx ky A^, then psi of the next stage
+    cd* sb = sa + NS * T;         // (kx^2 - ky^2) B^
+    const int bar = g + 1;
+    const bool final = a.rk2 ? stage == 2 : stage == 4;
+    const bool fuse = FUSE && next;
+    const size_t col = (size_t)kyl * NX;
+    const double kyv = a.ky_scale * (double)ky;
+    const size_t blk = (size_t)2 * ((a.ncols + 1) >> 1) * a.nrl;  // receive block per source
+    pdl_wait();
+    const int dflag = *reinterpret_cast<const volatile int*>(&a.flags->diverged);
+    cd v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int x = t + T * e;
+        const int ro = x >> a.lg_nrl, xl = x & (a.nrl - 1);
+        v[e] = a.rA[g][ro * blk + ((size_t)(kyl >> 1) * a.nrl + xl) * 2 + (kyl & 1)];
+    }
+    if (__syncthreads_or(dflag) != 0) return;
+    F::template run<-1>(v, ex, t, wb, 0, bar);
+    cd* own = g == 0 ? sa : sb;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= ZLO && e < ZHI) continue;
+        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+        const double kxv = a.kx_scale * (double)signed_index(t + T * e, NX);
+        own[slot * T + t] = scale(v[e], g == 0 ? kxv * kyv : kxv * kxv - kyv * kyv);
+    }
+    __syncthreads();
+    bool bad = false;
+    double sE = 0.0, sZ = 0.0, sD = 0.0;
+    const double pw = (ky == 0 || ky == a.nh - 1) ? 1.0 : 2.0;
+    if (final && a.diag && ky == 0 && g == 0 && t == 0) {
+        const cd u0 = a.u[col];  // mean mode: untouched, enstrophy only
+        sZ += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
+    }
+    const double e1y = a.has_sigma ? a.e1y[ky] : 1.0, e2y = a.has_sigma ? a.e2y[ky] : 1.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if (e >= ZLO && e < ZHI) continue;
+        const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+        if ((slot < NS / 2) != (g == 0)) continue;
+        const int i = t + T * e;
+        if (abs(signed_index(i, NX)) > a.kcx || (i == 0 && ky == 0)) {
+            if (fuse) sa[slot * T + t] = zero();  // psi of the next stage: 0 here
+            continue;
+        }
+        const double kxv = a.kx_scale * (double)signed_index(i, NX);
+        const XfOps o = xf_load(a, final, fuse, stage, e1y, e2y, i, col + i);
+        const cd kv = add(sa[slot * T + t], sb[slot * T + t]);
+        const cd wn = xf_point(a, stage, final, fuse, kyv, kxv, pw, col + i, kv, o, bad, sE, sZ, sD);
+        if (fuse) {  // psi = w / |k|^2 of the next stage (k1_xinv prologue)
+            const double ksq = kxv * kxv + kyv * kyv;
+            const double r = __drcp_rn(ksq);
+            sa[slot * T + t] = mk(wn.x * r, wn.y * r);
+        }
+    }
+    if (final && a.diag) diag_accumulate(a.diag + 3 * (a.flags->steps - 1), sE, sZ, sD);
+    if (bad) {
+        atomicMin(&a.flags->div_var, 0);
+        atomicExch(&a.flags->div_step, a.flags->steps);
+        atomicExch(&a.flags->diverged, 1);
+    }
+    if constexpr (FUSE) {
+        if (!next) return;
+        __syncthreads();  // psi complete
+        // next stage's x-inverse: group 0 X[psi], group 1 X[kx psi]
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (e >= ZLO && e < ZHI) {
+                v[e] = zero();
+                continue;
+            }
+            const int slot = e < ZLO ? e : e - (ZHI - ZLO);
+            const cd psi = sa[slot * T + t];
+            v[e] = g == 0 ? psi : scale(psi, a.kx_scale * (double)signed_index(t + T * e, NX));
+        }
+        F::template run<+1>(v, ex, t, wb, 0, bar);
+#pragma unroll
+        for (int e = 0; e < E; ++e) *xinv_dst(a, g, t + T * e, kyl) = v[e];
+        if (a.p2p) __threadfence_system();
+    }
+}
+
 template <int NX, bool PZ, int NM, int EM = 16, int CTW = 256>
 cudaError_t launch_k1(const Ns2dArgs& a, int stage, cudaStream_t s) {
     using C = XCfg<NX, EM, CTW>;
@@ -881,7 +1030,7 @@ cudaError_t launch_y(const Ns2dArgs& a, cudaStream_t s) {
 
 template <int NY, bool CFL>
 cudaError_t launch_fast_y_v(const Ns2dArgs& a, cudaStream_t s) {
-    constexpr int EM = NY >= 4096 ? SKG_FAST_Y_EM : SKG_FAST_Y_EM_SMALL;
+    constexpr int EM = NY >= 4096 ? SKG_FAST_Y_EM : NY <= SKG_Y_EM4_MAX ? 4 : SKG_FAST_Y_EM_SMALL;
     using F = BFFT<NY, false, EM>;
     constexpr int G = F::T >= 256 ? 1 : 256 / F::T;
     const size_t smem = sizeof(cd) * (F::SMEM + 2 * a.ld_i) * G;
@@ -899,7 +1048,7 @@ cudaError_t launch_fast_y(const Ns2dArgs& a, cudaStream_t s) {
 
 // elements per thread of the fast path's x passes
 template <int NX>
-constexpr int fast_em() { return NX >= 4096 ? SKG_FAST_X_EM : SKG_FAST_X_EM_SMALL; }
+constexpr int fast_em() { return NX >= 4096 ? SKG_FAST_X_EM : NX <= SKG_X_EM4_MAX ? 4 : SKG_FAST_X_EM_SMALL; }
 
 // mode 0: x-inverse (k1_xinv); 1: x-forward + RK; 2: x-forward + RK fused
 // with the next stage's x-inverse.
@@ -910,7 +1059,7 @@ cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     using F = typename C::F;
     constexpr int T = F::T;
     constexpr int LPC = C::LPC;
-    const size_t smem = sizeof(cd) * C::XF_SLOT * LPC;
+    const size_t smem = sizeof(cd) * xf_slot<NX, EM, CTW>() * LPC;
     const int grid = (a.ncols + LPC - 1) / LPC;
     if (grid == 0) return cudaSuccess;
     SKG_TRY(launch_pdl(k4b_xfwd<NX, EM, CTW, FUSE>, grid, T * LPC, smem, s,
@@ -918,10 +1067,22 @@ cudaError_t launch_k4b(const Ns2dArgs& a, int stage, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int NX, bool FUSE>
+cudaError_t launch_k4p(const Ns2dArgs& a, int stage, cudaStream_t s) {
+    constexpr int EM = fast_em<NX>();
+    using P = XPCfg<NX, EM>;
+    if (a.ncols == 0) return cudaSuccess;
+    SKG_TRY(launch_pdl(k4p_xfwd<NX, EM, FUSE>, a.ncols, P::CT, P::SMEM, s, a, stage, FUSE ? 1 : 0));
+    return cudaGetLastError();
+}
+
 template <int NX, int CTW>
 cudaError_t launch_fast_x_w(const Ns2dArgs& a, int stage, int mode, cudaStream_t s) {
     constexpr int EM = fast_em<NX>();
     if (mode == 0) return launch_k1<NX, true, 2, EM, CTW>(a, stage, s);
+    if constexpr (NX >= SKG_PAIRED_X_MIN && NX <= SKG_PAIRED_X_MAX) {
+        return mode == 2 ? launch_k4p<NX, true>(a, stage, s) : launch_k4p<NX, false>(a, stage, s);
+    }
 
     if (mode == 2) return launch_k4b<NX, CTW, true>(a, stage, s);
     return launch_k4b<NX, CTW, false>(a, stage, s);
