@@ -93,9 +93,11 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 
 // z pass, dealiased states: the Hermitian split of the forward output from
 // registers (z_store_pair) instead of a shared-memory round trip of all
-// elements.  Measured (ms/step) with the zero band on: 512^3 32.55 vs 32.09
-// without it, 256^3 3.88 vs 3.95, 128^3 0.644 vs 0.632 -- off (512^3 is the
-// BASELINE grid); the zero band alone: 512^3 32.70 -> 32.09, 256^3 4.06 -> 3.95.
+// elements.  Measured (ms/step) with the zero band on, register-fetch z
+// pass: 512^3 32.55 vs 32.09 without it, 256^3 3.88 vs 3.95, 128^3 0.644 vs
+// 0.632 -- off; the zero band alone: 512^3 32.70 -> 32.09, 256^3 4.06 -> 3.95.
+// With the staged, shared-memory-bound 512^3 z pass it pays (below: on
+// there, SKG3_Z_HERM forces it everywhere).
 #ifndef SKG3_Z_HERM
 #define SKG3_Z_HERM 0
 #endif
@@ -114,6 +116,11 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 #ifndef SKG3_ZSTAGE
 #define SKG3_ZSTAGE 1
 #endif
+// staged y-inverse: the stage filled by one bulk copy per kept line (nl
+// lanes, contiguous) on an mbarrier instead of 16-byte cp.async per element
+#ifndef SKG3_YBULK
+#define SKG3_YBULK 0
+#endif
 #ifndef SKG3_ZG512
 #define SKG3_ZG512 1
 #endif
@@ -122,8 +129,15 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 #endif
 template <int NZ>
 constexpr bool zstage() { return SKG3_ZSTAGE && (NZ == 256 || NZ == 512 || (NZ == 1024 && SKG3_ZSTAGE1024)); }
+// 512^3, staged: the second inverse output in registers (168 of them) and
+// the Hermitian split from registers -- the pass is shared-memory bound, and
+// these remove ~55 KB of its ~510 KB of shared traffic per row pair:
+// 30.38 -> 29.50 ms/step (either alone: 30.45 / 29.91); at 256^3 the split
+// from registers is slower (3.78 -> 3.89).
 template <int NZ>
-constexpr bool zreg() { return NZ == 256; }
+constexpr bool zreg() { return NZ == 256 || NZ == 512; }
+template <int NZ>
+constexpr bool zherm() { return NZ == 512 && zstage<NZ>(); }
 
 // Elements per thread of the strided (x, y) passes: 8 for N <= SKG3_EM8_MAX
 // (twice the threads per line; the small grids have too few lines to fill
@@ -388,17 +402,29 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
     const double kzv = a.kz_scale * (double)kz;
     const cd* Ab = a.slab ? a.rA : a.A;
     const size_t afs = a.slab ? a.rfs : a.fstride;
+    unsigned long long* mb = reinterpret_cast<unsigned long long*>(loff + NY);
+    if (SKG3_YBULK && threadIdx.x == 0) mbar_init(mb, 1);
     line_offsets<NY>(a, x, a.kz_in, loff);
     const int nl = a.kz_in - kz0 < C ? a.kz_in - kz0 : C;  // active lanes
+    unsigned phase = 0;
     auto issue = [&](int f) {
         const cd* src = Ab + (size_t)f * afs + kz0;
-        for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
-            const int kyi = i / C, ll = i % C;
-            if (ll >= nl) continue;
-            const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
-            cp_async16(&stg[i], src + loff[j] + ll);
+        if constexpr (SKG3_YBULK) {
+            // one bulk copy of the nl lanes (contiguous) per kept line
+            if (threadIdx.x == 0) mbar_expect_tx(mb, (unsigned)(K * nl) * 16u);
+            for (int kyi = threadIdx.x; kyi < K; kyi += blockDim.x) {
+                const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
+                bulk_g2s(&stg[kyi * C], src + loff[j], (unsigned)nl * 16u, mb);
+            }
+        } else {
+            for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
+                const int kyi = i / C, ll = i % C;
+                if (ll >= nl) continue;
+                const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
+                cp_async16(&stg[i], src + loff[j] + ll);
+            }
+            cp_async_commit();
         }
-        cp_async_commit();
     };
     // Processing order 0, 5, 4, 1, 3, 2: each secondary field (A0 for
     // outputs 5 and 4, A1 for 3) was this CTA's previous primary (still in
@@ -411,7 +437,14 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
 #pragma unroll 1
     for (int i = i0; i < i1; ++i) {
         const int m = order(i);
-        cp_async_wait_all();
+        if constexpr (SKG3_YBULK) {
+            if (i == i0 || primary(m) != primary(order(i - 1))) {
+                mbar_wait(mb, phase);
+                phase ^= 1u;
+            }
+        } else {
+            cp_async_wait_all();
+        }
         __syncthreads();
         const cd* sec = Ab + (size_t)(m == 3 ? 1 : 0) * afs;
         cd v[E];
@@ -554,7 +587,7 @@ __device__ __forceinline__ void z_store_pair(const Ns3dArgs& a, const cd* v, cd*
                                              bool active, cd* o0, cd* o1, double h) {
     using F = typename Z3<NZ>::F;
     constexpr int T = F::T, E = F::E, LO = ZBand<NZ, ZB>::LO, HI = ZBand<NZ, ZB>::HI;
-    if constexpr (ZB && SKG3_Z_HERM) {
+    if constexpr (ZB && (SKG3_Z_HERM || zherm<NZ>())) {
         static_assert(LO + HI == E, "zero band symmetric about N/2");
 #pragma unroll
         for (int e = HI; e < E; ++e) sm[(e - HI) * T + t] = v[e];
@@ -1076,7 +1109,7 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     const bool zb = NY >= 16 && 8 * a.kcy < 3 * NY;  // kept ky clear of the per-thread zero band
     if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
-                              sizeof(int) * NY;
+                              sizeof(int) * NY + 16;  // + the stage's mbarrier
         // the two output halves in separate CTAs (ms/step: 64^3 0.218 -> 0.202,
         // 128^3 0.621 -> 0.600, 512^3 31.27 -> 31.20, 256^3 3.868 -> 3.888)
         const dim3 grid(a.nrl * ((a.kz_in + C - 1) / C), 2);
