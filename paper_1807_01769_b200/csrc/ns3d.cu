@@ -116,11 +116,7 @@ __device__ __forceinline__ int ky_compact(const Ns3dArgs& a, int ky) {
 #ifndef SKG3_ZSTAGE
 #define SKG3_ZSTAGE 1
 #endif
-// staged y-inverse: the stage filled by one bulk copy per kept line (nl
-// lanes, contiguous) on an mbarrier instead of 16-byte cp.async per element
-#ifndef SKG3_YBULK
-#define SKG3_YBULK 0
-#endif
+
 #ifndef SKG3_ZG512
 #define SKG3_ZG512 1
 #endif
@@ -402,29 +398,17 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
     const double kzv = a.kz_scale * (double)kz;
     const cd* Ab = a.slab ? a.rA : a.A;
     const size_t afs = a.slab ? a.rfs : a.fstride;
-    unsigned long long* mb = reinterpret_cast<unsigned long long*>(loff + NY);
-    if (SKG3_YBULK && threadIdx.x == 0) mbar_init(mb, 1);
     line_offsets<NY>(a, x, a.kz_in, loff);
     const int nl = a.kz_in - kz0 < C ? a.kz_in - kz0 : C;  // active lanes
-    unsigned phase = 0;
     auto issue = [&](int f) {
         const cd* src = Ab + (size_t)f * afs + kz0;
-        if constexpr (SKG3_YBULK) {
-            // one bulk copy of the nl lanes (contiguous) per kept line
-            if (threadIdx.x == 0) mbar_expect_tx(mb, (unsigned)(K * nl) * 16u);
-            for (int kyi = threadIdx.x; kyi < K; kyi += blockDim.x) {
-                const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
-                bulk_g2s(&stg[kyi * C], src + loff[j], (unsigned)nl * 16u, mb);
-            }
-        } else {
-            for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
-                const int kyi = i / C, ll = i % C;
-                if (ll >= nl) continue;
-                const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
-                cp_async16(&stg[i], src + loff[j] + ll);
-            }
-            cp_async_commit();
+        for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
+            const int kyi = i / C, ll = i % C;
+            if (ll >= nl) continue;
+            const int j = kyi <= a.kcy ? kyi : kyi + (NY - K);
+            cp_async16(&stg[i], src + loff[j] + ll);
         }
+        cp_async_commit();
     };
     // Processing order 0, 5, 4, 1, 3, 2: each secondary field (A0 for
     // outputs 5 and 4, A1 for 3) was this CTA's previous primary (still in
@@ -437,14 +421,7 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
 #pragma unroll 1
     for (int i = i0; i < i1; ++i) {
         const int m = order(i);
-        if constexpr (SKG3_YBULK) {
-            if (i == i0 || primary(m) != primary(order(i - 1))) {
-                mbar_wait(mb, phase);
-                phase ^= 1u;
-            }
-        } else {
-            cp_async_wait_all();
-        }
+        cp_async_wait_all();
         __syncthreads();
         const cd* sec = Ab + (size_t)(m == 3 ? 1 : 0) * afs;
         cd v[E];
@@ -1109,7 +1086,7 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     const bool zb = NY >= 16 && 8 * a.kcy < 3 * NY;  // kept ky clear of the per-thread zero band
     if (inverse && CT <= 256 && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
-                              sizeof(int) * NY + 16;  // + the stage's mbarrier
+                              sizeof(int) * NY;
         // the two output halves in separate CTAs (ms/step: 64^3 0.218 -> 0.202,
         // 128^3 0.621 -> 0.600, 512^3 31.27 -> 31.20, 256^3 3.868 -> 3.888)
         const dim3 grid(a.nrl * ((a.kz_in + C - 1) / C), 2);

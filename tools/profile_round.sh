@@ -28,7 +28,7 @@ run() {  # cfg kernel_regex count
 }
 for cfg in $cfgs; do
   case $cfg in
-    ns2d_*) run $cfg 'k3b_phys|k4b_xfwd' 2 ;;
+    ns2d_*) run $cfg 'k3b_phys|k4b_xfwd|k4p_xfwd' 2 ;;
     ns3d_*) run $cfg 'k1_3d|k2s_3d|k3_3d|k2f_3d|k4_3d' 5 ;;
   esac
 done
