@@ -102,6 +102,9 @@ int skg_dist_p2p(skg_ctx* ctx, int enable);
  * one computes (events fork and join the streams; CUDA-graph capturable).
  * Off: one all-to-all per exchange on the context stream.  No effect on the
  * peer-memory exchange (it overlaps by construction) or on ns2d.
+ * enable == 2 (pencil contexts with all parts in one process; tests): the kz
+ * <-> y transposes run the NCCL route's pack -> block transfer -> unpack
+ * instead of direct strided stores, with copies standing in for send / recv.
  */
 int skg_dist_overlap(skg_ctx* ctx, int enable);
 
@@ -117,6 +120,30 @@ int skg_nccl_unique_id(char* out128);
 int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                     double dealias_coef, double nu, int scheme, int device, int rank, int world,
                     const char* nccl_id);
+
+/*
+ * Pencil-decomposed ns3d context (BASELINE configs[4]; the
+ * paper's p3dfft-style 2D process grid): py ranks along the
+ * kept ky lines / x rows (the slab split above) times pz ranks along the kept
+ * kz modes / y rows, global rank = r_y * pz + r_z, two transposes per 3D FFT:
+ *   x-inverse on (ky, kz) lines [own ky lines, own kz range]
+ *   -> all-to-all inside the py group (ky lines <-> x rows)
+ *   -> y-inverse on (x, kz) lines [own x rows, own kz range]
+ *   -> all-to-all inside the pz group (kz range <-> y rows)
+ *   -> z pass (c2r, u x w, r2c) on (x, y) rows [own x rows, own y rows]
+ *   -> the two transposes back around the y-forward -> x-forward + RK.
+ * State per rank: [kx][own kept ky lines][own kept kz].  Same kernels as the
+ * slab path.  nccl_id == NULL: all py * pz parts live in this process on
+ * `device` (copies stand in for the exchanges; tests); otherwise this process
+ * runs part `rank` and the transposes are grouped NCCL send/recv -- or, after
+ * skg_dist_open_peers, stores straight into the peers' buffers.
+ * Needs ny divisible by 2 pz, nx by py, py * pz <= 16, a dealiased state.
+ * set_state / get_state / diagnostics take the full reference-layout field
+ * on every rank, as for the slab contexts.
+ */
+int skg_create_pencil(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+                      double dealias_coef, double nu, int scheme, int device, int rank, int py, int pz,
+                      const char* nccl_id);
 
 /* Launch all work on this CUDA stream (cudaStream_t passed as void*);
  * NULL restores the context's own stream. */

@@ -35,7 +35,8 @@ EXPORTS = [
     "skg_iteration", "skg_time", "skg_tendency", "skg_fft_forward", "skg_fft_inverse",
     "skg_plan_forward", "skg_plan_inverse", "skg_get_grid", "skg_last_divergence",
     "skg_energy", "skg_pruned", "skg_launch_count", "skg_set_timing", "skg_kernel_stats",
-    "skg_reset_stats", "skg_fp64_peak", "skg_nccl_unique_id", "skg_create_dist", "skg_run",
+    "skg_reset_stats", "skg_fp64_peak", "skg_nccl_unique_id", "skg_create_dist", "skg_create_pencil",
+    "skg_run",
     "skg_set_cfl", "skg_last_dt", "skg_set_time", "skg_max_velocity", "skg_diagnostics",
     "skg_set_forcing", "skg_last_injection", "skg_sanitize_state", "skg_spectra",
     "skg_dist_p2p", "skg_dist_overlap", "skg_guard_violations", "skg_dist_ipc_handle", "skg_dist_open_peers", "skg_dft_r2c", "skg_dft_c2r",
@@ -95,6 +96,9 @@ def load_library():
     L.skg_destroy.argtypes = [vp]
     L.skg_create_dist.argtypes = [C.POINTER(vp), C.c_char_p, C.c_int, ip, dp, C.c_double,
                                   C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p]
+    L.skg_create_pencil.argtypes = [C.POINTER(vp), C.c_char_p, C.c_int, ip, dp, C.c_double,
+                                    C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_char_p]
     L.skg_nccl_unique_id.argtypes = [C.c_char_p]
     L.skg_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.skg_set_stream.argtypes = [vp, vp]
@@ -239,12 +243,15 @@ class Simulation:
 
     def __init__(self, solver: str, n, nu: float = 0.0, dt: float = 0.0, scheme: str = "RK4",
                  L=None, dealias_coef: float = 2.0 / 3.0, device: int = 0, world: int = 1,
-                 rank: int = 0, nccl_id: bytes | None = None, compact: bool = False):
+                 rank: int = 0, nccl_id: bytes | None = None, compact: bool = False,
+                 pencil: tuple[int, int] | None = None):
         """world > 1: slab decomposition (ns2d and ns3d).  With nccl_id (from
         nccl_unique_id() on rank 0) this process runs partition `rank` over
         NCCL; without it all `world` partitions run here on one device.
         compact (ns3d, world 1): the kept-modes-only layout of the slab path
-        on one GPU (dealiased states only; 1024^3 fits one B200)."""
+        on one GPU (dealiased states only; 1024^3 fits one B200).
+        pencil = (py, pz) (ns3d): 2D process grid of py * pz ranks
+        (skg_create_pencil; world is then py * pz, rank = r_y * pz + r_z)."""
         L_ = load_library()
         self.solver = solver
         self.n = tuple(int(x) for x in n)
@@ -259,7 +266,13 @@ class Simulation:
         cn = (C.c_int * self.dims)(*self.n)
         cL = None if L is None else (C.c_double * self.dims)(*L)
         sch = SKG_RK2 if self.scheme == "RK2" else SKG_RK4
-        if world > 1 or (compact and solver == "ns3d"):
+        if pencil is not None:
+            py, pz = (int(x) for x in pencil)
+            world = py * pz
+            rc = L_.skg_create_pencil(C.byref(h), solver.encode(), self.dims, cn, cL,
+                                      float(dealias_coef), self.nu, sch, int(device), int(rank),
+                                      py, pz, nccl_id)
+        elif world > 1 or (compact and solver == "ns3d"):
             rc = L_.skg_create_dist(C.byref(h), solver.encode(), self.dims, cn, cL,
                                     float(dealias_coef), self.nu, sch, int(device), int(rank),
                                     int(world), nccl_id)
@@ -268,6 +281,7 @@ class Simulation:
                                self.nu, sch, int(device))
         self.world = int(world)
         self.rank = int(rank)
+        self.pencil = None if pencil is None else (py, pz)
         self._nccl = nccl_id
         if rc:
             _raise(rc)
@@ -471,7 +485,7 @@ class Simulation:
     def set_overlap(self, on: bool) -> None:
         """ns3d slab, copy / NCCL exchange: all-to-all chunked per field on a
         second stream, overlapping the next field's pass (skg_dist_overlap)."""
-        self._call("skg_dist_overlap", C.c_int(1 if on else 0))
+        self._call("skg_dist_overlap", C.c_int(int(on)))
 
     def disable_p2p(self) -> None:
         """Back to the NCCL / device-copy exchange (skg_dist_p2p(0))."""

@@ -335,20 +335,25 @@ skg::Ns3dArgs args3d_part(skg_ctx* c, double dt, const Part& p) {
     a.rfs = p.rfs;
     a.G = c->G;
     a.r = p.r;
-    a.lead = p.r == 0 ? 1 : 0;
+    a.lead = &p == c->parts.data() ? 1 : 0;  // the process's first part counts the steps
     a.kys = p.c0;
     a.nkyl = p.ncols;
     a.nrl = c->nrl;
     a.ystate = p.ncols;
     a.slab = 1;
-    a.sz = c->kc[2] + 1;
+    // kz range of this part (all kept kz unless the pencil layout splits them)
+    a.sz = p.nkz;
+    a.kz_in = a.kz_o = p.nkz;
+    a.kz0 = p.kz0;
+    a.e1z += p.kz0;
+    a.e2z += p.kz0;
     a.p2p = c->p2p ? 1 : 0;
     if (c->p2p) {
         a.rD = p.rD3;
         a.dfs = c->dfs3;
-        for (int q = 0; q < c->G; ++q) {
-            a.peer_rA[q] = c->peer_rA3[q];
-            a.peer_D[q] = c->peer_D3[q];
+        for (int q = 0; q < c->G; ++q) {  // peers along the ky / x split: same pz
+            a.peer_rA[q] = c->peer_rA3[q * c->Pz + p.pz];
+            a.peer_D[q] = c->peer_D3[q * c->Pz + p.pz];
         }
     }
     return a;
@@ -425,7 +430,7 @@ int decide_pruned(skg_ctx* c, const cd* d_ref_layout) {
 // part are at most two runs of global ky (positive, then negative ky).
 int copy_slab3(skg_ctx* c, const Part& p, bool to_part) {
     const int kcy = c->kc[1], ny = c->n[1], nx = c->n[0];
-    const size_t nh = (size_t)c->nh, kzc = (size_t)c->kc[2] + 1;
+    const size_t nh = (size_t)c->nh, kzc = (size_t)p.nkz;  // the part's kz range [kz0, kz0 + nkz)
     const int runs[2][2] = {{0, kcy + 1}, {kcy + 1, 2 * kcy + 1}};  // compact ranges
     for (int b = 0; b < 2; ++b) {
         const int lo = std::max(runs[b][0], p.c0), hi = std::min(runs[b][1], p.c0 + p.ncols);
@@ -433,7 +438,7 @@ int copy_slab3(skg_ctx* c, const Part& p, bool to_part) {
         const int gy = b == 0 ? lo : lo + ny - (2 * kcy + 1);
         for (int v = 0; v < 3; ++v) {
             // kept kz of lines [gy, gy + hi - lo) for every kx: (kz, line, kx) boxes
-            cd* io = c->io + (size_t)v * c->S + (size_t)gy * nh;
+            cd* io = c->io + (size_t)v * c->S + (size_t)gy * nh + p.kz0;
             cd* st = p.u + (size_t)v * p.vs + (size_t)(lo - p.c0) * kzc;
             cudaPitchedPtr pio = make_cudaPitchedPtr(io, nh * sizeof(cd), kzc * sizeof(cd), ny);
             cudaPitchedPtr pst = make_cudaPitchedPtr(st, kzc * sizeof(cd), kzc * sizeof(cd), p.ncols);
@@ -530,7 +535,9 @@ int ensure_p2p_bufs(skg_ctx* c) {
     if (c->solver != 3) return SKG_OK;
     size_t maxcols = 0;
     for (int q = 0; q < c->G; ++q) maxcols = std::max(maxcols, (size_t)(c->cstart[q + 1] - c->cstart[q]));
-    c->dfs3 = (size_t)c->n[0] * maxcols * ((size_t)c->kc[2] + 1);
+    size_t maxkz = 0;
+    for (int z = 0; z < c->Pz; ++z) maxkz = std::max(maxkz, (size_t)(c->zstart[z + 1] - c->zstart[z]));
+    c->dfs3 = (size_t)c->n[0] * maxcols * maxkz;
     for (Part& p : c->parts)
         if (!p.rD3) CUDA_TRY(skg::dmalloc(&p.rD3, sizeof(cd) * 3 * c->dfs3));
     return SKG_OK;

@@ -83,6 +83,18 @@ struct Part {
     cd* sD3 = nullptr;
     cd* rD3 = nullptr;  // p2p: y-forward receive buffer (3 fields, stride dfs3)
     size_t vs = 0, fs = 0, rfs = 0;
+    // ns3d pencil layout (skg_create_pencil): r is the rank along the ky-line /
+    // x-row split (Py), pz the rank along the kept-kz / y-row split (Pz); the
+    // part holds the kept kz modes [kz0, kz0 + nkz) in its x and y passes and
+    // the y rows [pz nyl, (pz + 1) nyl) in its z pass.  Z3: the z pass's six
+    // input fields [xl][yl][kz] (all kept kz), stride fsz; its three outputs
+    // go to A3 with the same stride.  sZ / rZ: pack / unpack blocks of the
+    // NCCL route of the two kz <-> y transposes.
+    int pz = 0, kz0 = 0, nkz = 0;
+    cd* Z3 = nullptr;
+    cd* sZ = nullptr;
+    cd* rZ = nullptr;
+    size_t fsz = 0;
 };
 
 struct skg_ctx {
@@ -132,6 +144,13 @@ struct skg_ctx {
     bool dist = false;
     int G = 1, grank = 0, nrl = 0;
     std::vector<int> cstart;  // G + 1 entries
+    // ns3d pencil: G ranks along ky lines / x rows times Pz ranks along the
+    // kept kz / y rows; global rank = r Pz + pz; zstart: kz ranges (Pz + 1)
+    int Pz = 1, nyl = 0;
+    bool zpack = false;  // single process: run the NCCL route's pack / unpack (skg_dist_overlap(ctx, 2))
+    std::vector<int> zstart;
+    cd* peer_Z3[SKG_MAX_RANKS] = {};   // pencil: z-pass input buffers (Z3) by global rank
+    cd* peer_B3[SKG_MAX_RANKS] = {};   // pencil: y-pass buffers (B3) by global rank
     std::vector<Part> parts;
     int* d_kowner = nullptr;
     int* d_cstart = nullptr;
@@ -230,6 +249,7 @@ cd* twiddle_table(int device, int n);
 int refresh_forcing(skg_ctx* c);
 int sync_and_check(skg_ctx* c, long nsteps, double dt);
 int exchange(skg_ctx* c, int which);
+int exchange_z(skg_ctx* c, int dir, cudaStream_t st = nullptr);
 int enqueue_steps(skg_ctx* c, double dt, long nsteps);
 
 }  // namespace skh

@@ -184,19 +184,22 @@ int exchange3(skg_ctx* c, int which, unsigned fmask, cudaStream_t st) {
         return SKG_OK;
     }
     const size_t nrl = (size_t)c->nrl;
-    const size_t kz = (size_t)c->kc[2] + 1;  // kz_in = kz_o (pruned)
+    const int Pz = c->Pz;  // pencil: the exchange runs inside each group of equal pz
     auto nl = [&](int q) { return (size_t)(c->cstart[q + 1] - c->cstart[q]); };
     const int nf = which == 0 ? 5 : 3;
-    // block from rank r (buffers src) to rank q (buffers dst), field f
+    // block from rank r (buffers src) to rank q (buffers dst), field f; kz: the
+    // group's kz extent (kz_in = kz_o, pruned)
     auto src_ptr = [&](const Part& src, int q, int f) {
+        const size_t kz = (size_t)src.nkz;
         return which == 0 ? src.A3 + f * src.fs + (size_t)q * nrl * nl(src.r) * kz
                           : src.sD3 + f * src.rfs + nrl * c->cstart[q] * kz;
     };
     auto dst_ptr = [&](const Part& dst, int r, int f) {
+        const size_t kz = (size_t)dst.nkz;
         return which == 0 ? dst.rA3 + f * dst.rfs + nrl * c->cstart[r] * kz
                           : dst.B3 + f * dst.fs + (size_t)r * nrl * nl(dst.r) * kz;
     };
-    auto count = [&](int r, int q) { return nrl * kz * (which == 0 ? nl(r) : nl(q)); };
+    auto count = [&](int r, int q, size_t kz) { return nrl * kz * (which == 0 ? nl(r) : nl(q)); };
     const skg::LaunchHook hook = hook_of(c);
     hook.begin(4);
     double bytes = 0.0;
@@ -204,7 +207,8 @@ int exchange3(skg_ctx* c, int which, unsigned fmask, cudaStream_t st) {
         for (const Part& src : c->parts)
             for (const Part& dst : c->parts)
                 for (int f = 0; f < nf; ++f) {
-                    const size_t cnt = count(src.r, dst.r);
+                    if (src.pz != dst.pz) continue;
+                    const size_t cnt = count(src.r, dst.r, (size_t)src.nkz);
                     if (!cnt || !(fmask >> f & 1u)) continue;
                     CUDA_TRY(cudaMemcpyAsync(dst_ptr(dst, src.r, f), src_ptr(src, dst.r, f),
                                              cnt * sizeof(cd), cudaMemcpyDeviceToDevice, st));
@@ -215,17 +219,18 @@ int exchange3(skg_ctx* c, int which, unsigned fmask, cudaStream_t st) {
         const int r = me.r;
         ncclResult_t nr = nccl().GroupStart();
         for (int q = 0; q < G && nr == ncclSuccess; ++q) {
+            const int peer = q * Pz + me.pz;  // global rank of the group's member q
             for (int f = 0; f < nf && nr == ncclSuccess; ++f) {
                 if (!(fmask >> f & 1u)) continue;
-                const size_t scnt = count(r, q), rcnt = count(q, r);
+                const size_t scnt = count(r, q, (size_t)me.nkz), rcnt = count(q, r, (size_t)me.nkz);
                 cd* sptr = src_ptr(me, q, f);
                 cd* rptr = dst_ptr(me, q, f);
                 if (q == r) {
                     if (scnt) CUDA_TRY(cudaMemcpyAsync(rptr, sptr, scnt * sizeof(cd), cudaMemcpyDeviceToDevice, st));
                     continue;
                 }
-                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, q, c->comm, st);
-                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, q, c->comm, st);
+                if (scnt) nr = nccl().Send(sptr, 2 * scnt, ncclDouble, peer, c->comm, st);
+                if (nr == ncclSuccess && rcnt) nr = nccl().Recv(rptr, 2 * rcnt, ncclDouble, peer, c->comm, st);
                 bytes += scnt * sizeof(cd);
             }
         }
@@ -235,6 +240,140 @@ int exchange3(skg_ctx* c, int which, unsigned fmask, cudaStream_t st) {
     }
     hook.end(4, bytes);
     ++c->launches;
+    return SKG_OK;
+}
+
+// Pencil decomposition: the kz <-> y transposes inside each group of equal
+// r (Pz members).  dir = 0, after the y-inverse: the six fields
+// [xl][y][kz in the member's range] (B3) -> every member's z-pass input
+// [xl][y in its rows][all kept kz] (Z3).  dir = 1, after the z pass: its three
+// outputs [xl][yl][all kept kz] (A3, stride fsz) -> every member's y-forward
+// input [xl][y][kz in its range] (fields 3..5 of B3).  All parts local, or the
+// peer-memory route: ONE strided copy kernel per destination stores straight
+// into the destination's layout (peer memory over NVLink across processes;
+// no pack / unpack pass), then the barrier.  NCCL route: pack into one
+// contiguous block per member, grouped send / recv, unpack.
+int exchange_z(skg_ctx* c, int dir, cudaStream_t st) {
+    if (!st) st = c->stream;
+    const int Pz = c->Pz;
+    if (Pz == 1) return SKG_OK;
+    const size_t nrl = (size_t)c->nrl, ny = (size_t)c->n[1], nyl = (size_t)c->nyl;
+    const size_t kzf = (size_t)c->kc[2] + 1;
+    const int nf = dir == 0 ? 6 : 3;
+    const skg::LaunchHook hook = hook_of(c);
+    hook.begin(4);
+    double bytes = 0.0;
+    // box from member `s` (kz range [skz0, skz0 + snkz), rows of member spz) to
+    // member `d`: source and destination base pointers are the buffers' starts
+    auto box = [&](const cd* sbuf, size_t sfs, int spz, int skz0, int snkz, cd* dbuf, size_t dfs_,
+                   int dpz, int dkz0, int dnkz) {
+        skg::BoxCopy b{};
+        b.nf = nf;
+        b.nx = (int)nrl;
+        b.ny = (int)nyl;
+        if (dir == 0) {  // B3 [xl][ny][snkz] rows of d -> Z3 [xl][nyl][kzf] at kz skz0
+            b.nz = snkz;
+            b.src = sbuf + (size_t)dpz * nyl * snkz;
+            b.sf = sfs, b.sx = ny * snkz, b.sy = (size_t)snkz;
+            b.dst = dbuf + skz0;
+            b.df = dfs_, b.dx = nyl * kzf, b.dy = kzf;
+        } else {  // A3 [xl][nyl][kzf] kz of d -> B3 fields 3.. [xl][ny][dnkz] rows of s
+            b.nz = dnkz;
+            b.src = sbuf + dkz0;
+            b.sf = sfs, b.sx = nyl * kzf, b.sy = kzf;
+            b.dst = dbuf + 3 * dfs_ + (size_t)spz * nyl * dnkz;
+            b.df = dfs_, b.dx = ny * dnkz, b.dy = (size_t)dnkz;
+        }
+        return b;
+    };
+    if (c->comm == nullptr && !c->zpack) {  // all parts in this process
+        for (const Part& s : c->parts)
+            for (const Part& d : c->parts) {
+                if (s.r != d.r) continue;
+                const skg::BoxCopy b = dir == 0 ? box(s.B3, s.fs, s.pz, s.kz0, s.nkz, d.Z3, d.fsz, d.pz, d.kz0, d.nkz)
+                                                : box(s.A3, s.fsz, s.pz, s.kz0, s.nkz, d.B3, d.fs, d.pz, d.kz0, d.nkz);
+                CUDA_TRY(skg::launch_box_copy(b, false, st, &c->launches));
+                if (s.pz != d.pz) bytes += (double)sizeof(cd) * b.nf * b.nx * b.ny * b.nz;
+            }
+    } else if (c->comm && c->p2p) {  // stores into the members' buffers, then the barrier
+        const Part& s = c->parts[0];
+        for (int z = 0; z < Pz; ++z) {
+            const int peer = s.r * Pz + z;
+            const int dkz0 = c->zstart[z], dnkz = c->zstart[z + 1] - c->zstart[z];
+            // B3's and Z3's field strides are uniform over the ranks
+            const skg::BoxCopy b = dir == 0 ? box(s.B3, s.fs, s.pz, s.kz0, s.nkz, c->peer_Z3[peer], s.fsz, z, dkz0, dnkz)
+                                            : box(s.A3, s.fsz, s.pz, s.kz0, s.nkz, c->peer_B3[peer], s.fs, z, dkz0, dnkz);
+            CUDA_TRY(skg::launch_box_copy(b, true, st, &c->launches));
+            if (z != s.pz) bytes += (double)sizeof(cd) * b.nf * b.nx * b.ny * b.nz;
+        }
+        const ncclResult_t nr = nccl().AllReduce(c->d_barrier, c->d_barrier, 1, ncclDouble, ncclSum, c->comm, st);
+        if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
+    } else {  // NCCL (or its single-process stand-in): pack, send / recv, unpack
+        const size_t plane = nrl * nyl;  // (x, y) rows of one block
+        // member me's send block to member z / receive block from member z: offset, kz extent
+        auto nkz_of = [&](int z) { return (size_t)(c->zstart[z + 1] - c->zstart[z]); };
+        auto soff = [&](const Part& me, int z) {
+            return dir == 0 ? (size_t)z * nf * plane * me.nkz : (size_t)nf * plane * c->zstart[z];
+        };
+        auto skz = [&](const Part& me, int z) { return dir == 0 ? (size_t)me.nkz : nkz_of(z); };
+        auto roff = [&](const Part& me, int z) {
+            return dir == 0 ? (size_t)nf * plane * c->zstart[z] : (size_t)z * nf * plane * me.nkz;
+        };
+        auto rkz = [&](const Part& me, int z) { return dir == 0 ? nkz_of(z) : (size_t)me.nkz; };
+        for (Part& me : c->parts) {
+            if (!me.sZ) {
+                CUDA_TRY(skg::dmalloc(&me.sZ, sizeof(cd) * 6 * me.fsz));
+                CUDA_TRY(skg::dmalloc(&me.rZ, sizeof(cd) * 6 * me.fsz));
+            }
+            for (int z = 0; z < Pz; ++z) {  // pack (the own block goes straight to its place)
+                const int dkz0 = c->zstart[z], dnkz = (int)nkz_of(z);
+                skg::BoxCopy b = dir == 0 ? box(me.B3, me.fs, me.pz, me.kz0, me.nkz, me.Z3, me.fsz, z, dkz0, dnkz)
+                                          : box(me.A3, me.fsz, me.pz, me.kz0, me.nkz, me.B3, me.fs, z, dkz0, dnkz);
+                if (z != me.pz) {  // contiguous [f][xl][yl][kz]
+                    b.dst = me.sZ + soff(me, z);
+                    b.dy = skz(me, z), b.dx = nyl * skz(me, z), b.df = plane * skz(me, z);
+                }
+                CUDA_TRY(skg::launch_box_copy(b, false, st, &c->launches));
+            }
+        }
+        if (c->comm) {
+            const Part& me = c->parts[0];
+            ncclResult_t nr = nccl().GroupStart();
+            for (int z = 0; z < Pz && nr == ncclSuccess; ++z) {
+                if (z == me.pz) continue;
+                const int peer = me.r * Pz + z;
+                nr = nccl().Send(me.sZ + soff(me, z), 2 * nf * plane * skz(me, z), ncclDouble, peer, c->comm, st);
+                if (nr == ncclSuccess)
+                    nr = nccl().Recv(me.rZ + roff(me, z), 2 * nf * plane * rkz(me, z), ncclDouble, peer,
+                                     c->comm, st);
+                bytes += (double)sizeof(cd) * nf * plane * skz(me, z);
+            }
+            ncclResult_t ne = nccl().GroupEnd();
+            if (nr != ncclSuccess || ne != ncclSuccess)
+                return fail(SKG_ENCCL, std::string("pencil transpose: ") +
+                                           nccl().GetErrorString(nr != ncclSuccess ? nr : ne));
+        } else {  // the send / recv pairs as device copies
+            for (const Part& sp : c->parts)
+                for (const Part& dp : c->parts) {
+                    if (sp.r != dp.r || sp.pz == dp.pz) continue;
+                    const size_t cnt = nf * plane * skz(sp, dp.pz);
+                    CUDA_TRY(cudaMemcpyAsync(dp.rZ + roff(dp, sp.pz), sp.sZ + soff(sp, dp.pz), cnt * sizeof(cd),
+                                             cudaMemcpyDeviceToDevice, st));
+                    bytes += (double)cnt * sizeof(cd);
+                }
+        }
+        for (const Part& me : c->parts)
+            for (int z = 0; z < Pz; ++z) {  // unpack the received blocks
+                if (z == me.pz) continue;
+                // as if member z had stored it: the box from z to me, read from the block
+                skg::BoxCopy b = dir == 0 ? box(nullptr, 0, z, c->zstart[z], (int)nkz_of(z), me.Z3, me.fsz, me.pz, me.kz0, me.nkz)
+                                          : box(nullptr, 0, z, c->zstart[z], (int)nkz_of(z), me.B3, me.fs, me.pz, me.kz0, me.nkz);
+                b.src = me.rZ + roff(me, z);
+                b.sy = rkz(me, z), b.sx = nyl * rkz(me, z), b.sf = plane * rkz(me, z);
+                CUDA_TRY(skg::launch_box_copy(b, false, st, &c->launches));
+            }
+    }
+    hook.end(4, bytes);
     return SKG_OK;
 }
 
@@ -306,8 +445,37 @@ int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool las
     const int nst = c->scheme == SKG_RK2 ? 2 : 4;
     const skg::LaunchHook hook = hook_of(c);
     int rc;
-    if (c->solver == 3 && !c->p2p && c->G > 1 && !c->timing && !c->no_overlap)
+    if (c->solver == 3 && !c->p2p && c->G > 1 && c->Pz == 1 && !c->timing && !c->no_overlap)
         return enqueue_dist_step3_chunked(c, dt, counter);
+    if (c->solver == 3 && c->Pz > 1) {
+        // pencil: x-inverse, all-to-all over the ky / x split, y-inverse,
+        // kz -> y transpose, z pass on own (x, y) rows with all kept kz,
+        // y -> kz transpose, y-forward, all-to-all back, x-forward + RK
+        auto run = [&](int pass, int st) -> int {
+            for (const Part& p : c->parts) {
+                skg::Ns3dArgs a = args3d_part(c, dt, p);
+                if (pass == 6) {  // z pass: Z3 -> A3, nrl * nyl rows of all kept kz
+                    a.B = p.Z3;
+                    a.fstride = p.fsz;
+                    a.ny = c->nyl;
+                    a.kz_in = a.kz_o = c->kc[2] + 1;
+                } else if (pass == 4) {  // y-forward input: fields 3..5 of B3
+                    a.A = p.B3 + 3 * p.fs;
+                }
+                CUDA_TRY(skg::ns3d_pass(a, pass, st, c->stream, counter, hook));
+            }
+            return SKG_OK;
+        };
+        for (int st = 1; st <= nst; ++st) {
+            if ((rc = run(0, st)) || (rc = exchange(c, 0))) return rc;
+            if ((rc = run(5, st)) || (rc = exchange_z(c, 0))) return rc;
+            if ((rc = run(6, st)) || (rc = exchange_z(c, 1))) return rc;
+            if ((rc = run(4, st)) || (rc = exchange(c, 1))) return rc;
+            if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;
+            if ((rc = run(2, st))) return rc;
+        }
+        return SKG_OK;
+    }
     if (c->solver == 3) {
         for (int st = 1; st <= nst; ++st) {
             for (int pass = 0; pass < 3; ++pass) {
@@ -324,7 +492,7 @@ int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool las
     auto run_pass = [&](int pass, int st, int next) -> int {
         for (const Part& p : c->parts) {
             skg::Ns2dArgs a = args2d_part(c, dt, p);
-            a.lead = p.r == 0 ? 1 : 0;
+            a.lead = &p == c->parts.data() ? 1 : 0;
             CUDA_TRY(skg::ns2d_fast_pass(a, pass, st, c->stream, counter, hook, next));
         }
         return SKG_OK;

@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2_3d(Ns3dArgs a) {
     cd* sm = smem + l * F::SMEM;
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
-    const double kzv = a.kz_scale * (double)kz;
+    const double kzv = a.kz_scale * (double)(a.kz0 + kz);
     const cd* Ab = a.slab ? a.rA : a.A;
     const size_t afs = a.slab ? a.rfs : a.fstride;
     const cd* A0 = Ab;
@@ -395,7 +395,7 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
     int* loff = reinterpret_cast<int*>(stg + (size_t)K * C);
     const int salt = l & 7;
     const typename F::Bases wb = F::bases(t, a.twy);
-    const double kzv = a.kz_scale * (double)kz;
+    const double kzv = a.kz_scale * (double)(a.kz0 + kz);
     const cd* Ab = a.slab ? a.rA : a.A;
     const size_t afs = a.slab ? a.rfs : a.fstride;
     line_offsets<NY>(a, x, a.kz_in, loff);
@@ -911,15 +911,16 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     constexpr bool final = FIN;
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     const double kyv = a.ky_scale * (double)sky;
-    const double kzv = a.kz_scale * (double)kz;
+    const double kzv = a.kz_scale * (double)(a.kz0 + kz);
     const cd* l0 = (a.p2p ? a.rD : a.B) + lbase;
     const cd* l1 = (a.p2p ? a.rD + a.dfs : a.B + a.fstride) + lbase;
     int bad = 3;
     // per-step E and eps of the new state (Solver::mode_energy default,
     // simulation.cpp:163-170; dissipation_rate simulation.cpp:608-615)
     double sE = 0.0, sD = 0.0;
-    const double pw = (kz == 0 || kz == a.nh - 1) ? 1.0 : 2.0;
-    if (final && a.diag && active && ky == 0 && kz == 0 && t == 0) {
+    const int kzg = a.kz0 + kz;  // global kz (pencil layout: kz is the local index)
+    const double pw = (kzg == 0 || kzg == a.nh - 1) ? 1.0 : 2.0;
+    if (final && a.diag && active && ky == 0 && kzg == 0 && t == 0) {
         for (int c = 0; c < 3; ++c) {  // mean flow: untouched, energy only
             const cd u0 = a.u[sidx(a, 0, ys, 0) + c * a.vstride];
             sE += 0.5 * pw * (u0.x * u0.x + u0.y * u0.y);
@@ -931,7 +932,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
         const int i = t + T * e;
         const int si = signed_index(i, NX);
         bool keep = keep_y && abs(si) <= a.kcx;
-        if (i == 0 && ky == 0 && kz == 0) keep = false;  // mean mode of the tendency is 0
+        if (i == 0 && ky == 0 && kzg == 0) keep = false;  // mean mode of the tendency is 0
         if (!keep && a.pruned) continue;
         cd c0 = zero(), c1 = zero(), c2 = zero();
         if (keep) {
@@ -1203,19 +1204,26 @@ cudaError_t ns3d_pass(const Ns3dArgs& a, int pass, int stage, cudaStream_t s, lo
         if ((err = dispatch_x3(a, stage, true, s)) != cudaSuccess) return err;
         hook.end(0, B * (nin * kxk * lines_in * (stage == 1 ? 1.0 : 2.0) + nout * a.nx * lines_in));
         *launches += 1;
-    } else if (pass == 1 || pass == 3 || pass == 4) {
+    } else if (pass == 1 || pass == 3 || pass == 4 || pass == 5 || pass == 6) {
+        // 1: y-inverse, z, y-forward; 3: y-inverse, z; 4: y-forward; pencil
+        // layout: 5: y-inverse only, 6: z pass only
         Ns3dArgs b = a;  // the z pass of stage 1 feeds the CFL max
         b.ystage = stage;
         if (pass != 4) {
-            hook.begin(3);
-            if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
-            hook.end(3, B * (5.0 * a.nrl * kyk * a.kz_in + 6.0 * plane_in));
-            hook.begin(1);
-            if ((err = dispatch_z3(b, s)) != cudaSuccess) return err;
-            hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
-            *launches += 2;
+            if (pass != 6) {
+                hook.begin(3);
+                if ((err = dispatch_y3(a, true, s)) != cudaSuccess) return err;
+                hook.end(3, B * (5.0 * a.nrl * kyk * a.kz_in + 6.0 * plane_in));
+                *launches += 1;
+            }
+            if (pass != 5) {
+                hook.begin(1);
+                if ((err = dispatch_z3(b, s)) != cudaSuccess) return err;
+                hook.end(1, B * (6.0 * plane_in + 3.0 * plane_o));
+                *launches += 1;
+            }
         }
-        if (pass != 3) {
+        if (pass == 1 || pass == 4) {
             const double nf = pass == 4 ? a.ncomp : 3.0;
             hook.begin(5);
             if ((err = dispatch_y3(a, false, s)) != cudaSuccess) return err;

@@ -237,6 +237,11 @@ struct Ns3dArgs {
     cd* peer_D[SKG_MAX_RANKS];
     cd* rD;                 // p2p: this rank's y-forward receive buffer (3 fields, stride dfs);
     size_t dfs;             // B stays the y/z-pass intermediate, which peers must not touch
+    // Pencil layout (slab over ky lines / x rows as above, times a split of
+    // the kept kz modes over Pz ranks): this rank's x and y passes see the kz
+    // modes [kz0, kz0 + kz_in) only (local index kz, global kz0 + kz); the
+    // factor tables e1z / e2z are passed already shifted by kz0.
+    int kz0 = 0;
 };
 
 // Programmatic dependent launch (sm_90+): step kernels are launched with
@@ -314,6 +319,17 @@ bool ns3d_supported(int nx, int ny, int nz);
 // ---------------------------------------------------------------- utilities (util.cu)
 cudaError_t launch_transpose_c(const cd* in, cd* out, int rows, int cols, int conj_flag,
                                cudaStream_t s, long* launches);  // out[c][r] = in[r][c]
+// Strided box copy of complex fields (the pencil decomposition's kz <-> y
+// transposes): dst[f df + x dx + y dy + z] = src[f sf + x sx + y sy + z] for
+// f < nf, x < nx, y < ny, z < nz (z contiguous on both sides; dst may be peer
+// memory).  fence: __threadfence_system after the stores (peer destinations).
+struct BoxCopy {
+    const cd* src;
+    cd* dst;
+    int nf, nx, ny, nz;
+    size_t sf, sx, sy, df, dx, dy;
+};
+cudaError_t launch_box_copy(const BoxCopy& b, bool fence, cudaStream_t s, long* launches);
 cudaError_t launch_count_masked(const cd* f, int dims, const int* n, const int* kc, int nvars,
                                 long long spect_size, unsigned long long* d_count,
                                 cudaStream_t s, long* launches);

@@ -19,7 +19,7 @@ const char* skg_last_error(void) { return g_err.c_str(); }
 
 static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                        double dealias_coef, double nu, int scheme, int device, int rank, int world,
-                       const char* nccl_id, bool slab_one);
+                       const char* nccl_id, bool slab_one, int Pz = 1);
 
 int skg_create(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                double dealias_coef, double nu, int scheme, int device) {
@@ -31,6 +31,19 @@ int skg_create_dist(skg_ctx** out, const char* solver, int dims, const int* n, c
                     const char* nccl_id) {
     return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, rank, world, nccl_id,
                        world == 1);
+}
+
+// 3D pencil decomposition (BASELINE configs[4]): py ranks along
+// the kept ky lines / x rows (the slab split) times pz ranks along the kept kz
+// modes / y rows; global rank = r_y * pz + r_z.
+int skg_create_pencil(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
+                      double dealias_coef, double nu, int scheme, int device, int rank, int py, int pz,
+                      const char* nccl_id) {
+    if (py < 1 || pz < 1) return fail(SKG_ECONFIG, "pencil: process grid extents must be >= 1");
+    if (std::string(solver ? solver : "") != "ns3d")
+        return fail(SKG_EUNSUPPORTED, "pencil decomposition: ns3d only");
+    return create_impl(out, solver, dims, n, L, dealias_coef, nu, scheme, device, rank, py, nccl_id, true,
+                       pz);
 }
 
 int skg_nccl_unique_id(char* out128) {
@@ -45,7 +58,7 @@ int skg_nccl_unique_id(char* out128) {
 
 static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n, const double* L,
                        double dealias_coef, double nu, int scheme, int device, int rank, int world,
-                       const char* nccl_id, bool slab_one) {
+                       const char* nccl_id, bool slab_one, int Pz) {
     if (!out) return fail(SKG_ECONFIG, "create: null output pointer");
     *out = nullptr;
     std::string s = solver ? solver : "";
@@ -63,7 +76,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     if (scheme != SKG_RK4 && scheme != SKG_RK2) return fail(SKG_ECONFIG, "unknown time scheme");
     // extents outside the fused kernels' range run the generic step
     const bool generic = sid == 2 ? !skg::ns2d_supported(n[0], n[1]) : !skg::ns3d_supported(n[0], n[1], n[2]);
-    if (generic && (world > 1 || (sid == 3 && slab_one)))
+    if (generic && (world > 1 || Pz > 1 || (sid == 3 && slab_one)))
         return fail(SKG_EUNSUPPORTED,
                     "slab and compact layouts need the fused kernels' extents (powers of two)");
 
@@ -71,7 +84,10 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(SKG_ECUDA, "no CUDA device visible (the library has no CPU path)");
     if (device < 0 || device >= ndev) return fail(SKG_ECONFIG, "device ordinal out of range");
-    if (world < 1 || rank < 0 || rank >= world) return fail(SKG_ECONFIG, "bad rank / world size");
+    if (world < 1 || rank < 0 || rank >= world * Pz) return fail(SKG_ECONFIG, "bad rank / world size");
+    if (Pz > 1 && (n[1] % (2 * Pz) || world * Pz > SKG_MAX_RANKS))
+        return fail(SKG_ECONFIG, "pencil: ny must be divisible by 2 * pz and py * pz <= " +
+                                     std::to_string(SKG_MAX_RANKS));
     if (world > 1 && sid == 3 && n[0] % world)
         return fail(SKG_ECONFIG, "nx must be divisible by world for the slab decomposition");
     if (world > 1 && sid == 2 && n[0] % (4 * world))
@@ -126,6 +142,7 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     }
     c->dist = world > 1 || (sid == 3 && slab_one);
     c->G = world;
+    c->Pz = Pz;
     c->grank = rank;
     if (sid == 2) {  // column partition of the kept ky columns, row partition of x
         const int Kc = c->kc[1] + 1, PP = (Kc + 1) / 2;
@@ -160,38 +177,50 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
             cudaMemcpy(c->d_cstart, c->cstart.data(), sizeof(int) * (world + 1), cudaMemcpyHostToDevice);
         }
         // state lines and intermediates hold only the kept kz (slab layouts
-        // need a dealiased state); one partition: no exchange buffers
+        // need a dealiased state); one partition: no exchange buffers.
+        // Pencil (Pz > 1): the kept kz modes split in Pz contiguous ranges.
         const size_t nx = n[0], ny = n[1], kzc = (size_t)c->kc[2] + 1, nrl = c->nrl;
-        size_t maxcols = 0;  // B's field stride is uniform over the ranks (peer exchange)
+        if ((int)kzc < Pz) return cleanup(SKG_ECONFIG, "more ranks than kept kz modes");
+        c->nyl = n[1] / Pz;
+        c->zstart.resize(Pz + 1);
+        for (int z = 0; z <= Pz; ++z) c->zstart[z] = (int)((long long)z * (long long)kzc / Pz);
+        size_t maxcols = 0, maxkz = 0;  // B's field stride is uniform over the ranks (peer exchange)
         for (int q = 0; q < world; ++q) maxcols = std::max(maxcols, (size_t)(c->cstart[q + 1] - c->cstart[q]));
-        for (int q = 0; q < world; ++q) {
-            if (nccl_id && q != rank) continue;
-            Part p;
-            p.r = q;
-            p.c0 = c->cstart[q];
-            p.ncols = c->cstart[q + 1] - c->cstart[q];
-            p.vs = nx * p.ncols * kzc;
-            p.fs = std::max(nx * maxcols * kzc, nrl * ny * kzc);
-            p.rfs = nrl * Kyc * kzc;
-            ok = ok && alloc((void**)&p.u, sizeof(cd) * 3 * p.vs);
-            for (int i = 0; i < 3; ++i) ok = ok && alloc((void**)&p.k[i], sizeof(cd) * 3 * p.vs);
-            ok = ok && alloc((void**)&p.A3, sizeof(cd) * 5 * p.fs);
-            ok = ok && alloc((void**)&p.B3, sizeof(cd) * 6 * p.fs);
-            if (world > 1) {
-                ok = ok && alloc((void**)&p.rA3, sizeof(cd) * 5 * p.rfs);
-                ok = ok && alloc((void**)&p.sD3, sizeof(cd) * 3 * p.rfs);
-            } else {
-                p.rA3 = p.A3;
-                p.rfs = p.fs;
-                p.sD3 = p.B3;
+        for (int z = 0; z < Pz; ++z) maxkz = std::max(maxkz, (size_t)(c->zstart[z + 1] - c->zstart[z]));
+        for (int q = 0; q < world; ++q)
+            for (int z = 0; z < Pz; ++z) {
+                if (nccl_id && q * Pz + z != rank) continue;
+                Part p;
+                p.r = q;
+                p.pz = z;
+                p.kz0 = c->zstart[z];
+                p.nkz = c->zstart[z + 1] - c->zstart[z];
+                p.c0 = c->cstart[q];
+                p.ncols = c->cstart[q + 1] - c->cstart[q];
+                p.vs = nx * p.ncols * p.nkz;
+                p.fsz = Pz > 1 ? nrl * (size_t)c->nyl * kzc : 0;
+                p.fs = std::max(std::max(nx * maxcols * maxkz, nrl * ny * maxkz), p.fsz);
+                p.rfs = nrl * Kyc * p.nkz;
+                ok = ok && alloc((void**)&p.u, sizeof(cd) * 3 * p.vs);
+                for (int i = 0; i < 3; ++i) ok = ok && alloc((void**)&p.k[i], sizeof(cd) * 3 * p.vs);
+                ok = ok && alloc((void**)&p.A3, sizeof(cd) * 5 * p.fs);
+                ok = ok && alloc((void**)&p.B3, sizeof(cd) * 6 * p.fs);
+                if (Pz > 1) ok = ok && alloc((void**)&p.Z3, sizeof(cd) * 6 * p.fsz);
+                if (world > 1) {
+                    ok = ok && alloc((void**)&p.rA3, sizeof(cd) * 5 * p.rfs);
+                    ok = ok && alloc((void**)&p.sD3, sizeof(cd) * 3 * p.rfs);
+                } else {
+                    p.rA3 = p.A3;
+                    p.rfs = p.fs;
+                    p.sD3 = p.B3;
+                }
+                c->parts.push_back(p);
             }
-            c->parts.push_back(p);
-        }
         if (ok && nccl_id) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
             if (!nccl().ok) return cleanup(SKG_ENCCL, nccl().why);
-            const ncclResult_t nr = nccl().CommInitRank(&c->comm, world, id, rank);
+            const ncclResult_t nr = nccl().CommInitRank(&c->comm, world * Pz, id, rank);
             if (nr != ncclSuccess) return cleanup(SKG_ENCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(nr));
         }
     } else if (c->dist) {
@@ -301,6 +330,9 @@ int skg_destroy(skg_ctx* c) {
             skg::dfree(p.rA[f]);
         }
         skg::dfree(p.rD3);
+        skg::dfree(p.Z3);
+        skg::dfree(p.sZ);
+        skg::dfree(p.rZ);
         if (p.rA3 != p.A3) skg::dfree(p.rA3);
         if (p.sD3 != p.B3) skg::dfree(p.sD3);
         skg::dfree(p.A3);
@@ -767,18 +799,20 @@ int skg_set_time(skg_ctx* c, double t) {
 static const int kIpcBytes = 4 * (int)sizeof(cudaIpcMemHandle_t);
 
 int skg_dist_ipc_handle(skg_ctx* c, char* out) {
-    if (!c->dist || c->G < 2 || c->parts.size() != 1)
+    if (!c->dist || c->G * c->Pz < 2 || c->parts.size() != 1)
         return fail(SKG_EUNSUPPORTED, "IPC handles: one slab partition per process");
     if (skg::guards_enabled()) return fail(SKG_EUNSUPPORTED, "IPC handles: not with SKG_GUARD=1 (offset allocations)");
     CUDA_TRY(cudaSetDevice(c->device));
     if (int rc = ensure_p2p_bufs(c)) return rc;
     const Part& p = c->parts[0];
     cd* bufs[4] = {p.rI[0], p.rI[1], p.rA[0], p.rA[1]};
-    if (c->solver == 3) {
+    if (c->solver == 3) {  // pencil: + the z-pass input and the y-pass buffer
         bufs[0] = p.rA3;
         bufs[1] = p.rD3;
+        bufs[2] = p.Z3;
+        bufs[3] = p.B3;
     }
-    const int nb = c->solver == 3 ? 2 : 4;
+    const int nb = c->solver == 3 ? (c->Pz > 1 ? 4 : 2) : 4;
     std::memset(out, 0, kIpcBytes);
     for (int b = 0; b < nb; ++b) {
         cudaIpcMemHandle_t h;
@@ -789,19 +823,20 @@ int skg_dist_ipc_handle(skg_ctx* c, char* out) {
 }
 
 int skg_dist_open_peers(skg_ctx* c, const char* all) {
-    if (!c->dist || c->G < 2 || c->parts.size() != 1 || !c->comm)
+    const int W = c->G * c->Pz;  // global ranks (pencil: r Pz + pz)
+    if (!c->dist || W < 2 || c->parts.size() != 1 || !c->comm)
         return fail(SKG_EUNSUPPORTED, "peer exchange across processes: NCCL slab contexts");
-    if (c->G > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
+    if (W > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
     CUDA_TRY(cudaSetDevice(c->device));
     const Part& me = c->parts[0];
-    const int nb = c->solver == 3 ? 2 : 4;
-    for (int q = 0; q < c->G; ++q) {
+    const int nb = c->solver == 3 ? (c->Pz > 1 ? 4 : 2) : 4;
+    for (int q = 0; q < W; ++q) {
         cd* ptr[4] = {nullptr, nullptr, nullptr, nullptr};
-        if (q == me.r) {
+        if (q == c->grank) {
             ptr[0] = c->solver == 3 ? me.rA3 : me.rI[0];
             ptr[1] = c->solver == 3 ? me.rD3 : me.rI[1];
-            ptr[2] = me.rA[0];
-            ptr[3] = me.rA[1];
+            ptr[2] = c->solver == 3 ? me.Z3 : me.rA[0];
+            ptr[3] = c->solver == 3 ? me.B3 : me.rA[1];
         } else {
             for (int b = 0; b < nb; ++b) {
                 cudaIpcMemHandle_t h;
@@ -815,6 +850,8 @@ int skg_dist_open_peers(skg_ctx* c, const char* all) {
         if (c->solver == 3) {
             c->peer_rA3[q] = ptr[0];
             c->peer_D3[q] = ptr[1];
+            c->peer_Z3[q] = ptr[2];
+            c->peer_B3[q] = ptr[3];
             continue;
         }
         c->peer_rI[q][0] = ptr[0];
@@ -832,6 +869,7 @@ long skg_guard_violations(void) { return skg::guard_violations(); }
 int skg_dist_overlap(skg_ctx* c, int enable) {
     if (!c->dist) return fail(SKG_EUNSUPPORTED, "exchange overlap: slab-decomposed contexts");
     c->no_overlap = !enable;
+    c->zpack = enable == 2;  // pencil, single process: the NCCL route's pack / unpack blocks
     return SKG_OK;
 }
 
@@ -840,14 +878,17 @@ int skg_dist_p2p(skg_ctx* c, int enable) {
         c->p2p = false;
         return SKG_OK;
     }
-    if (!c->dist || c->G < 2) return fail(SKG_EUNSUPPORTED, "peer exchange: slab-decomposed contexts");
+    if (!c->dist || c->G * c->Pz < 2) return fail(SKG_EUNSUPPORTED, "peer exchange: slab-decomposed contexts");
     if (c->comm) return fail(SKG_ECONFIG, "multi-process contexts: skg_dist_open_peers");
-    if (c->G > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
+    if (c->G * c->Pz > SKG_MAX_RANKS) return fail(SKG_EUNSUPPORTED, "peer exchange: too many ranks");
+    if (c->G < 2) return SKG_OK;  // 1 x Pz pencil: the kz <-> y transposes store into the parts already
     if (int rc = ensure_p2p_bufs(c)) return rc;
     for (const Part& p : c->parts) {
         if (c->solver == 3) {
-            c->peer_rA3[p.r] = p.rA3;
-            c->peer_D3[p.r] = p.rD3;
+            c->peer_rA3[p.r * c->Pz + p.pz] = p.rA3;
+            c->peer_D3[p.r * c->Pz + p.pz] = p.rD3;
+            c->peer_Z3[p.r * c->Pz + p.pz] = p.Z3;
+            c->peer_B3[p.r * c->Pz + p.pz] = p.B3;
             continue;
         }
         for (int f = 0; f < 2; ++f) {

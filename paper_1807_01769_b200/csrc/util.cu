@@ -224,7 +224,36 @@ MaskGeo make_geo(int dims, const int* n, const int* kc) {
     return g;
 }
 
+// Pencil transposes: one (f, x, y) row of nz contiguous complex per group of
+// 32 lanes; rows grid-strided so the grid stays a multiple of the SM count.
+__global__ void __launch_bounds__(256) box_copy(BoxCopy b, int fence) {
+    const long long rows = (long long)b.nf * b.nx * b.ny;
+    const int lane = threadIdx.x & 31;
+    for (long long r = blockIdx.x * 8ll + (threadIdx.x >> 5); r < rows; r += 8ll * gridDim.x) {
+        const int y = (int)(r % b.ny);
+        const long long q = r / b.ny;
+        const int x = (int)(q % b.nx), f = (int)(q / b.nx);
+        const cd* s = b.src + f * b.sf + x * b.sx + y * b.sy;
+        cd* d = b.dst + f * b.df + x * b.dx + y * b.dy;
+        for (int z = lane; z < b.nz; z += 32) d[z] = s[z];
+    }
+    if (fence) __threadfence_system();
+}
+
 }  // namespace
+
+cudaError_t launch_box_copy(const BoxCopy& b, bool fence, cudaStream_t s, long* launches) {
+    const long long rows = (long long)b.nf * b.nx * b.ny;
+    if (rows == 0 || b.nz == 0) return cudaSuccess;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long want = (rows + 7) / 8;
+    const int grid = (int)(want < 8ll * nsm ? want : 8ll * nsm);
+    box_copy<<<grid, 256, 0, s>>>(b, fence ? 1 : 0);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_transpose_c(const cd* in, cd* out, int rows, int cols, int, cudaStream_t s,
                                long* launches) {
