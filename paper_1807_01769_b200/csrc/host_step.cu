@@ -321,9 +321,11 @@ int exchange_z(skg_ctx* c, int dir, cudaStream_t st) {
         };
         auto rkz = [&](const Part& me, int z) { return dir == 0 ? nkz_of(z) : (size_t)me.nkz; };
         for (Part& me : c->parts) {
-            if (!me.sZ) {
-                CUDA_TRY(skg::dmalloc(&me.sZ, sizeof(cd) * 6 * me.fsz));
-                CUDA_TRY(skg::dmalloc(&me.rZ, sizeof(cd) * 6 * me.fsz));
+            if (!me.sZ) {  // Pz blocks of up to max nkz modes (uneven kz ranges)
+                size_t maxkz = 0;
+                for (int z = 0; z < Pz; ++z) maxkz = std::max(maxkz, nkz_of(z));
+                CUDA_TRY(skg::dmalloc(&me.sZ, sizeof(cd) * 6 * plane * Pz * maxkz));
+                CUDA_TRY(skg::dmalloc(&me.rZ, sizeof(cd) * 6 * plane * Pz * maxkz));
             }
             for (int z = 0; z < Pz; ++z) {  // pack (the own block goes straight to its place)
                 const int dkz0 = c->zstart[z], dnkz = (int)nkz_of(z);
