@@ -20,12 +20,13 @@ def partition(Kc, nx, G):
     return cstart, nx // G
 
 
-def _a2a(send_blocks, recv_sizes):
-    """all_to_all_single of complex blocks (lists indexed by peer)."""
+def _a2a(send_blocks, recv_sizes, group=None):
+    """all_to_all_single of complex blocks (lists indexed by peer; group: the
+    sub-communicator of a pencil row / column, default the world)."""
     s = torch.from_numpy(np.concatenate([b.view(np.float64) for b in send_blocks]))
     r = torch.empty(2 * sum(recv_sizes), dtype=torch.float64)
     dist.all_to_all_single(r, s, output_split_sizes=[2 * x for x in recv_sizes],
-                           input_split_sizes=[b.size * 2 for b in send_blocks])
+                           input_split_sizes=[b.size * 2 for b in send_blocks], group=group)
     out, o = [], 0
     rn = r.numpy().view(np.complex128)
     for x in recv_sizes:
@@ -167,3 +168,84 @@ def slab3d_tendency(v_full, n, rank, G):
     if c0 == 0:
         out[:, 0, 0, 0] = 0
     return out, gky[c0:c1], kzc
+
+
+# ------------------------------------------------------------------ ns3d pencil
+def pencil_groups(py, pz):
+    """Sub-communicators of the py x pz process grid (global rank = r_y pz +
+    r_z, csrc/skgpu.cu skg_create_pencil): for every rank its ky / x group
+    (equal r_z, py members) and its kz / y group (equal r_y, pz members).
+    Collective: every rank creates all groups in the same order."""
+    gy = [dist.new_group([q * pz + z for q in range(py)]) for z in range(pz)]
+    gz = [dist.new_group([r * pz + z for z in range(pz)]) for r in range(py)]
+    return gy, gz
+
+
+def pencil3d_tendency(v_full, n, rank, py, pz, groups):
+    """Dealiased-path ns3d tendency on part (r_y, r_z) of the pencil layout
+    with the block layouts of csrc/host_step.cu exchange3 (inside the ky / x
+    group, per-part kz range) and exchange_z (the kz <-> y transposes, NCCL
+    route: contiguous [xl][yl][kz] blocks per member).  Returns this part's
+    lines (3, nx, nkyl, nkz), their global ky indices and the kz range."""
+    nx, ny, nz = n
+    ry, rz = divmod(rank, pz)
+    gy, gz = groups[0][rz], groups[1][ry]
+    kx, ky, kz = O.k_axes(n)
+    mask = O.dealias_mask(n).astype(bool)
+    kcy = int(np.abs(ky[mask[0, :, 0]]).max() / (ky[1] - ky[0]) + 0.5)
+    kzc = int(mask[0, 0].sum())
+    Kyc = 2 * kcy + 1
+    gky = np.array(list(range(kcy + 1)) + list(range(ny - kcy, ny)))
+    kstart, nrl = partition3(Kyc, nx, py)
+    zstart = [z * kzc // pz for z in range(pz + 1)]
+    nkzs = [zstart[z + 1] - zstart[z] for z in range(pz)]
+    k0, k1 = zstart[rz], zstart[rz + 1]
+    nkz, nyl = k1 - k0, ny // pz
+    c0, c1 = kstart[ry], kstart[ry + 1]
+    nl = [kstart[q + 1] - kstart[q] for q in range(py)]
+    V = v_full[:, :, gky[c0:c1], k0:k1]                    # (3, nx, nkyl, nkz)
+    KX = kx[:, None, None]
+    X = [np.fft.ifft(f, axis=0) * nx for f in (V[0], V[1], V[2], KX * V[1], KX * V[2])]
+    sizes = [nrl * nl[q] * nkz for q in range(py)]
+    R = [_a2a([x[q * nrl:(q + 1) * nrl].reshape(-1).copy() for q in range(py)], sizes, gy) for x in X]
+    P = [np.concatenate([Rf[q].reshape(nrl, nl[q], nkz) for q in range(py)], axis=1) for Rf in R]
+    KY = ky[gky][None, :, None]
+    KZ = kz[k0:k1][None, None, :]
+    spec = [P[0], P[1], P[2], 1j * KY * P[2] - 1j * KZ * P[1], 1j * KZ * P[0] - 1j * P[4],
+            1j * P[3] - 1j * KY * P[0]]
+    def y_inverse(h):                                      # (xl, ny, nkz)
+        full = np.zeros((nrl, ny, nkz), complex)
+        full[:, gky, :] = h
+        return np.fft.ifft(full, axis=1) * ny
+    def kz_to_y(f):                                        # -> (xl, nyl, kzc)
+        rs = [nrl * nyl * nkzs[z] for z in range(pz)]
+        got = _a2a([f[:, z * nyl:(z + 1) * nyl, :].reshape(-1).copy() for z in range(pz)], rs, gz)
+        return np.concatenate([got[z].reshape(nrl, nyl, nkzs[z]) for z in range(pz)], axis=2)
+    def c2r_z(h):
+        full = np.zeros((nrl, nyl, nz // 2 + 1), complex)
+        full[..., :kzc] = h
+        full[..., 0] = full[..., 0].real
+        return np.fft.irfft(full, n=nz, axis=2) * nz
+    ux, uy, uz, ox, oy, oz = (c2r_z(kz_to_y(y_inverse(h))) for h in spec)
+    cross = [uy * oz - uz * oy, uz * ox - ux * oz, ux * oy - uy * ox]
+    def y_to_kz(c):                                        # (xl, nyl, kzc) -> (xl, ny, nkz)
+        rs = [nrl * nyl * nkz] * pz
+        got = _a2a([c[:, :, zstart[z]:zstart[z + 1]].reshape(-1).copy() for z in range(pz)], rs, gz)
+        return np.concatenate([got[z].reshape(nrl, nyl, nkz) for z in range(pz)], axis=1)
+    D = [np.fft.fft(y_to_kz(np.fft.rfft(c, axis=2)[..., :kzc] / (nx * ny * nz)), axis=1)[:, gky, :]
+         for c in cross]                                   # (xl, Kyc, nkz)
+    sizes = [nrl * nl[ry] * nkz] * py
+    RD = [_a2a([d[:, kstart[q]:kstart[q + 1]].reshape(-1).copy() for q in range(py)], sizes, gy) for d in D]
+    out = [np.fft.fft(np.concatenate([r[q].reshape(nrl, nl[ry], nkz) for q in range(py)], axis=0), axis=0)
+           for r in RD]
+    KYl = ky[gky[c0:c1]][None, :, None]
+    ksq = KX ** 2 + KYl ** 2 + KZ ** 2
+    nzm = ksq != 0
+    s = (KX * out[0] + KYl * out[1] + KZ * out[2]) / np.where(nzm, ksq, 1.0)
+    out = [np.where(nzm, out[0] - KX * s, out[0]), np.where(nzm, out[1] - KYl * s, out[1]),
+           np.where(nzm, out[2] - KZ * s, out[2])]
+    keep = mask[:, gky[c0:c1], k0:k1]
+    out = np.stack([np.where(keep, o, 0) for o in out])
+    if c0 == 0 and k0 == 0:
+        out[:, 0, 0, 0] = 0
+    return out, gky[c0:c1], (k0, k1)
