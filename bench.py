@@ -284,12 +284,25 @@ def run_our_arm(args):
     S = u0.size  # complex modes over all variables
     slab = ws > 1
     p2p_used = False
+    grid = None
+    if args.decomp == "pencil":
+        if solver != "ns3d":
+            raise SystemExit("bench.py: --decomp pencil is an ns3d decomposition")
+        if args.grid:
+            grid = tuple(int(x) for x in args.grid.lower().split("x"))
+        else:  # the paper's process grids: 2x2 at 4 ranks, 2x4 at 8
+            grid = {1: (2, 2), 2: (1, 2), 4: (2, 2), 8: (2, 4), 16: (4, 4)}.get(ws, (1, ws))
     if slab:
         # slab decomposition over the ranks (strong scaling of
         # one grid), transposes as NCCL all-to-all inside libskgpu
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
+        if grid is not None:  # BASELINE configs[4]: py x pz pencils, two transposes per 3D FFT
+            if grid[0] * grid[1] != ws:
+                raise SystemExit(f"bench.py: --grid {grid[0]}x{grid[1]} needs {grid[0] * grid[1]} ranks")
+            sim = api.Simulation(solver, n, nu, dt, device=local, rank=rank, nccl_id=obj[0], pencil=grid)
+        else:
+            sim = api.Simulation(solver, n, nu, dt, device=local, world=ws, rank=rank, nccl_id=obj[0])
         if not args.no_p2p:
             # fused exchange: the pass epilogues store into the owners'
             # receive buffers (CUDA IPC over NVLink); every rank must agree,
@@ -309,6 +322,10 @@ def run_our_arm(args):
                 if rank == 0:
                     print(f"peer exchange unavailable ({why or 'another rank failed'}); "
                           "NCCL all-to-all", file=sys.stderr)
+    elif grid is not None:
+        # one GPU: all py x pz parts in this process, device copies as the
+        # exchanges (the decomposition's compute and layout cost, no NVLink)
+        sim = api.Simulation(solver, n, nu, dt, device=local, pencil=grid)
     else:
         compact = args.layout == "compact" or (args.layout == "auto" and args.config in COARSE_IC)
         sim = api.Simulation(solver, n, nu, dt, device=local, compact=compact)
@@ -324,6 +341,7 @@ def run_our_arm(args):
         if dist is not None:
             dist.barrier()
 
+    nparts = grid[0] * grid[1] if (grid and not slab) else 1
     # ---- warm-up (also captures the per-step CUDA graph)
     sim.step(args.warmup)
     l0 = sim.launch_count
@@ -466,8 +484,12 @@ def run_our_arm(args):
                 "workload": f"{args.config}: {solver} {'x'.join(map(str, n))} RK4 step, "
                             f"nu={nu}, dt={dt:.6g} (CFL 0.5)",
                 "solver": solver, "n": list(n), "global_batch": 1 if slab else ws,
-                "parallelism": (f"slab{ws} ({'peer-memory exchange over NVLink' if p2p_used else 'NCCL all-to-all'})"
-                                if slab else "single-gpu"),
+                "parallelism": (
+                    (f"pencil {grid[0]}x{grid[1]}" if grid else f"slab{ws}") +
+                    f" ({'peer-memory exchange over NVLink' if p2p_used else 'NCCL all-to-all'})"
+                    if slab else
+                    f"pencil {grid[0]}x{grid[1]}, all parts on one GPU (device copies as the exchanges)"
+                    if grid else "single-gpu"),
                 "l2": "every field array > 126 MB L2; no flush needed",
                 "dealiased_fast_path": pruned,
             },
@@ -479,10 +501,11 @@ def run_our_arm(args):
                          "step_frac": (step_bytes / (ms_step / 1e3) / 1e9) / peak},
             "fmp_roofline": fmp,
             "fp64_roofline": fp64,
-            "all_to_all": ({"bytes_per_step_per_gpu": stats["exchange"][2] / k_inst,
+            # one GPU with all pencil parts: the exchange class sums over the parts
+            "all_to_all": ({"bytes_per_step_per_gpu": stats["exchange"][2] / k_inst / nparts,
                             "ms_per_step": stats["exchange"][0] / k_inst,
-                            "t_roof_ms_at_900GBps": stats["exchange"][2] / k_inst / 900e9 * 1e3}
-                           if slab else None),
+                            "t_roof_ms_at_900GBps": stats["exchange"][2] / k_inst / nparts / 900e9 * 1e3}
+                           if slab or grid else None),
             "kernels": kernels,
             "instrumented": {"steps": k_inst, "ms_per_step": inst_ms_step,
                              "note": "per-kernel CUDA events (no graph); roofline.achieved uses these"},
@@ -515,6 +538,11 @@ def main():
     ap.add_argument("--no-p2p", action="store_true",
                     help="slab under torchrun: NCCL all-to-all copies instead of the peer-memory "
                          "exchange (CUDA IPC stores from the pass epilogues, the default)")
+    ap.add_argument("--decomp", choices=["slab", "pencil"], default="slab",
+                    help="multi-GPU decomposition of ns3d: slab (one all-to-all per 3D FFT, the "
+                         "default: fewer NVLink bytes up to 8 GPUs) or the py x pz pencils BASELINE "
+                         "configs[4] names (two all-to-alls per 3D FFT)")
+    ap.add_argument("--grid", default="", help="pencil process grid PYxPZ (default 2x2 / 2x4 at 4 / 8 ranks)")
     ap.add_argument("--layout", choices=["auto", "full", "compact"], default="auto",
                     help="ns3d one-GPU layout (auto: compact where the full layout does not fit)")
     args = ap.parse_args()

@@ -159,3 +159,33 @@ def test_pencil_exchange_volume_matches_model(n, grid):
     t2 = 9 * nx * ny * kz * 16 * (pz - 1) / pz
     model = 4 * (t1 + t2) / (py * pz)
     assert abs(got - model) <= 1e-9 * model
+
+
+@pytest.mark.slow
+def test_real_split_ns3d_512_pencil_2x4():
+    """BASELINE configs[3]'s grid on the 2 x 4 process grid of configs[4]
+    (8 parts on one GPU): equals one partition; measured exchange volume per
+    GPU = the kept-mode pencil model."""
+    n, grid = (512, 512, 512), (2, 4)
+    py, pz = grid
+    u0 = ic.ns3d_ic(n, seed=1234)
+    dt = ic.cfl_dt("ns3d", n, u0)
+    one = api.Simulation("ns3d", n, 2e-4, dt)
+    one.set_state(u0)
+    one.step(3)
+    ref = one.get_state()
+    one.close()
+    d = api.Simulation("ns3d", n, 2e-4, dt, pencil=grid)
+    d.set_state(u0)
+    d.step(3)
+    s = d.get_state()
+    for v in range(3):
+        assert O.rel_l2(s[v], ref[v]) < 1e-14
+    del s
+    K, kz = 341, 171
+    t1 = 8 * n[0] * K * kz * 16 * (py - 1) / py
+    t2 = 9 * n[0] * n[1] * kz * 16 * (pz - 1) / pz
+    model = 4 * (t1 + t2) / (py * pz)
+    got = a2a_bytes_per_gpu_step(d, py * pz, 1)
+    assert abs(got - model) <= 1e-9 * model
+    d.close()
