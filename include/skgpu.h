@@ -105,6 +105,9 @@ int skg_dist_p2p(skg_ctx* ctx, int enable);
  * enable == 2 (pencil contexts with all parts in one process; tests): the kz
  * <-> y transposes run the NCCL route's pack -> block transfer -> unpack
  * instead of direct strided stores, with copies standing in for send / recv.
+ * enable == 3 (pencil): the kz -> y transpose as a separate strided-copy
+ * kernel instead of the y-inverse kernel's own stores (the default wherever
+ * the members' buffers are addressable).
  */
 int skg_dist_overlap(skg_ctx* ctx, int enable);
 

@@ -147,6 +147,7 @@ struct skg_ctx {
     // ns3d pencil: G ranks along ky lines / x rows times Pz ranks along the
     // kept kz / y rows; global rank = r Pz + pz; zstart: kz ranges (Pz + 1)
     int Pz = 1, nyl = 0;
+    bool zfuse = true;   // kz -> y transpose from the y-inverse's stores (skg_dist_overlap(ctx, 3): off)
     bool zpack = false;  // single process: run the NCCL route's pack / unpack (skg_dist_overlap(ctx, 2))
     std::vector<int> zstart;
     cd* peer_Z3[SKG_MAX_RANKS] = {};   // pencil: z-pass input buffers (Z3) by global rank

@@ -257,6 +257,19 @@ int exchange_z(skg_ctx* c, int dir, cudaStream_t st) {
     if (!st) st = c->stream;
     const int Pz = c->Pz;
     if (Pz == 1) return SKG_OK;
+    if (dir == 2) {  // the y-inverse stored into the members' Z3 already: the barrier remains
+        const skg::LaunchHook hook = hook_of(c);
+        double moved = 0.0;  // bytes its stores sent to other members
+        for (const Part& s : c->parts)
+            moved += (double)sizeof(cd) * 6 * c->nrl * c->nyl * s.nkz * (Pz - 1);
+        hook.begin(4);
+        hook.end(4, moved);
+        if (c->comm) {
+            const ncclResult_t nr = nccl().AllReduce(c->d_barrier, c->d_barrier, 1, ncclDouble, ncclSum, c->comm, st);
+            if (nr != ncclSuccess) return fail(SKG_ENCCL, nccl().GetErrorString(nr));
+        }
+        return SKG_OK;
+    }
     const size_t nrl = (size_t)c->nrl, ny = (size_t)c->n[1], nyl = (size_t)c->nyl;
     const size_t kzf = (size_t)c->kc[2] + 1;
     const int nf = dir == 0 ? 6 : 3;
@@ -453,6 +466,9 @@ int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool las
         // pencil: x-inverse, all-to-all over the ky / x split, y-inverse,
         // kz -> y transpose, z pass on own (x, y) rows with all kept kz,
         // y -> kz transpose, y-forward, all-to-all back, x-forward + RK
+        // kz -> y transpose fused into the y-inverse's stores wherever the
+        // members' buffers are addressable (one process, or peer memory)
+        const bool zfused = c->zfuse && (c->comm ? c->p2p : !c->zpack);
         auto run = [&](int pass, int st) -> int {
             for (const Part& p : c->parts) {
                 skg::Ns3dArgs a = args3d_part(c, dt, p);
@@ -463,6 +479,20 @@ int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool las
                     a.kz_in = a.kz_o = c->kc[2] + 1;
                 } else if (pass == 4) {  // y-forward input: fields 3..5 of B3
                     a.A = p.B3 + 3 * p.fs;
+                } else if (pass == 5 && zfused) {  // y-inverse stores go to the members' Z3
+                    a.zfused = 1;
+                    a.nyl = c->nyl;
+                    while ((1 << a.lg_nyl) < a.nyl) ++a.lg_nyl;
+                    a.kzf = c->kc[2] + 1;
+                    a.fsz = p.fsz;
+                    for (int z = 0; z < c->Pz; ++z) {
+                        if (c->comm) {
+                            a.peer_Z[z] = c->peer_Z3[p.r * c->Pz + z];
+                        } else {
+                            for (const Part& q : c->parts)
+                                if (q.r == p.r && q.pz == z) a.peer_Z[z] = q.Z3;
+                        }
+                    }
                 }
                 CUDA_TRY(skg::ns3d_pass(a, pass, st, c->stream, counter, hook));
             }
@@ -470,7 +500,7 @@ int enqueue_dist_step(skg_ctx* c, double dt, long* counter, bool first, bool las
         };
         for (int st = 1; st <= nst; ++st) {
             if ((rc = run(0, st)) || (rc = exchange(c, 0))) return rc;
-            if ((rc = run(5, st)) || (rc = exchange_z(c, 0))) return rc;
+            if ((rc = run(5, st)) || (rc = exchange_z(c, zfused ? 2 : 0))) return rc;
             if ((rc = run(6, st)) || (rc = exchange_z(c, 1))) return rc;
             if ((rc = run(4, st)) || (rc = exchange(c, 1))) return rc;
             if (st == 1 && c->adaptive && (rc = dist_dt_update(c, counter))) return rc;

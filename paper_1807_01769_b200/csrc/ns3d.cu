@@ -455,12 +455,22 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
         }
         F::template run<+1>(v, sm, t, wb, salt);
         if (active) {
-            cd* out = a.B + m * a.fstride;
+            if (a.zfused) {  // pencil: straight into the row owner's z-pass input
+                const size_t base = m * a.fsz + (size_t)x * a.nyl * a.kzf + a.kz0 + kz;
 #pragma unroll
-            for (int e = 0; e < E; ++e)
-                out[((size_t)x * a.ny + (t + T * e)) * a.kz_in + kz] = v[e];
+                for (int e = 0; e < E; ++e) {
+                    const int y = t + T * e;
+                    a.peer_Z[y >> a.lg_nyl][base + (size_t)(y & (a.nyl - 1)) * a.kzf] = v[e];
+                }
+            } else {
+                cd* out = a.B + m * a.fstride;
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    out[((size_t)x * a.ny + (t + T * e)) * a.kz_in + kz] = v[e];
+            }
         }
     }
+    if (a.zfused && a.p2p) __threadfence_system();  // peer stores visible before the barrier
     __syncthreads();  // smem (stage, line offsets) free for the next tile
 }
 

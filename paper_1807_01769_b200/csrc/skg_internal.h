@@ -242,6 +242,13 @@ struct Ns3dArgs {
     // modes [kz0, kz0 + kz_in) only (local index kz, global kz0 + kz); the
     // factor tables e1z / e2z are passed already shifted by kz0.
     int kz0 = 0;
+    // kz -> y transpose fused into the y-inverse's stores (zfused; all parts
+    // in one process or peer memory): output (m, x, y, kz) goes straight to
+    // the z-pass input of the pz-group member y / nyl, Z3 [xl][yl][kzf]
+    // (field stride fsz), instead of this rank's B.
+    int zfused = 0, lg_nyl = 0, nyl = 0, kzf = 0;
+    size_t fsz = 0;
+    cd* peer_Z[SKG_MAX_RANKS];
 };
 
 // Programmatic dependent launch (sm_90+): step kernels are launched with

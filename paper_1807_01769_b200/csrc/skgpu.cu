@@ -868,8 +868,15 @@ long skg_guard_violations(void) { return skg::guard_violations(); }
 
 int skg_dist_overlap(skg_ctx* c, int enable) {
     if (!c->dist) return fail(SKG_EUNSUPPORTED, "exchange overlap: slab-decomposed contexts");
+    if (c->gexec) {  // the captured step holds the old exchange sequence
+        CUDA_TRY(cudaSetDevice(c->device));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
     c->no_overlap = !enable;
     c->zpack = enable == 2;  // pencil, single process: the NCCL route's pack / unpack blocks
+    c->zfuse = enable != 3;  // 3: the kz -> y transpose as a separate strided-copy kernel
     return SKG_OK;
 }
 

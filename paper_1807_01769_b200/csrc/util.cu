@@ -1,5 +1,6 @@
 // util.cu -- layout transposes, dealias-state check, device grid dump and
 // diagnostic reductions.
+#include <algorithm>
 #include "skg_internal.h"
 
 #include <cstdlib>
@@ -224,18 +225,30 @@ MaskGeo make_geo(int dims, const int* n, const int* kc) {
     return g;
 }
 
-// Pencil transposes: one (f, x, y) row of nz contiguous complex per group of
-// 32 lanes; rows grid-strided so the grid stays a multiple of the SM count.
+// Pencil transposes: blockIdx.y = (f, x), the (y, z) plane of nz-long
+// contiguous runs flattened over the threads (every lane busy whatever nz is),
+// four independent 16-byte loads in flight per thread.
 __global__ void __launch_bounds__(256) box_copy(BoxCopy b, int fence) {
-    const long long rows = (long long)b.nf * b.nx * b.ny;
-    const int lane = threadIdx.x & 31;
-    for (long long r = blockIdx.x * 8ll + (threadIdx.x >> 5); r < rows; r += 8ll * gridDim.x) {
-        const int y = (int)(r % b.ny);
-        const long long q = r / b.ny;
-        const int x = (int)(q % b.nx), f = (int)(q / b.nx);
-        const cd* s = b.src + f * b.sf + x * b.sx + y * b.sy;
-        cd* d = b.dst + f * b.df + x * b.dx + y * b.dy;
-        for (int z = lane; z < b.nz; z += 32) d[z] = s[z];
+    const unsigned x = blockIdx.y % b.nx, f = blockIdx.y / b.nx;
+    const cd* __restrict__ s = b.src + f * b.sf + x * b.sx;
+    cd* __restrict__ d = b.dst + f * b.df + x * b.dx;
+    const unsigned nz = b.nz, total = (unsigned)b.ny * nz, stride = gridDim.x * 256u;
+    unsigned i = blockIdx.x * 256u + threadIdx.x;
+    for (; i + 3u * stride < total; i += 4u * stride) {
+        cd v[4];
+        size_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned idx = i + k * stride, y = idx / nz, z = idx - y * nz;
+            v[k] = s[y * b.sy + z];
+            o[k] = y * b.dy + z;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[o[k]] = v[k];
+    }
+    for (; i < total; i += stride) {
+        const unsigned y = i / nz, z = i - y * nz;
+        d[y * b.dy + z] = s[y * b.sy + z];
     }
     if (fence) __threadfence_system();
 }
@@ -243,14 +256,11 @@ __global__ void __launch_bounds__(256) box_copy(BoxCopy b, int fence) {
 }  // namespace
 
 cudaError_t launch_box_copy(const BoxCopy& b, bool fence, cudaStream_t s, long* launches) {
-    const long long rows = (long long)b.nf * b.nx * b.ny;
-    if (rows == 0 || b.nz == 0) return cudaSuccess;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const long long want = (rows + 7) / 8;
-    const int grid = (int)(want < 8ll * nsm ? want : 8ll * nsm);
-    box_copy<<<grid, 256, 0, s>>>(b, fence ? 1 : 0);
+    const long long planes = (long long)b.nf * b.nx, per = (long long)b.ny * b.nz;
+    if (planes == 0 || per == 0) return cudaSuccess;
+    if (planes > 65535 || per >= (1ll << 31)) return cudaErrorInvalidValue;
+    const int gx = (int)std::min<long long>((per + 1023) / 1024, 64);
+    box_copy<<<dim3(gx, (unsigned)planes), 256, 0, s>>>(b, fence ? 1 : 0);
     ++*launches;
     return cudaGetLastError();
 }

@@ -12,7 +12,7 @@ from paper_1807_01769_b200 import api, ic
 pytestmark = pytest.mark.gpu
 
 
-def run_pair(n, grid, steps=3, nu=1e-3, seed=7, p2p=False, packed=False):
+def run_pair(n, grid, steps=3, nu=1e-3, seed=7, p2p=False, packed=False, unfused=False):
     u0 = ic.ns3d_ic(n, seed=seed)
     dt = ic.cfl_dt("ns3d", n, u0)
     one = api.Simulation("ns3d", n, nu, dt)
@@ -23,6 +23,8 @@ def run_pair(n, grid, steps=3, nu=1e-3, seed=7, p2p=False, packed=False):
         d.enable_p2p()
     if packed:
         d.set_overlap(2)
+    if unfused:
+        d.set_overlap(3)
     d.set_state(u0)
     d.step(steps)
     return d, one
@@ -61,16 +63,25 @@ def test_pencil_matches_reference(ref_lib, n, grid):
 
 @pytest.mark.parametrize("n,grid", [((32, 32, 32), (2, 2)), ((64, 64, 64), (2, 4)), ((128, 128, 128), (4, 2))])
 def test_pencil_peer_and_packed_routes_match(n, grid):
-    """The three exchange routes agree bit for bit: direct strided stores
-    into the members' buffers (single process), the peer-memory route of the
-    ky / x all-to-all (producers store into the owners' blocks), and the NCCL
-    route's pack -> block transfer -> unpack with copies as send / recv."""
+    """The exchange routes agree bit for bit: the kz -> y transpose from the
+    y-inverse kernel's own stores into the members' buffers (the default with
+    all parts in one process) or as a separate strided-copy kernel, the
+    peer-memory route of the ky / x all-to-all (producers store into the
+    owners' blocks), and the NCCL route's pack -> block transfer -> unpack with
+    copies as send / recv."""
     a, one = run_pair(n, grid, steps=4)
     b, _ = run_pair(n, grid, steps=4, p2p=True)
     c, _ = run_pair(n, grid, steps=4, packed=True)
+    e, _ = run_pair(n, grid, steps=4, unfused=True)
     sa = a.get_state()
     assert np.array_equal(sa, b.get_state())
     assert np.array_equal(sa, c.get_state())
+    assert np.array_equal(sa, e.get_state())
+    # switching the route between calls re-captures the step graph
+    e.set_overlap(1)
+    e.step(4)
+    a.step(4)
+    assert np.array_equal(a.get_state(), e.get_state())
     r = one.get_state()
     for v in range(3):
         assert O.rel_l2(sa[v], r[v]) < 1e-14
