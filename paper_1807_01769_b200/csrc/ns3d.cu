@@ -487,18 +487,36 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
 // ------------------------------------------------------------------ z pass
 // Per group: one row pair (r, r+1) of (x, y) rows along z.
 // 8 elements per thread (twice the warps per byte of shared memory).
+// Elements per thread of the z lines: 8, except where 16 saves an exchange
+// (1024 = 16 * 16 * 4: three passes instead of four).
+#ifndef SKG3_ZE128
+#define SKG3_ZE128 8
+#endif
+#ifndef SKG3_ZE1024
+#define SKG3_ZE1024 8
+#endif
+#ifndef SKG3_ZG1024
+#define SKG3_ZG1024 0
+#endif
+template <int NZ>
+constexpr int ze3() { return NZ == 128 ? SKG3_ZE128 : NZ == 1024 ? SKG3_ZE1024 : 8; }
+
 template <int NZ>
 struct Z3 {
-    using F = BFFT<NZ, false, 8>;
+    using F = BFFT<NZ, false, ze3<NZ>()>;
     static constexpr int T = F::T;
-    static constexpr int G = NZ == 128                      ? SKG3_ZG128
-                             : (NZ == 512 && zstage<NZ>())  ? SKG3_ZG512
-                             : (NZ == 1024 && zstage<NZ>()) ? 1
-                             : T >= 256                     ? 1
-                                                            : 256 / T;
+    static constexpr int G = NZ == 128                          ? SKG3_ZG128
+                             : (NZ == 512 && zstage<NZ>())      ? SKG3_ZG512
+                             : (NZ == 1024 && zstage<NZ>())     ? 1
+                             : (NZ == 1024 && SKG3_ZG1024 != 0) ? SKG3_ZG1024
+                             : T >= 256                         ? 1
+                                                                : 256 / T;
     static constexpr bool STG = zstage<NZ>(), REG = zreg<NZ>();
     // resident CTAs: 2, or 6 groups per SM at 512 (168 registers)
-    static constexpr int MINB = (NZ == 512 && STG) ? 6 / G : (NZ == 1024 && STG) ? 3 : 2;
+    static constexpr int MINB = (NZ == 512 && STG)                             ? 6 / G
+                                : (NZ == 1024 && STG)                          ? 3
+                                : (NZ == 1024 && ze3<NZ>() == 16 && G * T >= 256) ? 1
+                                                                               : 2;
     // exchange + 5 rows of doubles (cd units); staged: 3 rows when the
     // second inverse output stays in registers, + the bulk-copy stage of
     // one packed pair
