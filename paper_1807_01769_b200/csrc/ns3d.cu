@@ -487,16 +487,23 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2s_3d(Ns3dArgs a) 
 // ------------------------------------------------------------------ z pass
 // Per group: one row pair (r, r+1) of (x, y) rows along z.
 // 8 elements per thread (twice the warps per byte of shared memory).
-// Elements per thread of the z lines: 8, except where 16 saves an exchange
-// (1024 = 16 * 16 * 4: three passes instead of four).
+// Elements per thread of the z lines: 8, except at 1024, where 16 saves an
+// exchange of the shared-memory-bound pass (1024 = 16 * 16 * 4: three passes
+// instead of 8 * 8 * 8 * 2's four) at 64 threads per line.  Measured at
+// 1024^3 (ms per z-pass launch / ms per step, B200): 8 elements, 2 groups of
+// 128 threads per CTA 28.1 / 318.2; 16 elements with 2 groups per CTA (two
+// CTAs per SM) 22.9 / 297.4, 4 groups (one CTA) 23.7 / 301.0, ONE group per
+// 64-thread CTA (three CTAs per SM) 22.3 / 295.0, staged inputs (bulk copies,
+// SKG3_ZSTAGE1024) 25.1 / 306.0.  At 128^3 16 elements are slower (8 threads
+// per line: 0.572 -> 0.632 ms/step with 16 groups per CTA, 0.722 with 28).
 #ifndef SKG3_ZE128
 #define SKG3_ZE128 8
 #endif
 #ifndef SKG3_ZE1024
-#define SKG3_ZE1024 8
+#define SKG3_ZE1024 16
 #endif
 #ifndef SKG3_ZG1024
-#define SKG3_ZG1024 0
+#define SKG3_ZG1024 1
 #endif
 template <int NZ>
 constexpr int ze3() { return NZ == 128 ? SKG3_ZE128 : NZ == 1024 ? SKG3_ZE1024 : 8; }
@@ -1097,9 +1104,19 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
 
 // 128-thread CTAs (fewer kz lanes, finer kz blocks) when 256-thread CTAs
 // would leave SMs idle (small grids)
+// 1024-point strided passes with 512-thread CTAs (8 kz lanes: 128-byte runs
+// instead of 64, one CTA per SM); bit 0 x-inverse, 1 x-forward, 2 y-inverse,
+// 3 y-forward.
+#ifndef SKG3_CT1024
+#define SKG3_CT1024 0
+#endif
+
 template <int NX>
 cudaError_t launch_x3(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NX, 256>::C;
+    if constexpr (NX == 1024 && (SKG3_CT1024 & 3) != 0) {
+        if (a.pruned && ((SKG3_CT1024 >> (inverse ? 0 : 1)) & 1)) return launch_x3_v<NX, 512>(a, stage, inverse, s);
+    }
     if constexpr (C > 1) {
         const int kz = inverse ? a.kz_in : a.kz_o;
         if (a.nkyl * ((kz + C - 1) / C) < a.wave) return launch_x3_v<NX, 128>(a, stage, inverse, s);
@@ -1113,7 +1130,7 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     using F = BF3<NY>;
     const size_t smem = sizeof(cd) * F::SMEM * C + 2 * sizeof(int) * NY;  // + line offsets, owners
     const bool zb = NY >= 16 && 8 * a.kcy < 3 * NY;  // kept ky clear of the per-thread zero band
-    if (inverse && CT <= 256 && a.pruned) {
+    if (inverse && a.pruned) {
         const size_t smem_s = sizeof(cd) * ((size_t)F::SMEM * C + (size_t)(2 * a.kcy + 1) * C) +
                               sizeof(int) * NY;
         // the two output halves in separate CTAs (ms/step: 64^3 0.218 -> 0.202,
@@ -1141,6 +1158,9 @@ cudaError_t launch_y3_v(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
 template <int NY>
 cudaError_t launch_y3(const Ns3dArgs& a, bool inverse, cudaStream_t s) {
     constexpr int C = Strided<NY, 256>::C;
+    if constexpr (NY == 1024 && (SKG3_CT1024 & 12) != 0) {
+        if (a.pruned && ((SKG3_CT1024 >> (inverse ? 2 : 3)) & 1)) return launch_y3_v<NY, 512>(a, inverse, s);
+    }
     if constexpr (C > 1) {
         const int kz = inverse ? a.kz_in : a.kz_o;
         if (a.nrl * ((kz + C - 1) / C) < a.wave) return launch_y3_v<NY, 128>(a, inverse, s);
