@@ -1106,9 +1106,13 @@ cudaError_t launch_x3_v(const Ns3dArgs& a, int stage, bool inverse, cudaStream_t
 // would leave SMs idle (small grids)
 // 1024-point strided passes with 512-thread CTAs (8 kz lanes: 128-byte runs
 // instead of 64, one CTA per SM); bit 0 x-inverse, 1 x-forward, 2 y-inverse,
-// 3 y-forward.
+// 3 y-forward.  Measured at 1024^3 (ms per launch, 256- vs 512-thread CTAs):
+// x-inverse 11.9 -> 10.9, x-forward + RK 13.0 -> 10.4, y-inverse 18.2 -> 17.7,
+// y-forward 8.24 -> 8.63 (kept at 256); step 297.4 -> 282.1 ms.  (At 512^3
+// the 256-thread CTAs already have 128-byte runs and 512 threads measured
+// slower, DESIGN 6b.)
 #ifndef SKG3_CT1024
-#define SKG3_CT1024 0
+#define SKG3_CT1024 7
 #endif
 
 template <int NX>

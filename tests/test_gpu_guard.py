@@ -1,7 +1,8 @@
 """Out-of-bounds write check of every kernel class (compute-sanitizer is
 refused on the GPU pool): the small step cases of tools/sanitize_case.py --
 general and fast ns2d kernels, ns3d passes, slab emulation with the copy,
-overlapped-copy and peer-memory exchanges -- run in a
+overlapped-copy and peer-memory exchanges, pencil grids with the fused,
+unfused and packed transposes -- run in a
 subprocess with SKG_GUARD=1, where every device allocation has 64 KB guard
 zones; no guard byte may change."""
 import os

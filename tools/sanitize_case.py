@@ -22,6 +22,12 @@ CASES = {
     "ns3d_16": ("ns3d", (16, 16, 16), 1, False),
     "ns3d_32_w2_p2p": ("ns3d", (32, 32, 32), 2, True),
     "ns3d_32_w4": ("ns3d", (32, 32, 32), 4, False),   # overlapped copy exchange
+    # pencil grids (world = (py, pz)): fused kz -> y stores, packed (NCCL-route) blocks,
+    # peer-memory ky / x exchange; uneven kz ranges (11 kept kz over 4 and 3... ranks)
+    "ns3d_32_p2x2": ("ns3d", (32, 32, 32), (2, 2), False),
+    "ns3d_32_p2x4_p2p": ("ns3d", (32, 32, 32), (2, 4), True),
+    "ns3d_p1x4_packed": ("ns3d", (16, 64, 32), (1, 4), "packed"),
+    "ns3d_p4x2_unfused": ("ns3d", (64, 32, 32), (4, 2), "unfused"),
 }
 
 
@@ -29,10 +35,17 @@ def main(name):
     solver, n, world, p2p = CASES[name]
     u0 = ic.initial_state(solver, n, seed=3)
     dt = ic.cfl_dt(solver, n, u0)
-    kw = {"world": world} if world > 1 else {}
+    pencil = isinstance(world, tuple)
+    kw = {"pencil": world} if pencil else {"world": world} if world > 1 else {}
     s = api.Simulation(solver, n, 1e-3, dt, **kw)
-    if p2p:
+    if p2p is True:
         s.enable_p2p()
+    elif p2p == "packed":
+        s.set_overlap(2)
+    elif p2p == "unfused":
+        s.set_overlap(3)
+    if pencil:
+        world = world[0] * world[1]
     s.set_state(u0)
     s.step(2)
     if world == 1:
