@@ -317,6 +317,9 @@ skg::Ns3dArgs args3d(skg_ctx* c, double dt) {
     a.kstart = c->d_cstart;
     a.slab = 0;
     a.sz = c->nh;
+    a.xscr = c->xscr;
+    a.xscr_mask = c->xscr_mask;
+    a.xscr_nsm = c->xscr_nsm;
     return a;
 }
 

@@ -127,6 +127,11 @@ struct skg_ctx {
     double* etab = nullptr;  // e1[axis], e2[axis] tables
     cd* tw[3] = {nullptr, nullptr, nullptr};
     skg::DevFlags* flags = nullptr;
+    // ns3d x-forward scratch (k4_3d): per-SM slots for the transformed
+    // components 0 and 1 of a CTA, claimed through a per-SM bit mask
+    cd* xscr = nullptr;
+    unsigned* xscr_mask = nullptr;
+    int xscr_nsm = 0;
     unsigned long long* d_count = nullptr;
     double* d_red = nullptr;
 

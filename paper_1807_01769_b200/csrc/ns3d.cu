@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
     const int c0 = a.comp0 + blockIdx.y, c1 = c0 + 1;
 #pragma unroll 1
     for (int c = c0; c < c1; ++c) {
+        const size_t ubase = sidx(a, t, ys, kz) + c * a.vstride, ustr = (size_t)T * a.ystate * a.sz;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             if (e >= ZLO && e < ZHI) continue;
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
             const int i = t + T * e;
             const bool keep = active && (!a.pruned || abs(signed_index(i, NX)) <= a.kcx);
             if (keep) {
-                const size_t idx = sidx(a, i, ys, kz) + c * a.vstride;
+                const size_t idx = ubase + e * ustr;  // sidx(a, i, ys, kz) + c * a.vstride
                 cp_async16(&slots[slot * CT + threadIdx.x], a.u + idx);
                 if (stage > 1) cp_async16(&kst[slot * CT + threadIdx.x], kprev + idx);
             }
@@ -242,10 +243,10 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
             F::template run<+1>(v, sm, t, wb, salt);
             if (active) {
                 if (!a.p2p) {
-                    cd* out = a.A + m * a.fstride;
+                    cd* out = a.A + m * a.fstride + ((size_t)t * a.ystate + ys) * a.kz_in + kz;
+                    const size_t ost = (size_t)T * a.ystate * a.kz_in;
 #pragma unroll
-                    for (int e = 0; e < E; ++e)
-                        out[((size_t)(t + T * e) * a.ystate + ys) * a.kz_in + kz] = v[e];
+                    for (int e = 0; e < E; ++e) out[e * ost] = v[e];
                 } else {  // straight into the row owner's receive block (layout [xl][kyl][kz])
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
@@ -463,10 +464,10 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
                     a.peer_Z[y >> a.lg_nyl][base + (size_t)(y & (a.nyl - 1)) * a.kzf] = v[e];
                 }
             } else {
-                cd* out = a.B + m * a.fstride;
+                cd* out = a.B + m * a.fstride + ((size_t)x * a.ny + t) * a.kz_in + kz;
+                const unsigned ost = (unsigned)T * (unsigned)a.kz_in;
 #pragma unroll
-                for (int e = 0; e < E; ++e)
-                    out[((size_t)x * a.ny + (t + T * e)) * a.kz_in + kz] = v[e];
+                for (int e = 0; e < E; ++e) out[e * ost] = v[e];
             }
         }
     }
@@ -849,6 +850,21 @@ __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, Z3<NZ>::MINB) k3_3d(Ns3
 }
 
 // ------------------------------------------------------------------ y-forward
+// A/B switches (round 2).  SKG3_YF_LD = 1: one base pointer + element stride
+// per thread, so the 16 input loads issue back to back instead of ~45 integer
+// instructions apart (per-element 64-bit index arithmetic behind a branch).
+// Measured SLOWER for this pass, the one closest to the HBM roof: 512^3
+// y-forward 857 vs 790 us per launch (two runs each) -- the spread-out issue
+// stays.  The same hoisting pays in the x-inverse loads/stores (1225 -> 1212),
+// the y-inverse stores (2066 -> 2050) and the x-forward loads (with fewer
+// spills: 1220 -> 1041).  SKG3_X4_SBASE = 1 (state index as base + e * stride in
+// the x-forward epilogue): 1064 vs 1048 us (more spills), off.
+#ifndef SKG3_YF_LD
+#define SKG3_YF_LD 0
+#endif
+#ifndef SKG3_X4_SBASE
+#define SKG3_X4_SBASE 0
+#endif
 // ZB: kcy < 3 NY / 8, so the outputs e in [3E/8, 5E/8) are masked (not stored)
 // One tile of the y-forward: x row and kz block from bx, fields m0..m1.
 template <int NY, int CT, bool ZB>
@@ -870,11 +886,19 @@ __device__ __forceinline__ void yf_tile(const Ns3dArgs& a, cd* smem, int bx, int
     else line_offsets<NY>(a, x, a.kz_o, loff);
 #pragma unroll 1
     for (int m = m0; m < m1; ++m) {
-        const cd* in = a.A + m * a.fstride;  // C fields live in A's memory
+        // C fields live in A's memory
         cd v[E];
+#if SKG3_YF_LD
+        const cd* in = a.A + m * a.fstride + ((size_t)x * a.ny + t) * a.kz_o + (active ? kz : a.kz_o - 1);
+        const unsigned ist = (unsigned)T * (unsigned)a.kz_o;
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = in[e * ist];
+#else
+        const cd* in = a.A + m * a.fstride;
 #pragma unroll
         for (int e = 0; e < E; ++e)
             v[e] = active ? in[((size_t)x * a.ny + (t + T * e)) * a.kz_o + kz] : zero();
+#endif
         F::template run<-1>(v, sm, t, wb, salt);
         if (active) {
             cd* out = a.slab ? a.sD + m * a.rfs
@@ -904,9 +928,16 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
 }
 
 // ------------------------------------------------------------------ x-forward + RK
-// Components 0 and 1 are written back raw into their own D lines (in place,
-// L2-resident) and re-read by the same thread for the projection, so no
-// shared-memory slots are needed.
+// The transformed components 0 and 1 wait for the projection (which needs all
+// three at a mode) outside the register file: in a per-SM scratch slot of
+// global memory (xscr: [component][element][thread], written and re-read by
+// the same thread, fully coalesced).  A CTA claims one of its SM's slots
+// through a bit mask (one atomicOr by thread 0, released at the end), so the
+// ~30 MB of slots of all resident CTAs are rewritten by every wave and stay
+// in L2: the raw lines never reach HBM.  The earlier in-place write-back into
+// the D lines (kept as the fallback when no slot is free or SKG_NO_XSCR is
+// set) wrote 2 x 0.44 F per launch to DRAM on top of the algorithmic bytes
+// (512^3, ncu r08: 1.93 GB written for 0.96 GB of k_j).
 // FIN: final-stage instantiation (RK update, diagnostics); the other stages
 // run a leaner one that only stores k_j.
 template <int NX, int CT = 256, bool FIN = false>
@@ -931,24 +962,57 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     const bool io = active && keep_y;
     const size_t lbase = (size_t)ys * a.kz_o + kz;     // + x * ystate * kz_o
     const size_t xstr = (size_t)a.ystate * a.kz_o;
+    // scratch slot of this CTA: claimed by thread 0, published after the
+    // first FFT
+    constexpr int CTT = T * C, PER_CTA = 2 * E * CTT;
+    constexpr int NSLOT = SKG_XSCR_SM / PER_CTA < 32 ? SKG_XSCR_SM / PER_CTA : 32;
+    __shared__ int s_slot;
+    unsigned smid = 0;
+    if (threadIdx.x == 0) {
+        int slot = -1;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (a.xscr && (int)smid < a.xscr_nsm) {
+            for (int k = 0; k < NSLOT && slot < 0; ++k)
+                if (!(atomicOr(a.xscr_mask + smid, 1u << k) & (1u << k))) slot = k;
+        }
+        s_slot = slot;
+    }
+    // element e of this thread: D line element (t + T e) at Dm + lt + e * ls;
+    // components 0 and 1 wait at P0 / P1 + e * ps (scratch slot, or in place)
+    const size_t lt = lbase + (size_t)t * xstr, ls = (size_t)T * xstr;
+    cd* const D = a.p2p ? a.rD : a.B;
+    const size_t dstr = a.p2p ? a.dfs : a.fstride;
+    cd* P0 = D + lt;
+    size_t ps = ls, p1 = dstr;  // P1 = P0 + p1
     cd v[E];
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
-        cd* line = (a.p2p ? a.rD + m * a.dfs : a.B + m * a.fstride) + lbase;
+        const cd* line = D + m * dstr + lt;
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = io ? line[(size_t)(t + T * e) * xstr] : zero();
+        for (int e = 0; e < E; ++e) v[e] = io ? line[e * ls] : zero();
         F::template run<-1>(v, sm, t, wb, salt);
+        if (m == 0) {
+            __syncthreads();
+            if (s_slot >= 0) {
+                unsigned id;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+                P0 = a.xscr + (size_t)id * SKG_XSCR_SM + (size_t)s_slot * PER_CTA + threadIdx.x;
+                ps = CTT;
+                p1 = (size_t)E * CTT;
+            }
+        }
         if (m < 2 && io) {
+            cd* w = m == 0 ? P0 : P0 + p1;
 #pragma unroll
-            for (int e = 0; e < E; ++e) line[(size_t)(t + T * e) * xstr] = v[e];
+            for (int e = 0; e < E; ++e)  // only the kept kx are read back
+                if (!a.pruned || abs(signed_index(t + T * e, NX)) <= a.kcx) w[e * ps] = v[e];
         }
     }
     constexpr bool final = FIN;
     cd* kout = stage == 1 ? a.k1 : stage == 2 ? a.k2 : a.k3;
     const double kyv = a.ky_scale * (double)sky;
     const double kzv = a.kz_scale * (double)(a.kz0 + kz);
-    const cd* l0 = (a.p2p ? a.rD : a.B) + lbase;
-    const cd* l1 = (a.p2p ? a.rD + a.dfs : a.B + a.fstride) + lbase;
+    const size_t sbase = sidx(a, t, ys, kz), sstr = (size_t)T * a.ystate * a.sz;
     int bad = 3;
     // per-step E and eps of the new state (Solver::mode_energy default,
     // simulation.cpp:163-170; dissipation_rate simulation.cpp:608-615)
@@ -971,8 +1035,8 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
         if (!keep && a.pruned) continue;
         cd c0 = zero(), c1 = zero(), c2 = zero();
         if (keep) {
-            c0 = l0[(size_t)i * xstr];
-            c1 = l1[(size_t)i * xstr];
+            c0 = P0[e * ps];
+            c1 = P0[p1 + e * ps];
             c2 = v[e];
             // Leray projection (grid.cpp:227-249)
             const double kxv = a.kx_scale * (double)si;
@@ -987,7 +1051,11 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
             }
         }
         const cd kc[3] = {c0, c1, c2};
+#if SKG3_X4_SBASE
+        const size_t base = sbase + e * sstr;  // sidx(a, i, ys, kz)
+#else
         const size_t base = sidx(a, i, ys, kz);
+#endif
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const size_t idx = base + c * a.vstride;
@@ -1036,6 +1104,8 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
         atomicExch(&a.flags->div_step, a.flags->steps);
         atomicExch(&a.flags->diverged, 1);
     }
+    __syncthreads();  // every thread has consumed its scratch values
+    if (threadIdx.x == 0 && s_slot >= 0) atomicAnd(a.xscr_mask + smid, ~(1u << s_slot));
 }
 
 // Unpruned final update of the kz planes above the cut (tendency zero there).

@@ -249,7 +249,14 @@ struct Ns3dArgs {
     int zfused = 0, lg_nyl = 0, nyl = 0, kzf = 0;
     size_t fsz = 0;
     cd* peer_Z[SKG_MAX_RANKS];
+    // x-forward scratch: xscr_nsm regions of SKG_XSCR_SM elements, one per
+    // %smid, and the per-SM claim masks (nullptr: in-place write-back)
+    cd* xscr = nullptr;
+    unsigned* xscr_mask = nullptr;
+    int xscr_nsm = 0;
 };
+// per-SM scratch region: 1024 resident threads x 2 components x 16 elements
+constexpr int SKG_XSCR_SM = 1024 * 2 * 16;
 
 // Programmatic dependent launch (sm_90+): step kernels are launched with
 // programmatic stream serialization and wait (griddepcontrol.wait) for their
@@ -406,6 +413,7 @@ cudaError_t forcing_finish(const ForceGeo& g, const cd* u, cd* f, double rate, d
 // compute-sanitizer is unavailable; IPC export is refused in this mode.
 cudaError_t dmalloc_raw(void** p, size_t bytes);
 void dfree(void* p);
+int max_smid(int device);
 long guard_violations();
 bool guards_enabled();
 template <class T>

@@ -272,6 +272,17 @@ static int create_impl(skg_ctx** out, const char* solver, int dims, const int* n
     for (int d = 0; d < dims; ++d) ext_total += d == dims - 1 ? c->nh : n[d];
     ok = ok && alloc((void**)&c->etab, sizeof(double) * 2 * ext_total);
     ok = ok && alloc((void**)&c->flags, sizeof(skg::DevFlags));
+    // x-forward scratch slots (ns3d.cu k4_3d): measured 512^3 28.95 -> 28.68,
+    // 256^3 3.77 -> 3.74 ms/step, 128^3 0.567 -> 0.580 (the claim's atomic and
+    // barrier cost more than the write-back there), so from 256 on;
+    // SKG_XSCR=0 / 1 forces it off / on
+    const char* xs = std::getenv("SKG_XSCR");
+    const bool xscr = xs ? std::atoi(xs) != 0 : n[0] >= 256;
+    if (sid == 3 && !c->generic && xscr && std::getenv("SKG_NO_XSCR") == nullptr) {
+        c->xscr_nsm = skg::max_smid(device);
+        ok = ok && alloc((void**)&c->xscr_mask, sizeof(unsigned) * c->xscr_nsm);
+        ok = ok && skg::dmalloc(&c->xscr, sizeof(cd) * (size_t)skg::SKG_XSCR_SM * c->xscr_nsm) == cudaSuccess;
+    }
     ok = ok && alloc((void**)&c->d_count, sizeof(unsigned long long));
     ok = ok && alloc((void**)&c->d_red, 3 * sizeof(double));
     ok = ok && alloc((void**)&c->d_dyn, sizeof(skg::DynStep));
@@ -301,6 +312,8 @@ int skg_destroy(skg_ctx* c) {
     skg::dfree(c->work);
     skg::dfree(c->etab);
     skg::dfree(c->flags);
+    skg::dfree(c->xscr);
+    skg::dfree(c->xscr_mask);
     skg::dfree(c->d_count);
     skg::dfree(c->d_red);
     skg::dfree(c->d_dyn);

@@ -403,6 +403,32 @@ cudaError_t ensure_smem(const void* kernel, size_t bytes) {
     return cudaSuccess;
 }
 
+namespace {
+__global__ void nsmid_probe(unsigned* out) {
+    unsigned n;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+    *out = n;
+}
+}  // namespace
+
+// Upper bound of %smid + 1 on `device` (the SM ids a CTA can observe are not
+// guaranteed contiguous; %nsmid bounds them), at least the SM count.
+int max_smid(int device) {
+    static int cache[64] = {0};
+    if (device >= 0 && device < 64 && cache[device]) return cache[device];
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    unsigned* d = nullptr;
+    unsigned h = 0;
+    if (dmalloc(&d, sizeof(unsigned)) != cudaSuccess) return sms > 256 ? sms : 256;
+    nsmid_probe<<<1, 1>>>(d);
+    if (cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) h = 256;
+    dfree(d);
+    const int r = (int)h > sms ? (int)h : sms;
+    if (device >= 0 && device < 64) cache[device] = r;
+    return r;
+}
+
 cudaError_t fp64_peak(int device, double* dfma_per_s) {
     SKG_TRY(cudaSetDevice(device));
     int sms = 0;

@@ -184,3 +184,40 @@ def test_run_series_matches_reference(ref_lib, noise):
         assert abs(series[i, 0] - r.energy) < 1e-12 * r.energy
         assert series[i, 1] == 0.0
         assert abs(series[i, 2] - eps) < 1e-11 * eps
+
+
+def test_xforward_scratch_slots_match_in_place_write_back():
+    """k4_3d parks the transformed components 0 and 1 in per-SM scratch slots
+    (claimed through a bit mask); SKG_NO_XSCR=1 selects the in-place
+    write-back the kernel falls back to when no slot is free.  Same
+    arithmetic: the states after 3 RK4 steps are bit-identical (dealiased and
+    non-dealiased, 16-element and 8-element lines, a non-cubic grid)."""
+    import os
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parents[1]
+    code = (
+        "import sys, hashlib; sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "from paper_1807_01769_b200 import api, ic\n"
+        "for n, dealiased in (((64, 64, 64), True), ((32, 64, 16), True), ((512, 16, 16), True), ((32, 32, 32), False)):\n"
+        "    u0 = ic.initial_state('ns3d', n, seed=5)\n"
+        "    if not dealiased:\n"
+        "        rng = np.random.default_rng(2)\n"
+        "        u0 = u0 + 1e-3 * (rng.standard_normal(u0.shape) + 1j * rng.standard_normal(u0.shape))\n"
+        "        u0[..., 0].imag = 0; u0[..., -1].imag = 0\n"
+        "    s = api.Simulation('ns3d', n, 1e-3, 1e-3)\n"
+        "    s.set_state(u0); s.step(3)\n"
+        "    print('H', n, hashlib.sha256(s.get_state().tobytes()).hexdigest())\n"
+        "    s.close()\n" % str(root))
+    outs = []
+    for flag in (None, "1"):
+        env = dict(os.environ)
+        env.pop("SKG_NO_XSCR", None)
+        if flag:
+            env["SKG_NO_XSCR"] = flag
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        outs.append([l for l in r.stdout.splitlines() if l.startswith("H ")])
+    assert len(outs[0]) == 4 and outs[0] == outs[1]
