@@ -3,6 +3,8 @@
 // the state I/O between the reference layout and the internal layouts.
 #include "host_ctx.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace skh {
 
 // NCCL is loaded on first use (multi-GPU contexts only) instead of at link
@@ -102,9 +104,29 @@ void timing_hook(void* user, int cls, int phase, double bytes) {
     }
 }
 
+// SKG_NVTX=1: an NVTX range around every pass of the step (named by kernel
+// class, visible in Nsight Systems / ncu --nvtx), on top of the per-class
+// CUDA-event timing when that is on.  nvtx3 is header-only and a no-op
+// without an attached tool.
+void nvtx_hook(void* user, int cls, int phase, double bytes) {
+    static const char* const names[6] = {"skg x_inverse", "skg physical", "skg x_forward_rk",
+                                         "skg y_inverse", "skg exchange", "skg y_forward"};
+    auto* c = static_cast<skg_ctx*>(user);
+    if (phase == 0) nvtxRangePushA(names[cls >= 0 && cls < 6 ? cls : 1]);
+    if (c->timing) timing_hook(user, cls, phase, bytes);
+    if (phase != 0) nvtxRangePop();
+}
+
 skg::LaunchHook hook_of(skg_ctx* c) {
+    static const bool nvtx = [] {
+        const char* e = std::getenv("SKG_NVTX");
+        return e && std::atoi(e) != 0;
+    }();
     skg::LaunchHook h;
-    if (c->timing) {
+    if (nvtx) {
+        h.fn = nvtx_hook;
+        h.user = c;
+    } else if (c->timing) {
         h.fn = timing_hook;
         h.user = c;
     }
