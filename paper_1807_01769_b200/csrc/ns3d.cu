@@ -36,6 +36,21 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Inter-pass intermediates are written once and read once by the next
+// kernel, gigabytes later: SKG3_STCS = 1 stores them with the streaming
+// (evict-first) policy so they do not displace the L2-resident reuse sets
+// (scratch slots, secondary fields, twiddle tables).  A/B macro.
+#ifndef SKG3_STCS
+#define SKG3_STCS 0
+#endif
+__device__ __forceinline__ void st_stream(cd* p, cd v) {
+#if SKG3_STCS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 // RK stage state from loaded u and previous k (time_stepping.cpp:128-170).
 __device__ __forceinline__ cd stage_combine3(const Ns3dArgs& a, int stage, int i, int ky, int kz,
                                              cd u, cd k) {
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(CB, Strided<NX, CB>::MINB) k1_3d(Ns3dArgs a, i
                     cd* out = a.A + m * a.fstride + ((size_t)t * a.ystate + ys) * a.kz_in + kz;
                     const size_t ost = (size_t)T * a.ystate * a.kz_in;
 #pragma unroll
-                    for (int e = 0; e < E; ++e) out[e * ost] = v[e];
+                    for (int e = 0; e < E; ++e) st_stream(out + e * ost, v[e]);
                 } else {  // straight into the row owner's receive block (layout [xl][kyl][kz])
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
@@ -467,7 +482,7 @@ __device__ __forceinline__ void y_inv_tile(const Ns3dArgs& a, cd* smem, int bx, 
                 cd* out = a.B + m * a.fstride + ((size_t)x * a.ny + t) * a.kz_in + kz;
                 const unsigned ost = (unsigned)T * (unsigned)a.kz_in;
 #pragma unroll
-                for (int e = 0; e < E; ++e) out[e * ost] = v[e];
+                for (int e = 0; e < E; ++e) st_stream(out + e * ost, v[e]);
             }
         }
     }
@@ -613,8 +628,8 @@ __device__ __forceinline__ void z_store_pair(const Ns3dArgs& a, const cd* v, cd*
                 if (k >= a.kz_o) break;
                 const cd zk = v[e];
                 const cd zm = t == 0 ? (e == 0 ? v[0] : v[E - e]) : sm[(E - 1 - e - HI) * T + tp];
-                o0[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-                o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+                st_stream(o0 + k, mk((zk.x + zm.x) * h, (zk.y - zm.y) * h));
+                st_stream(o1 + k, mk((zk.y + zm.y) * h, (zm.x - zk.x) * h));
             }
         }
     } else {
@@ -625,8 +640,8 @@ __device__ __forceinline__ void z_store_pair(const Ns3dArgs& a, const cd* v, cd*
             for (int k = t; k < a.kz_o; k += T) {
                 const cd zk = sm[F::pad(k)];
                 const cd zm = sm[F::pad((NZ - k) & (NZ - 1))];
-                o0[k] = mk((zk.x + zm.x) * h, (zk.y - zm.y) * h);
-                o1[k] = mk((zk.y + zm.y) * h, (zm.x - zk.x) * h);
+                st_stream(o0 + k, mk((zk.x + zm.x) * h, (zk.y - zm.y) * h));
+                st_stream(o1 + k, mk((zk.y + zm.y) * h, (zm.x - zk.x) * h));
             }
         }
     }
@@ -909,7 +924,7 @@ __device__ __forceinline__ void yf_tile(const Ns3dArgs& a, cd* smem, int bx, int
                 const int lo = loff[t + T * e];
                 if (lo >= 0 && abs(signed_index(t + T * e, NY)) <= a.kcy) {  // masked: never read
                     if (a.p2p) a.peer_D[lown[t + T * e]][m * a.dfs + (size_t)lo + kz] = v[e];
-                    else out[(size_t)lo + kz] = v[e];
+                    else st_stream(out + (size_t)lo + kz, v[e]);
                 }
             }
         }
@@ -928,6 +943,36 @@ __global__ void __launch_bounds__(CT, Strided<NY, CT>::MINB) k2f_3d(Ns3dArgs a) 
 }
 
 // ------------------------------------------------------------------ x-forward + RK
+// SKG3_XSCR_HINT = 1: scratch-slot stores and loads carry an L2 evict_last
+// policy (512^3 x-forward 1048 -> 1015 us per launch, step 28.58 -> 28.42 ms;
+// 256^3 3.700 -> 3.695)
+#ifndef SKG3_XSCR_HINT
+#define SKG3_XSCR_HINT 1
+#endif
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_keep(cd* p, cd v, unsigned long long pol) {
+#if SKG3_XSCR_HINT
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+#else
+    (void)pol;
+    *p = v;
+#endif
+}
+__device__ __forceinline__ cd ld_keep(const cd* p, unsigned long long pol) {
+#if SKG3_XSCR_HINT
+    cd v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol) : "memory");
+    return v;
+#else
+    (void)pol;
+    return *p;
+#endif
+}
 // The transformed components 0 and 1 wait for the projection (which needs all
 // three at a mode) outside the register file: in a per-SM scratch slot of
 // global memory (xscr: [component][element][thread], written and re-read by
@@ -984,6 +1029,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
     const size_t dstr = a.p2p ? a.dfs : a.fstride;
     cd* P0 = D + lt;
     size_t ps = ls, p1 = dstr;  // P1 = P0 + p1
+    const unsigned long long pol = SKG3_XSCR_HINT ? l2_keep_policy() : 0ull;
     cd v[E];
 #pragma unroll 1
     for (int m = 0; m < 3; ++m) {
@@ -1005,7 +1051,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
             cd* w = m == 0 ? P0 : P0 + p1;
 #pragma unroll
             for (int e = 0; e < E; ++e)  // only the kept kx are read back
-                if (!a.pruned || abs(signed_index(t + T * e, NX)) <= a.kcx) w[e * ps] = v[e];
+                if (!a.pruned || abs(signed_index(t + T * e, NX)) <= a.kcx) st_keep(w + e * ps, v[e], pol);
         }
     }
     constexpr bool final = FIN;
@@ -1035,8 +1081,8 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
         if (!keep && a.pruned) continue;
         cd c0 = zero(), c1 = zero(), c2 = zero();
         if (keep) {
-            c0 = P0[e * ps];
-            c1 = P0[p1 + e * ps];
+            c0 = ld_keep(P0 + e * ps, pol);
+            c1 = ld_keep(P0 + p1 + e * ps, pol);
             c2 = v[e];
             // Leray projection (grid.cpp:227-249)
             const double kxv = a.kx_scale * (double)si;
@@ -1062,7 +1108,7 @@ __global__ void __launch_bounds__(CT, Strided<NX, CT>::MINB) k4_3d(Ns3dArgs a, i
             cd kv = kc[c];
             if (a.force && keep) kv = add(kv, a.force[idx]);  // forcing addend (simulation.cpp:544-547)
             if (!final) {
-                kout[idx] = kv;
+                st_stream(kout + idx, kv);
                 continue;
             }
             const cd u = a.u[idx];
