@@ -24,7 +24,7 @@ def test_no_guard_zone_writes():
         "for c in sorted(sc.CASES): sc.main(c)\n"
         "print('violations', api.guard_violations())\n"
         "assert api.guard_violations() == 0\n" % (str(ROOT), str(ROOT / "tools")))
-    env = dict(os.environ, SKG_GUARD="1")
+    env = dict(os.environ, SKG_GUARD="1", SKG_XSCR="1")  # x-forward scratch slots on at every size
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]

@@ -188,7 +188,7 @@ def test_run_series_matches_reference(ref_lib, noise):
 
 def test_xforward_scratch_slots_match_in_place_write_back():
     """k4_3d parks the transformed components 0 and 1 in per-SM scratch slots
-    (claimed through a bit mask); SKG_NO_XSCR=1 selects the in-place
+    (claimed through a bit mask); SKG_XSCR=0 selects the in-place
     write-back the kernel falls back to when no slot is free.  Same
     arithmetic: the states after 3 RK4 steps are bit-identical (dealiased and
     non-dealiased, 16-element and 8-element lines, a non-cubic grid)."""
@@ -212,11 +212,10 @@ def test_xforward_scratch_slots_match_in_place_write_back():
         "    print('H', n, hashlib.sha256(s.get_state().tobytes()).hexdigest())\n"
         "    s.close()\n" % str(root))
     outs = []
-    for flag in (None, "1"):
+    for flag in ("1", "0"):  # slots forced on (default: from nx = 256) / off
         env = dict(os.environ)
         env.pop("SKG_NO_XSCR", None)
-        if flag:
-            env["SKG_NO_XSCR"] = flag
+        env["SKG_XSCR"] = flag
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
         outs.append([l for l in r.stdout.splitlines() if l.startswith("H ")])
