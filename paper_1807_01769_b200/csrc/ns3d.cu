@@ -760,13 +760,22 @@ __device__ __forceinline__ void z_tile_s(const Ns3dArgs& a, cd* smem, long long 
         bulk_g2s(stg, FP[k % 3] + row, bytes, mb);
         bulk_g2s(stg + KZS, FQ[k % 3] + row, bytes, mb);
     };
+    // divergence flag (cta_diverged): loaded here, checked once the first
+    // bulk copy is in flight, so its round trip overlaps the copy's (the
+    // wait for the first pair was 55% of the z pass's long-scoreboard
+    // samples, profiles/r27)
+    const int dflag = *reinterpret_cast<const volatile int*>(&a.flags->diverged);
     if (t == 0) mbar_init(mb, 1);
     line_sync<T>(bar);
     if (active && t == 0) {
+        issue(0);
         const size_t rb = sizeof(cd) * 2 * a.kz_in;  // the rest of the row pair into L2
         for (int f = 0; f < 6; ++f)
             if (f != 2 && f != 3) l2_prefetch(B + f * fs + (size_t)r0 * a.kz_in, rb, 0, 1);
-        issue(0);
+    }
+    if (__syncthreads_or(dflag) != 0) {  // frozen state: let the copy land, then leave
+        if (active) mbar_wait(mb, 0);
+        return;
     }
     unsigned phase = 0;
     // packed spectrum of pair k from the stage; then the stage is released
@@ -859,9 +868,12 @@ template <int NZ, bool CFL, bool ZB>
 __global__ void __launch_bounds__(Z3<NZ>::T * Z3<NZ>::G, Z3<NZ>::MINB) k3_3d(Ns3dArgs a) {
     extern __shared__ cd smem[];
     pdl_wait();
-    if (cta_diverged(a.flags)) return;
-    if constexpr (Z3<NZ>::STG) z_tile_s<NZ, CFL, ZB>(a, smem, blockIdx.x);
-    else z_tile<NZ, CFL, ZB>(a, smem, blockIdx.x);
+    if constexpr (Z3<NZ>::STG) {
+        z_tile_s<NZ, CFL, ZB>(a, smem, blockIdx.x);  // checks the divergence flag itself
+    } else {
+        if (cta_diverged(a.flags)) return;
+        z_tile<NZ, CFL, ZB>(a, smem, blockIdx.x);
+    }
 }
 
 // ------------------------------------------------------------------ y-forward
